@@ -1,0 +1,223 @@
+/*
+ * dci.h — C ABI of libdci, the B200-native (sm_100a) hot path of DCI (arXiv 2503.01281):
+ * dual-cache mini-batch preparation for sampled GNN inference.
+ *
+ * Citation key: P:n = PAPER.md line n (the paper's LaTeX, /root/reference at build time);
+ * O-k / Ck = oracle definition / reading k of DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns dci_status; no C++ exception crosses the ABI.  On failure a
+ *    thread-local message is available from dci_last_error().
+ *  - "host" pointers are ordinary CPU memory; "device" pointers are CUDA device memory of
+ *    the context's device (e.g. torch tensors' data_ptr()).  `stream` is a cudaStream_t
+ *    passed as void* (NULL = legacy default stream).
+ *  - Sizes are element counts unless named *_bytes.  Node ids are int32 (N < 2^31).
+ *  - A context belongs to one device.  Calls on one context are not thread-safe, except
+ *    that distinct workspaces may run dci_sample_gather concurrently on distinct streams.
+ *  - Asynchronous calls (dci_sample_gather*) never synchronise the host.  Per-batch data
+ *    errors (bad seed id, duplicate seed) are reported through the device status word of
+ *    dci_batch_out, not the return value.
+ */
+#ifndef DCI_H_
+#define DCI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DCI_VERSION 100          /* 1.0.0 */
+#define DCI_MAX_LAYERS 8         /* L <= 8 hops */
+#define DCI_MAX_FANOUT 32        /* per-hop fan-out 1..32 (warp-register selection) */
+
+typedef enum dci_status {
+  DCI_OK = 0,
+  DCI_EINVAL = 1,  /* bad argument (null pointer, size, fan-out, layout) */
+  DCI_ESTATE = 2,  /* call not allowed in the context's current state */
+  DCI_ECUDA = 3,   /* CUDA runtime error (message in dci_last_error) */
+  DCI_ENOMEM = 4,  /* device or pinned host allocation failed */
+  DCI_ESEED = 5,   /* a seed id is outside [0, N)                (device status word) */
+  DCI_EDUP = 6,    /* a seed id appears twice in one batch       (device status word) */
+  DCI_ECAP = 7,    /* an output buffer is smaller than dci_output_bounds requires */
+  DCI_ERANGE = 8   /* a count/size exceeds a documented limit */
+} dci_status;
+
+typedef struct dci_ctx dci_ctx;
+typedef struct dci_workspace dci_workspace;
+
+/* Context lifecycle states (dci_cache_info.state). */
+enum { DCI_STATE_LOADED = 1, DCI_STATE_FILLED = 2 };
+
+/* --------------------------------------------------------------------------------------
+ * dci_load_graph — S0.  P:130-131 (CSC: Col_ptr / Row_index), P:147 + P:170 (host graph
+ * reached through UVA on a miss).
+ *  indptr  host int64[N+1]  CSC column pointers (Col_ptr): indptr[0]=0, non-decreasing,
+ *                           indptr[N]=E.  Node v's in-neighbours are
+ *                           indices[indptr[v] .. indptr[v+1]).
+ *  indices host int32[E]    in-neighbour ids (Row_index), each in [0, N).
+ *  feats   host fp32[N*D]   row-major node features.
+ *  The library copies indices and feats into its own pinned, device-mapped host buffers
+ *  (feature rows padded to pitch = round_up(D, 4) floats so every row is 16-byte aligned;
+ *  the pad is zero) and builds the per-node device directory.  The caller's buffers may
+ *  be freed on return.  Validates the CSC invariants (O(E) host pass) -> DCI_EINVAL.
+ *  flags: reserved, pass 0.
+ *  Limits: 1 <= N < 2^31, 0 <= E < 2^40, 1 <= D.  *out owns all device and pinned memory.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const int64_t* indptr,
+                          const int32_t* indices, const float* feats, int32_t D, uint32_t flags);
+
+dci_status dci_destroy(dci_ctx* ctx);
+
+/* --------------------------------------------------------------------------------------
+ * Output of one mini-batch (all pointers are DEVICE memory owned by the caller).
+ * Hop h (0 = the seeds' hop) samples dst = F_h with fan-out fanouts[L-1-h] (DGL order,
+ * C3) and produces the block CSR (bptr[h], bsrc[h]) over dst = F_h, src ids local to
+ * F_{h+1}.  frontier holds F_L; every F_h is its prefix of length sizes[h] (C2, C6).
+ *  frontier  int32[frontier_cap]       global node ids, first-occurrence order (O-6)
+ *  sizes     int64[L+1]                |F_0| .. |F_L|
+ *  bptr[h]   int32[hop_cap[h] + 1]     block row pointers (bptr[h][0] = 0)
+ *  bsrc[h]   int32[bsrc_cap[h]]        block column ids (local ids into F_{h+1})
+ *  X         fp32[frontier_cap * ldx]  X[i][0..D) = feats[F_L[i]] (O-7); columns
+ *                                      [D, pitch) receive the zero pad when ldx >= pitch;
+ *                                      may be NULL (sampling only)
+ *  counters  uint64[4]                 {adj_hit, adj_miss, feat_hit, feat_miss} of this
+ *                                      batch (O-9), overwritten
+ *  status    int32[1]                  DCI_OK or DCI_ESEED / DCI_EDUP, overwritten
+ * Capacities must be >= the values dci_output_bounds returns (checked on the host ->
+ * DCI_ECAP), so the device path never truncates.
+ * ------------------------------------------------------------------------------------ */
+typedef struct dci_batch_out {
+  int32_t* frontier;
+  int64_t frontier_cap;
+  int64_t* sizes;
+  int32_t* bptr[DCI_MAX_LAYERS];
+  int32_t* bsrc[DCI_MAX_LAYERS];
+  int64_t hop_cap[DCI_MAX_LAYERS];
+  int64_t bsrc_cap[DCI_MAX_LAYERS];
+  float* X;
+  int64_t ldx;
+  uint64_t* counters;
+  int32_t* status;
+} dci_batch_out;
+
+/* Worst-case sizes for a batch of B seeds: frontier_caps[h] = min(N, B*prod_{j<h}(1+f_j))
+ * for h = 0..L (host int64[L+1]), bsrc_caps[h] = frontier_caps[h] * f_h (host int64[L]),
+ * feature pitch in floats.  Pure host arithmetic. */
+dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanouts, int32_t L,
+                             int64_t* frontier_caps, int64_t* bsrc_caps, int32_t* pitch);
+
+/* --------------------------------------------------------------------------------------
+ * Workspace: per-stream scratch for one in-flight batch (node->position table of N int32,
+ * candidate / count arrays, scan tile state, hit/miss lists, events, an auxiliary stream).
+ * Sized for batches of up to max_batch seeds with fan-outs up to max_fanouts[.] (L hops).
+ * Use one workspace per concurrently in-flight batch.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* max_fanouts, int32_t L,
+                                dci_workspace** out);
+dci_status dci_workspace_destroy(dci_workspace* ws);
+
+/* --------------------------------------------------------------------------------------
+ * dci_sample_gather — S5..S8, the per-batch hot loop.  P:116-117, P:128 (sampled
+ * inference), P:170 (hit -> GPU memory, miss -> host memory through UVA)
+ * (adjacency prefix-hit rule), P:200 (feature cache lookup).
+ *  seeds  device int32[B] (unique ids in [0, N)); B >= 0, B <= the workspace's max_batch.
+ *  fanouts host int32[L] (DGL order, each 1..32, each <= the workspace's max_fanouts).
+ *  seed   64-bit sampling seed; draws are Philox(ctr=(node, slot, hop, pass=0),
+ *         key=seed) (O-2), so results do not depend on batch composition or GPU count.
+ * Asynchronous on `stream`; enqueues only device work (no host sync, no allocation).
+ * Allowed in both states: before dci_fill it samples the original CSC with no cache.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B,
+                             const int32_t* fanouts, int32_t L, uint64_t seed, const dci_batch_out* out,
+                             void* stream);
+
+/* End-to-end variant: seeds_host is HOST memory (pinned for full overlap); the call
+ * enqueues the host->device copy of the seeds, the batch, and device->host copies of
+ * sizes (int64[L+1]), counters (uint64[4]) and status (int32) into the given host buffers.
+ * Asynchronous: the host buffers are valid after the stream is synchronised. */
+dci_status dci_sample_gather_host(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds_host, int32_t B,
+                                  const int32_t* fanouts, int32_t L, uint64_t seed, const dci_batch_out* out,
+                                  int64_t* sizes_host, uint64_t* counters_host, int32_t* status_host,
+                                  void* stream);
+
+/* --------------------------------------------------------------------------------------
+ * dci_presample — S1.  P:177 (pre-sampling batches), P:196 (t_sample, t_feature per
+ * batch), P:200 (per-node visit counts), P:203 (per-element Counts, Fig. 6(a)).
+ * Runs ceil(num_seeds / batch) batches (last one ragged) with pass = 1 over the ORIGINAL
+ * CSC and no cache, and ACCUMULATES (+=) into the caller's device arrays:
+ *   node_visits int32[N]: +1 per batch in which v is in F_L (C7)
+ *   edge_counts int32[E]: +1 per (hop, batch) in which element e is sampled (C8)
+ * and writes host uint64 t_sample_ns[nb], t_feature_ns[nb] (CUDA-event stage times of
+ * each batch: hops S5-S6 vs route+gather S7-S8).  Synchronises `stream`.
+ * Errors: DCI_EINVAL, DCI_ESTATE (after dci_fill), DCI_ESEED / DCI_EDUP (bad seeds).
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_presample(dci_ctx* ctx, const int32_t* seeds, int64_t num_seeds, int32_t batch,
+                         const int32_t* fanouts, int32_t L, uint64_t seed, int32_t* node_visits,
+                         int32_t* edge_counts, uint64_t* t_sample_ns, uint64_t* t_feature_ns, void* stream);
+
+/* --------------------------------------------------------------------------------------
+ * dci_allocate — S2, Eq. (1).  Exact integer arithmetic (O-10):
+ *   C_adj = floor(C * S / (S + F)), C_feat = C - C_adj, S = sum t_sample_ns, F = sum
+ *   t_feature_ns; S + F == 0 -> C_adj = floor(C / 2).
+ *   ratio_den > 0: C_adj = floor(C * ratio_num / ratio_den) instead (sweeps, C20).
+ *   C == 0 ("auto"): C = free device memory - the presample's peak per-batch
+ *   workspace - 1 GiB reserve (C21), floored at 0.
+ * Postcondition: *c_adj + *c_feat == C.  Host-only.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_allocate(dci_ctx* ctx, uint64_t C, const uint64_t* t_sample_ns, const uint64_t* t_feature_ns,
+                        int32_t n, int64_t ratio_num, int64_t ratio_den, uint64_t* c_adj, uint64_t* c_feat);
+
+/* --------------------------------------------------------------------------------------
+ * dci_fill — S3 + S4.  Feature fill P:200 (O-11): cap = min(N, floor(c_feat / (4*pitch)))
+ * rows; admits the top-cap nodes by (visits desc, id asc) via a device radix select and
+ * assigns slots in ascending id.  Adjacency fill, Algorithm 1 P:209-243 + Fig. 6
+ * P:203-206 (O-12): per-node stable reorder of each run by count desc (level 2, always
+ * applied to the host CSC), node order (total desc, id asc) (level 1) found by a weighted
+ * radix select, node-major prefix of floor(c_adj / 4) elements (whole CSC if it fits).
+ *  node_visits device int32[N], edge_counts device int32[E] (e.g. the presample output,
+ *  allreduced across ranks).  Re-filling recomputes from the original CSC (idempotent).
+ * Synchronises `stream`.  Device memory: caches + ~8E bytes temporarily.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_fill(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
+                    uint64_t c_feat, void* stream);
+
+/* --------------------------------------------------------------------------------------
+ * Introspection (parity tests).  Every output pointer is HOST memory and may be NULL.
+ *  cached_len int32[N], cache_off int64[N] (element offset of v's prefix in acache),
+ *  slot_of int32[N] (-1 = not cached), acache int32[info.adj_elems] (prefixes laid out in
+ *  ascending node id), fcache fp32[info.feat_rows * pitch], indices_cur int32[E] (the
+ *  current host CSC: original before fill, level-2 reordered after).
+ * ------------------------------------------------------------------------------------ */
+typedef struct dci_cache_info {
+  int32_t state;
+  int32_t pitch;          /* floats per cached/host feature row */
+  int64_t N, E;
+  int32_t D;
+  int32_t whole_fit;      /* 1 if the whole CSC is cached (Alg. 1 lines 1-3) */
+  uint64_t c_adj, c_feat; /* bytes granted by the last fill */
+  int64_t adj_elems;      /* elements in the adjacency cache */
+  int64_t feat_rows;      /* rows in the feature cache */
+  uint64_t presample_peak_bytes;
+  uint64_t launches;      /* kernels this context has launched so far */
+} dci_cache_info;
+
+dci_status dci_cache_info_get(const dci_ctx* ctx, dci_cache_info* info);
+dci_status dci_cache_state(dci_ctx* ctx, int32_t* cached_len, int64_t* cache_off, int32_t* slot_of,
+                           int32_t* acache, float* fcache, int32_t* indices_cur);
+
+/* Stage times of the workspace's last batch, in ms (CUDA events recorded on the launch
+ * stream around the sampling hops and around the gather; requires profiling on). */
+dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on);
+dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms);
+
+/* Kernels launched by this context so far (all workspaces). */
+uint64_t dci_launch_count(const dci_ctx* ctx);
+
+const char* dci_last_error(void);
+int32_t dci_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCI_H_ */

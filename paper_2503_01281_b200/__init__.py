@@ -1,0 +1,331 @@
+"""Python binding of libdci (include/dci.h) — argument marshalling only.
+
+Every step of the DCI hot path (sampling, dedup/relabel, feature route, gather, presample
+counting, radix-select fills) runs in the CUDA kernels of ``libdci.so``; this module only
+converts arguments, allocates output tensors with torch (device memory plumbing) and
+passes torch's current CUDA stream.  There is no CPU fallback: if the extension is missing
+or no CUDA device is present, the compute calls raise.
+
+Names follow the C ABI: ``load_graph``, ``presample``, ``allocate``, ``fill``,
+``sample_gather`` (+ ``sample_gather_host``), ``output_bounds``, ``workspace_create``,
+``cache_state``, ``cache_info``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdci.so")
+MAX_LAYERS = 8
+MAX_FANOUT = 32
+
+STATUS = {0: "DCI_OK", 1: "DCI_EINVAL", 2: "DCI_ESTATE", 3: "DCI_ECUDA", 4: "DCI_ENOMEM", 5: "DCI_ESEED",
+          6: "DCI_EDUP", 7: "DCI_ECAP", 8: "DCI_ERANGE"}
+OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
+
+EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
+            "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
+            "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
+            "dci_launch_count", "dci_last_error", "dci_version"]
+
+
+class DciError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str = ""):
+        super().__init__(f"{where}: {STATUS.get(code, code)} {msg}")
+        self.code = code
+
+
+class dci_batch_out(C.Structure):
+    _fields_ = [("frontier", C.c_void_p), ("frontier_cap", C.c_int64), ("sizes", C.c_void_p),
+                ("bptr", C.c_void_p * MAX_LAYERS), ("bsrc", C.c_void_p * MAX_LAYERS),
+                ("hop_cap", C.c_int64 * MAX_LAYERS), ("bsrc_cap", C.c_int64 * MAX_LAYERS),
+                ("X", C.c_void_p), ("ldx", C.c_int64), ("counters", C.c_void_p), ("status", C.c_void_p)]
+
+
+class dci_cache_info(C.Structure):
+    _fields_ = [("state", C.c_int32), ("pitch", C.c_int32), ("N", C.c_int64), ("E", C.c_int64), ("D", C.c_int32),
+                ("whole_fit", C.c_int32), ("c_adj", C.c_uint64), ("c_feat", C.c_uint64), ("adj_elems", C.c_int64),
+                ("feat_rows", C.c_int64), ("presample_peak_bytes", C.c_uint64), ("launches", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdci.so (built in-tree by __graft_entry__.build()); raise if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+    sig = {
+        "dci_load_graph": [C.POINTER(C.c_void_p), C.c_int, i64, i64, vp, vp, vp, i32, C.c_uint32],
+        "dci_destroy": [vp],
+        "dci_output_bounds": [vp, i32, vp, i32, vp, vp, vp],
+        "dci_workspace_create": [vp, i32, vp, i32, C.POINTER(C.c_void_p)],
+        "dci_workspace_destroy": [vp],
+        "dci_sample_gather": [vp, vp, vp, i32, vp, i32, u64, C.POINTER(dci_batch_out), vp],
+        "dci_sample_gather_host": [vp, vp, vp, i32, vp, i32, u64, C.POINTER(dci_batch_out), vp, vp, vp, vp],
+        "dci_presample": [vp, vp, i64, i32, vp, i32, u64, vp, vp, vp, vp, vp],
+        "dci_allocate": [vp, u64, vp, vp, i32, i64, i64, C.POINTER(u64), C.POINTER(u64)],
+        "dci_fill": [vp, vp, vp, u64, u64, vp],
+        "dci_cache_info_get": [vp, C.POINTER(dci_cache_info)],
+        "dci_cache_state": [vp, vp, vp, vp, vp, vp, vp],
+        "dci_workspace_set_profiling": [vp, i32],
+        "dci_workspace_stage_ms": [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)],
+        "dci_launch_count": [vp],
+        "dci_last_error": [],
+        "dci_version": [],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    L.dci_launch_count.restype = C.c_uint64
+    L.dci_last_error.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def _check(rc: int, where: str):
+    if rc != OK:
+        raise DciError(rc, where, lib().dci_last_error().decode(errors="replace"))
+
+
+def _np_ptr(a):
+    return a.ctypes.data
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _t_ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class Context:
+    """Owns a dci_ctx (graph in pinned host memory + device directory + caches)."""
+
+    def __init__(self, handle, N, E, D, device):
+        self.handle, self.N, self.E, self.D, self.device = handle, N, E, D, device
+
+    def close(self):
+        if self.handle:
+            lib().dci_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(lib().dci_launch_count(self.handle))
+
+
+def load_graph(indptr, indices, feats, device: int = 0) -> Context:
+    """dci_load_graph (S0).  indptr int64[N+1], indices int32[E], feats fp32[N, D]: host arrays
+    (numpy or CPU torch); copied into pinned, device-mapped memory."""
+    ip = np.ascontiguousarray(_to_np(indptr), np.int64)
+    ix = np.ascontiguousarray(_to_np(indices), np.int32)
+    ft = np.ascontiguousarray(_to_np(feats), np.float32)
+    N, E, D = len(ip) - 1, len(ix), ft.shape[1]
+    h = C.c_void_p()
+    _check(lib().dci_load_graph(C.byref(h), device, N, E, _np_ptr(ip), _np_ptr(ix) if E else None, _np_ptr(ft),
+                                D, 0), "dci_load_graph")
+    return Context(h, N, E, D, device)
+
+
+def _to_np(a):
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            return a.detach().cpu().numpy()
+    except ImportError:
+        pass
+    return np.asarray(a)
+
+
+def output_bounds(ctx: Context, B: int, fanouts):
+    """dci_output_bounds: worst-case |F_h| (h=0..L), bsrc sizes per hop, feature pitch."""
+    fan = np.ascontiguousarray(fanouts, np.int32)
+    L = len(fan)
+    fc = np.zeros(L + 1, np.int64)
+    bc = np.zeros(L, np.int64)
+    p = C.c_int32()
+    _check(lib().dci_output_bounds(ctx.handle, B, _np_ptr(fan), L, _np_ptr(fc), _np_ptr(bc), C.byref(p)),
+           "dci_output_bounds")
+    return fc, bc, int(p.value)
+
+
+class Workspace:
+    def __init__(self, ctx: Context, max_batch: int, max_fanouts):
+        fan = np.ascontiguousarray(max_fanouts, np.int32)
+        h = C.c_void_p()
+        _check(lib().dci_workspace_create(ctx.handle, max_batch, _np_ptr(fan), len(fan), C.byref(h)),
+               "dci_workspace_create")
+        self.handle, self.ctx, self.max_batch, self.fanouts = h, ctx, max_batch, tuple(int(f) for f in fan)
+
+    def close(self):
+        if self.handle:
+            lib().dci_workspace_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_profiling(self, on: bool = True):
+        _check(lib().dci_workspace_set_profiling(self.handle, 1 if on else 0), "dci_workspace_set_profiling")
+
+    def stage_ms(self):
+        s, g = C.c_float(), C.c_float()
+        _check(lib().dci_workspace_stage_ms(self.handle, C.byref(s), C.byref(g)), "dci_workspace_stage_ms")
+        return float(s.value), float(g.value)
+
+
+def workspace_create(ctx: Context, max_batch: int, max_fanouts) -> Workspace:
+    return Workspace(ctx, max_batch, max_fanouts)
+
+
+class BatchOut:
+    """Caller-owned device output buffers of one batch (torch tensors on ctx.device)."""
+
+    def __init__(self, ctx: Context, B: int, fanouts, with_x: bool = True, ldx: int | None = None):
+        import torch
+        fc, bc, pitch = output_bounds(ctx, B, fanouts)
+        dev = torch.device("cuda", ctx.device)
+        L = len(fanouts)
+        self.L, self.D, self.pitch = L, ctx.D, pitch
+        self.ldx = pitch if ldx is None else int(ldx)
+        self.frontier = torch.empty(max(int(fc[L]), 1), dtype=torch.int32, device=dev)
+        self.sizes = torch.zeros(L + 1, dtype=torch.int64, device=dev)
+        self.bptr = [torch.empty(int(fc[h]) + 1, dtype=torch.int32, device=dev) for h in range(L)]
+        self.bsrc = [torch.empty(max(int(bc[h]), 1), dtype=torch.int32, device=dev) for h in range(L)]
+        self.X = torch.empty((max(int(fc[L]), 1), self.ldx), dtype=torch.float32, device=dev) if with_x else None
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        s = dci_batch_out()
+        s.frontier = self.frontier.data_ptr()
+        s.frontier_cap = int(fc[L])
+        s.sizes = self.sizes.data_ptr()
+        for h in range(L):
+            s.bptr[h] = self.bptr[h].data_ptr()
+            s.bsrc[h] = self.bsrc[h].data_ptr()
+            s.hop_cap[h] = int(fc[h])
+            s.bsrc_cap[h] = int(bc[h])
+        s.X = _t_ptr(self.X)
+        s.ldx = self.ldx
+        s.counters = self.counters.data_ptr()
+        s.status = self.status.data_ptr()
+        self.struct = s
+
+    def result(self):
+        """Synchronise and return host copies trimmed to the batch's actual sizes."""
+        import torch
+        torch.cuda.synchronize(self.frontier.device)
+        n = self.sizes.cpu().numpy()
+        L = self.L
+        bptr = [self.bptr[h][: n[h] + 1].cpu().numpy() for h in range(L)]
+        bsrc = [self.bsrc[h][: int(bptr[h][-1])].cpu().numpy() for h in range(L)]
+        out = {
+            "F": self.frontier[: n[L]].cpu().numpy(),
+            "sizes": n,
+            "bptr": bptr,
+            "bsrc": bsrc,
+            "counters": self.counters.cpu().numpy().astype(np.uint64),
+            "status": int(self.status.cpu().item()),
+        }
+        if self.X is not None:
+            out["X"] = self.X[: n[L], : self.D].cpu().numpy()
+        return out
+
+
+def sample_gather(ctx: Context, ws: Workspace, seeds, fanouts, seed: int, out: BatchOut, stream=None):
+    """dci_sample_gather (S5-S8), asynchronous on `stream` (default: torch current stream).
+    seeds: int32 CUDA tensor on ctx.device."""
+    fan = np.ascontiguousarray(fanouts, np.int32)
+    _check(lib().dci_sample_gather(ctx.handle, ws.handle, seeds.data_ptr(), int(seeds.numel()), _np_ptr(fan),
+                                   len(fan), seed, C.byref(out.struct), _stream_ptr(stream)), "dci_sample_gather")
+
+
+def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: int, out: BatchOut, sizes_host,
+                       counters_host, status_host, stream=None):
+    """dci_sample_gather_host: seeds from (pinned) host memory; sizes/counters/status copied back
+    to host buffers (pinned torch tensors) on the same stream."""
+    fan = np.ascontiguousarray(fanouts, np.int32)
+    _check(lib().dci_sample_gather_host(ctx.handle, ws.handle, seeds_host.data_ptr(), int(seeds_host.numel()),
+                                        _np_ptr(fan), len(fan), seed, C.byref(out.struct),
+                                        sizes_host.data_ptr(), counters_host.data_ptr(), status_host.data_ptr(),
+                                        _stream_ptr(stream)), "dci_sample_gather_host")
+
+
+def presample(ctx: Context, seeds, batch: int, fanouts, seed: int, node_visits, edge_counts, stream=None):
+    """dci_presample (S1): accumulates into node_visits int32[N] / edge_counts int32[E] (CUDA
+    tensors); returns host uint64 arrays (t_sample_ns, t_feature_ns), one entry per batch."""
+    fan = np.ascontiguousarray(fanouts, np.int32)
+    n = int(seeds.numel())
+    nb = (n + batch - 1) // batch
+    ts = np.zeros(max(nb, 1), np.uint64)
+    tf = np.zeros(max(nb, 1), np.uint64)
+    _check(lib().dci_presample(ctx.handle, seeds.data_ptr(), n, batch, _np_ptr(fan), len(fan), seed,
+                               node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None, _np_ptr(ts),
+                               _np_ptr(tf), _stream_ptr(stream)), "dci_presample")
+    return ts[:nb], tf[:nb]
+
+
+def allocate(ctx: Context | None, C_bytes: int, t_sample=(), t_feature=(), ratio=None):
+    """dci_allocate (S2, Eq. 1).  C_bytes = 0 -> auto budget.  ratio=(num, den) overrides."""
+    ts = np.ascontiguousarray(t_sample, np.uint64).reshape(-1)
+    tf = np.ascontiguousarray(t_feature, np.uint64).reshape(-1)
+    n = len(ts)
+    if n == 0:
+        ts = np.zeros(1, np.uint64)
+        tf = np.zeros(1, np.uint64)
+    num, den = (0, 0) if ratio is None else ratio
+    a, f = C.c_uint64(), C.c_uint64()
+    _check(lib().dci_allocate(ctx.handle if ctx else None, C_bytes, _np_ptr(ts), _np_ptr(tf), n, num, den,
+                              C.byref(a), C.byref(f)), "dci_allocate")
+    return int(a.value), int(f.value)
+
+
+def fill(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat: int, stream=None):
+    """dci_fill (S3 + S4)."""
+    _check(lib().dci_fill(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None, c_adj,
+                          c_feat, _stream_ptr(stream)), "dci_fill")
+
+
+def cache_info(ctx: Context) -> dict:
+    info = dci_cache_info()
+    _check(lib().dci_cache_info_get(ctx.handle, C.byref(info)), "dci_cache_info_get")
+    return {k: getattr(info, k) for k, _ in dci_cache_info._fields_}
+
+
+def cache_state(ctx: Context) -> dict:
+    """dci_cache_state: host copies of the directory cache fields, both caches and the current
+    host CSC."""
+    info = cache_info(ctx)
+    N, E, pitch = info["N"], info["E"], info["pitch"]
+    cl = np.zeros(N, np.int32)
+    co = np.zeros(N, np.int64)
+    so = np.zeros(N, np.int32)
+    ac = np.zeros(max(info["adj_elems"], 1), np.int32)
+    fc = np.zeros((max(info["feat_rows"], 1), pitch), np.float32)
+    ix = np.zeros(max(E, 1), np.int32)
+    _check(lib().dci_cache_state(ctx.handle, _np_ptr(cl), _np_ptr(co), _np_ptr(so), _np_ptr(ac), _np_ptr(fc),
+                                 _np_ptr(ix)), "dci_cache_state")
+    return {"cached_len": cl, "cache_off": co, "slot_of": so, "acache": ac[: info["adj_elems"]],
+            "fcache": fc[: info["feat_rows"]], "indices_cur": ix[:E], "info": info}

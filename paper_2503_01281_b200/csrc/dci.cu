@@ -1,0 +1,580 @@
+// C-ABI of libdci (include/dci.h): context lifecycle, workspaces, presample (S1), Eq. (1)
+// allocation (S2), fill (S3/S4, fill.cu) and the per-batch hot loop (S5-S8, sample.cu /
+// gather.cu).  Host code only orchestrates: every step of the path runs in a kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "dci_internal.cuh"
+
+namespace dci {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+dci_status fail(dci_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+dci_status cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? DCI_ENOMEM : DCI_ECUDA;
+}
+
+void launch_fill_i32(dci_ctx* ctx, int32_t* p, int64_t n, int32_t val, cudaStream_t s);
+
+int occupancy_blocks(const void* kernel, int block, int cap) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(kernel);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, 0) != cudaSuccess || n < 1) n = 1;
+  n = std::min(n, cap);
+  cache[kernel] = n;
+  return n;
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// |F_h| <= min(N, B * prod_{j<h} (1 + f_j)), hop j using fanouts[L-1-j] (reading C3).
+void frontier_bounds(int64_t N, int64_t B, const int32_t* fan, int32_t L, int64_t* caps) {
+  caps[0] = std::min<int64_t>(N, B);
+  for (int h = 0; h < L; ++h) {
+    const int64_t f = fan[L - 1 - h];
+    const double est = (double)caps[h] * (double)(1 + f);
+    caps[h + 1] = est >= (double)N ? N : std::min<int64_t>(N, caps[h] * (1 + f));
+  }
+}
+
+dci_status check_fanouts(const int32_t* fanouts, int32_t L) {
+  if (!fanouts || L < 1 || L > DCI_MAX_LAYERS) return fail(DCI_EINVAL, "L must be in [1, DCI_MAX_LAYERS]");
+  for (int i = 0; i < L; ++i)
+    if (fanouts[i] < 1 || fanouts[i] > DCI_MAX_FANOUT) return fail(DCI_EINVAL, "fan-out must be in [1, 32]");
+  return DCI_OK;
+}
+
+// Enqueue one batch (shared by inference pass 0 and presample pass 1).
+dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, const int32_t* fanouts,
+                     int32_t L, uint64_t seed, uint32_t pass, const dci_batch_out* out, int32_t* node_visits,
+                     int32_t* edge_counts, cudaStream_t s) {
+  if (ws->ctx != ctx) return fail(DCI_EINVAL, "workspace belongs to another context");
+  dci_status st = check_fanouts(fanouts, L);
+  if (st != DCI_OK) return st;
+  if (!out || !out->frontier || !out->sizes || !out->counters || !out->status)
+    return fail(DCI_EINVAL, "dci_batch_out has a null required pointer");
+  if (B < 0 || B > ws->max_batch) return fail(DCI_EINVAL, "B exceeds the workspace's max_batch");
+  if (B > 0 && !seeds) return fail(DCI_EINVAL, "seeds is null");
+  if (L != ws->L) return fail(DCI_EINVAL, "L differs from the workspace's L");
+  for (int i = 0; i < L; ++i)
+    if (fanouts[i] > ws->max_fan[i]) return fail(DCI_EINVAL, "fan-out exceeds the workspace's max_fanouts");
+  int64_t caps[DCI_MAX_LAYERS + 1];
+  frontier_bounds(ctx->N, B, fanouts, L, caps);
+  if (out->frontier_cap < caps[L]) return fail(DCI_ECAP, "frontier_cap < dci_output_bounds");
+  for (int h = 0; h < L; ++h) {
+    const int64_t f = fanouts[L - 1 - h];
+    if (!out->bptr[h] || !out->bsrc[h]) return fail(DCI_EINVAL, "null bptr/bsrc");
+    if (out->hop_cap[h] < caps[h] || out->bsrc_cap[h] < caps[h] * f)
+      return fail(DCI_ECAP, "hop_cap/bsrc_cap < dci_output_bounds");
+  }
+  if (out->X && out->ldx < ctx->D) return fail(DCI_EINVAL, "ldx < D");
+
+  DeviceGuard g(ctx->device);
+  const bool prof = ws->profiling || pass == 1;
+  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[0], s));
+  HopParams prev{};
+  for (int h = 0; h < L; ++h) {
+    HopParams p{};
+    p.F_in = (h == 0) ? seeds : out->frontier;
+    p.F = out->frontier;
+    p.hop = h;
+    p.f = fanouts[L - 1 - h];
+    p.pass = pass;
+    p.seed = seed;
+    p.B = B;
+    p.cand = ws->cand[h & 1];
+    p.kcnt = ws->kcnt[h & 1];
+    if (h > 0) {
+      p.prev_cand = prev.cand;
+      p.prev_kcnt = prev.kcnt;
+      p.prev_bptr = out->bptr[h - 1];
+      p.prev_bsrc = out->bsrc[h - 1];
+      p.prev_f = prev.f;
+    }
+    p.bptr = out->bptr[h];
+    p.edge_counts = edge_counts;
+    launch_sample_hop(ctx, ws, p, s);
+    launch_scan_hop(ctx, ws, p, s);
+    prev = p;
+  }
+  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[1], s));
+  launch_route(ctx, ws, L, B, out->frontier, prev.cand, prev.kcnt, out->bptr[L - 1], out->bsrc[L - 1], prev.f,
+               node_visits, s);
+  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[2], s));
+  if (out->X) {
+    // misses (PCIe/UVA) on the auxiliary stream, hits (HBM) on the caller's stream
+    DCI_CUDA(cudaEventRecord(ws->ev_fork, s));
+    DCI_CUDA(cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0));
+    launch_gather(ctx, ws, false, out->frontier, L, out->X, out->ldx, ws->aux);
+    launch_gather(ctx, ws, true, out->frontier, L, out->X, out->ldx, s);
+    DCI_CUDA(cudaEventRecord(ws->ev_join, ws->aux));
+    DCI_CUDA(cudaStreamWaitEvent(s, ws->ev_join, 0));
+  }
+  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], s));
+  launch_finish(ctx, ws, L, B, out, s);
+  ws->have_times = prof ? 1 : 0;
+  DCI_CUDA(cudaGetLastError());
+  return DCI_OK;
+}
+
+void free_ctx(dci_ctx* c) {
+  if (!c) return;
+  if (c->pre_ws) dci_workspace_destroy(c->pre_ws);
+  if (c->pre_out_mem) cudaFree(c->pre_out_mem);
+  if (c->d_dir) cudaFree(c->d_dir);
+  if (c->d_acache) cudaFree(c->d_acache);
+  if (c->d_fcache) cudaFree(c->d_fcache);
+  if (c->h_idx_cur && c->h_idx_cur != c->h_idx_orig) cudaFreeHost(c->h_idx_cur);
+  if (c->h_idx_orig) cudaFreeHost(c->h_idx_orig);
+  if (c->h_feats) cudaFreeHost(c->h_feats);
+  free(c->h_indptr);
+  delete c;
+}
+
+}  // namespace
+}  // namespace dci
+
+using namespace dci;
+
+extern "C" {
+
+const char* dci_last_error(void) { return g_last_error.c_str(); }
+int32_t dci_version(void) { return DCI_VERSION; }
+
+dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const int64_t* indptr,
+                          const int32_t* indices, const float* feats, int32_t D, uint32_t flags) {
+  if (!out) return fail(DCI_EINVAL, "out is null");
+  *out = nullptr;
+  if (flags != 0) return fail(DCI_EINVAL, "flags must be 0");
+  if (N < 1 || N >= (1ll << 31)) return fail(DCI_EINVAL, "N must be in [1, 2^31)");
+  if (E < 0 || E >= (1ll << 40)) return fail(DCI_EINVAL, "E must be in [0, 2^40)");
+  if (D < 1) return fail(DCI_EINVAL, "D must be >= 1");
+  if (!indptr || (E > 0 && !indices) || !feats) return fail(DCI_EINVAL, "null input pointer");
+  // CSC invariants: monotone column pointers, ids in range
+  if (indptr[0] != 0 || indptr[N] != E) return fail(DCI_EINVAL, "indptr[0] must be 0 and indptr[N] == E");
+  for (int64_t v = 0; v < N; ++v) {
+    if (indptr[v + 1] < indptr[v]) return fail(DCI_EINVAL, "indptr must be non-decreasing");
+    if (indptr[v + 1] - indptr[v] >= (1ll << 31)) return fail(DCI_ERANGE, "a degree exceeds 2^31-1");
+  }
+  for (int64_t e = 0; e < E; ++e)
+    if (indices[e] < 0 || (int64_t)indices[e] >= N) return fail(DCI_EINVAL, "indices entry out of [0, N)");
+  int ndev = 0;
+  DCI_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(DCI_EINVAL, "bad device ordinal");
+  DeviceGuard g(device);
+  dci_ctx* c = new (std::nothrow) dci_ctx();
+  if (!c) return fail(DCI_ENOMEM, "host allocation failed");
+  c->device = device;
+  c->N = N;
+  c->E = E;
+  c->D = D;
+  c->pitch = (D + 3) / 4 * 4;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  auto bail = [&](dci_status s) {
+    free_ctx(c);
+    return s;
+  };
+  c->h_indptr = static_cast<int64_t*>(malloc(sizeof(int64_t) * (N + 1)));
+  if (!c->h_indptr) return bail(fail(DCI_ENOMEM, "host allocation failed"));
+  memcpy(c->h_indptr, indptr, sizeof(int64_t) * (N + 1));
+  cudaError_t e;
+  e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_idx_orig), sizeof(int32_t) * std::max<int64_t>(E, 1),
+                    cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(indices)"));
+  if (E) memcpy(c->h_idx_orig, indices, sizeof(int32_t) * E);
+  c->h_idx_cur = c->h_idx_orig;
+  const size_t fbytes = sizeof(float) * (size_t)N * c->pitch;
+  e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_feats), fbytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(feats)"));
+  if (c->pitch == D) {
+    memcpy(c->h_feats, feats, fbytes);
+  } else {
+    for (int64_t v = 0; v < N; ++v) {
+      memcpy(c->h_feats + v * c->pitch, feats + v * D, sizeof(float) * D);
+      memset(c->h_feats + v * c->pitch + D, 0, sizeof(float) * (c->pitch - D));
+    }
+  }
+  void* dp = nullptr;
+  if ((e = cudaHostGetDevicePointer(&dp, c->h_idx_orig, 0)) != cudaSuccess)
+    return bail(cuda_fail(e, "cudaHostGetDevicePointer"));
+  c->u_idx_orig = c->u_idx_cur = static_cast<const int32_t*>(dp);
+  if ((e = cudaHostGetDevicePointer(&dp, c->h_feats, 0)) != cudaSuccess)
+    return bail(cuda_fail(e, "cudaHostGetDevicePointer"));
+  c->u_feats = static_cast<const float*>(dp);
+  if ((e = cudaMalloc(&c->d_dir, sizeof(DirEntry) * N)) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(dir)"));
+  int64_t* d_indptr = nullptr;
+  if ((e = cudaMalloc(&d_indptr, sizeof(int64_t) * (N + 1))) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc"));
+  cudaMemcpy(d_indptr, indptr, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice);
+  launch_build_directory(c, d_indptr, 0);
+  e = cudaDeviceSynchronize();
+  cudaFree(d_indptr);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "build directory"));
+  c->state = DCI_STATE_LOADED;
+  *out = c;
+  return DCI_OK;
+}
+
+dci_status dci_destroy(dci_ctx* ctx) {
+  if (!ctx) return DCI_OK;
+  DeviceGuard g(ctx->device);
+  cudaDeviceSynchronize();
+  free_ctx(ctx);
+  return DCI_OK;
+}
+
+dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanouts, int32_t L,
+                             int64_t* frontier_caps, int64_t* bsrc_caps, int32_t* pitch) {
+  if (!ctx || B < 0) return fail(DCI_EINVAL, "bad arguments");
+  dci_status st = check_fanouts(fanouts, L);
+  if (st != DCI_OK) return st;
+  int64_t caps[DCI_MAX_LAYERS + 1];
+  frontier_bounds(ctx->N, B, fanouts, L, caps);
+  if (caps[L] * 32 >= (1ll << 31)) return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
+  for (int h = 0; h <= L; ++h)
+    if (frontier_caps) frontier_caps[h] = caps[h];
+  for (int h = 0; h < L; ++h)
+    if (bsrc_caps) bsrc_caps[h] = caps[h] * fanouts[L - 1 - h];
+  if (pitch) *pitch = ctx->pitch;
+  return DCI_OK;
+}
+
+dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* max_fanouts, int32_t L,
+                                dci_workspace** out) {
+  if (!ctx || !out || max_batch < 1) return fail(DCI_EINVAL, "bad arguments");
+  *out = nullptr;
+  dci_status st = check_fanouts(max_fanouts, L);
+  if (st != DCI_OK) return st;
+  DeviceGuard g(ctx->device);
+  dci_workspace* w = new (std::nothrow) dci_workspace();
+  if (!w) return fail(DCI_ENOMEM, "host allocation failed");
+  w->ctx = ctx;
+  w->max_batch = max_batch;
+  w->L = L;
+  for (int i = 0; i < L; ++i) w->max_fan[i] = max_fanouts[i];
+  frontier_bounds(ctx->N, max_batch, max_fanouts, L, w->hop_cap);
+  int64_t max_front = 0;
+  for (int h = 0; h <= L; ++h) max_front = std::max(max_front, w->hop_cap[h]);
+  if (max_front * 32 >= (1ll << 31)) {
+    delete w;
+    return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
+  }
+  w->cand_cap = 0;
+  w->tiles_cap = 0;
+  for (int h = 0; h < L; ++h) {
+    w->cand_cap = std::max(w->cand_cap, w->hop_cap[h] * max_fanouts[L - 1 - h]);
+    w->tile_off[h] = w->tiles_cap;
+    w->tiles_cap += (w->hop_cap[h] + kScanTile - 1) / kScanTile + 1;
+  }
+  auto bail = [&](cudaError_t e, const char* what) {
+    dci_workspace_destroy(w);
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&w->pos_of, sizeof(int32_t) * ctx->N)) != cudaSuccess) return bail(e, "cudaMalloc(pos_of)");
+  for (int i = 0; i < 2; ++i) {
+    if ((e = cudaMalloc(&w->cand[i], sizeof(int32_t) * std::max<int64_t>(w->cand_cap, 1))) != cudaSuccess)
+      return bail(e, "cudaMalloc(cand)");
+    if ((e = cudaMalloc(&w->kcnt[i], sizeof(int32_t) * std::max<int64_t>(max_front, 1))) != cudaSuccess)
+      return bail(e, "cudaMalloc(kcnt)");
+  }
+  if ((e = cudaMalloc(&w->tile_state, sizeof(unsigned long long) * w->tiles_cap)) != cudaSuccess)
+    return bail(e, "cudaMalloc(tile_state)");
+  if ((e = cudaMalloc(&w->hit_list, sizeof(int64_t) * std::max<int64_t>(w->hop_cap[L], 1))) != cudaSuccess)
+    return bail(e, "cudaMalloc(hit_list)");
+  if ((e = cudaMalloc(&w->miss_list, sizeof(int64_t) * std::max<int64_t>(w->hop_cap[L], 1))) != cudaSuccess)
+    return bail(e, "cudaMalloc(miss_list)");
+  if ((e = cudaMalloc(&w->scal, sizeof(BatchScalars))) != cudaSuccess) return bail(e, "cudaMalloc(scal)");
+  if ((e = cudaMalloc(&w->seeds_stage, sizeof(int32_t) * max_batch)) != cudaSuccess) return bail(e, "cudaMalloc");
+  if ((e = cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "stream");
+  if ((e = cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  for (int i = 0; i < 4; ++i)
+    if ((e = cudaEventCreate(&w->ev_t[i])) != cudaSuccess) return bail(e, "event");
+  launch_fill_i32(ctx, w->pos_of, ctx->N, kPosEmpty, 0);
+  cudaMemset(w->tile_state, 0, sizeof(unsigned long long) * w->tiles_cap);
+  cudaMemset(w->scal, 0, sizeof(BatchScalars));
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "workspace init");
+  *out = w;
+  return DCI_OK;
+}
+
+dci_status dci_workspace_destroy(dci_workspace* w) {
+  if (!w) return DCI_OK;
+  DeviceGuard g(w->ctx->device);
+  cudaDeviceSynchronize();
+  cudaFree(w->pos_of);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(w->cand[i]);
+    cudaFree(w->kcnt[i]);
+  }
+  cudaFree(w->tile_state);
+  cudaFree(w->hit_list);
+  cudaFree(w->miss_list);
+  cudaFree(w->scal);
+  cudaFree(w->seeds_stage);
+  if (w->aux) cudaStreamDestroy(w->aux);
+  if (w->ev_fork) cudaEventDestroy(w->ev_fork);
+  if (w->ev_join) cudaEventDestroy(w->ev_join);
+  for (int i = 0; i < 4; ++i)
+    if (w->ev_t[i]) cudaEventDestroy(w->ev_t[i]);
+  delete w;
+  return DCI_OK;
+}
+
+dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B,
+                             const int32_t* fanouts, int32_t L, uint64_t seed, const dci_batch_out* out,
+                             void* stream) {
+  if (!ctx || !ws) return fail(DCI_EINVAL, "null context/workspace");
+  return run_batch(ctx, ws, seeds, B, fanouts, L, seed, 0, out, nullptr, nullptr,
+                   static_cast<cudaStream_t>(stream));
+}
+
+dci_status dci_sample_gather_host(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds_host, int32_t B,
+                                  const int32_t* fanouts, int32_t L, uint64_t seed, const dci_batch_out* out,
+                                  int64_t* sizes_host, uint64_t* counters_host, int32_t* status_host,
+                                  void* stream) {
+  if (!ctx || !ws) return fail(DCI_EINVAL, "null context/workspace");
+  if (B < 0 || B > ws->max_batch) return fail(DCI_EINVAL, "B exceeds the workspace's max_batch");
+  if (B > 0 && !seeds_host) return fail(DCI_EINVAL, "seeds_host is null");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DeviceGuard g(ctx->device);
+  if (B > 0)
+    DCI_CUDA(cudaMemcpyAsync(ws->seeds_stage, seeds_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+  dci_status st = run_batch(ctx, ws, ws->seeds_stage, B, fanouts, L, seed, 0, out, nullptr, nullptr, s);
+  if (st != DCI_OK) return st;
+  if (sizes_host)
+    DCI_CUDA(cudaMemcpyAsync(sizes_host, out->sizes, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToHost, s));
+  if (counters_host)
+    DCI_CUDA(cudaMemcpyAsync(counters_host, out->counters, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, s));
+  if (status_host) DCI_CUDA(cudaMemcpyAsync(status_host, out->status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  return DCI_OK;
+}
+
+dci_status dci_presample(dci_ctx* ctx, const int32_t* seeds, int64_t num_seeds, int32_t batch,
+                         const int32_t* fanouts, int32_t L, uint64_t seed, int32_t* node_visits,
+                         int32_t* edge_counts, uint64_t* t_sample_ns, uint64_t* t_feature_ns, void* stream) {
+  if (!ctx) return fail(DCI_EINVAL, "null context");
+  if (ctx->state != DCI_STATE_LOADED) return fail(DCI_ESTATE, "dci_presample must run before dci_fill");
+  if (batch < 1 || num_seeds < 0) return fail(DCI_EINVAL, "batch must be >= 1");
+  if (num_seeds > 0 && !seeds) return fail(DCI_EINVAL, "seeds is null");
+  if (!node_visits || (ctx->E > 0 && !edge_counts)) return fail(DCI_EINVAL, "null count array");
+  dci_status st = check_fanouts(fanouts, L);
+  if (st != DCI_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DeviceGuard g(ctx->device);
+  const int32_t B = (int32_t)std::min<int64_t>(batch, std::max<int64_t>(num_seeds, 1));
+  // (re)create the internal presample workspace and outputs when the shape changes
+  bool same = ctx->pre_ws && ctx->pre_B == B && ctx->pre_L == L;
+  for (int i = 0; same && i < L; ++i) same = ctx->pre_fan[i] == fanouts[i];
+  int64_t caps[DCI_MAX_LAYERS + 1];
+  frontier_bounds(ctx->N, B, fanouts, L, caps);
+  if (!same) {
+    DCI_CUDA(cudaDeviceSynchronize());
+    if (ctx->pre_ws) dci_workspace_destroy(ctx->pre_ws);
+    ctx->pre_ws = nullptr;
+    if (ctx->pre_out_mem) cudaFree(ctx->pre_out_mem);
+    ctx->pre_out_mem = nullptr;
+    st = dci_workspace_create(ctx, B, fanouts, L, &ctx->pre_ws);
+    if (st != DCI_OK) return st;
+    size_t bytes = 0;
+    auto take = [&](size_t n) {
+      size_t off = bytes;
+      bytes += (n + 255) / 256 * 256;
+      return off;
+    };
+    size_t o_front = take(sizeof(int32_t) * caps[L]);
+    size_t o_sizes = take(sizeof(int64_t) * (L + 1));
+    size_t o_cnt = take(sizeof(uint64_t) * 4);
+    size_t o_status = take(sizeof(int32_t));
+    size_t o_bptr[DCI_MAX_LAYERS], o_bsrc[DCI_MAX_LAYERS];
+    for (int h = 0; h < L; ++h) {
+      o_bptr[h] = take(sizeof(int32_t) * (caps[h] + 1));
+      o_bsrc[h] = take(sizeof(int32_t) * caps[h] * fanouts[L - 1 - h]);
+    }
+    size_t o_x = take(sizeof(float) * caps[L] * ctx->pitch);
+    DCI_CUDA(cudaMalloc(&ctx->pre_out_mem, bytes));
+    char* base = static_cast<char*>(ctx->pre_out_mem);
+    dci_batch_out& o = ctx->pre_out;
+    memset(&o, 0, sizeof(o));
+    o.frontier = reinterpret_cast<int32_t*>(base + o_front);
+    o.frontier_cap = caps[L];
+    o.sizes = reinterpret_cast<int64_t*>(base + o_sizes);
+    o.counters = reinterpret_cast<uint64_t*>(base + o_cnt);
+    o.status = reinterpret_cast<int32_t*>(base + o_status);
+    for (int h = 0; h < L; ++h) {
+      o.bptr[h] = reinterpret_cast<int32_t*>(base + o_bptr[h]);
+      o.bsrc[h] = reinterpret_cast<int32_t*>(base + o_bsrc[h]);
+      o.hop_cap[h] = caps[h];
+      o.bsrc_cap[h] = caps[h] * fanouts[L - 1 - h];
+    }
+    o.X = reinterpret_cast<float*>(base + o_x);
+    o.ldx = ctx->pitch;
+    ctx->pre_B = B;
+    ctx->pre_L = L;
+    for (int i = 0; i < L; ++i) ctx->pre_fan[i] = fanouts[i];
+    // predicted peak per-batch workspace for the auto budget: outputs + scratch
+    uint64_t ws_bytes = bytes + sizeof(int32_t) * (uint64_t)ctx->N +
+                        sizeof(int32_t) * 2 * (uint64_t)(ctx->pre_ws->cand_cap + caps[L]) +
+                        sizeof(int64_t) * 2 * (uint64_t)caps[L];
+    ctx->presample_peak = std::max<uint64_t>(ctx->presample_peak, ws_bytes);
+  }
+  int32_t status = 0;
+  const int64_t nb = (num_seeds + batch - 1) / batch;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int32_t nbat = (int32_t)std::min<int64_t>(batch, num_seeds - b * batch);
+    st = run_batch(ctx, ctx->pre_ws, seeds + b * batch, nbat, fanouts, L, seed, 1, &ctx->pre_out, node_visits,
+                   edge_counts, s);
+    if (st != DCI_OK) return st;
+    DCI_CUDA(cudaMemcpyAsync(&status, ctx->pre_out.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    DCI_CUDA(cudaStreamSynchronize(s));
+    float ms_s = 0.f, ms_f = 0.f;
+    DCI_CUDA(cudaEventElapsedTime(&ms_s, ctx->pre_ws->ev_t[0], ctx->pre_ws->ev_t[1]));
+    DCI_CUDA(cudaEventElapsedTime(&ms_f, ctx->pre_ws->ev_t[1], ctx->pre_ws->ev_t[3]));
+    if (t_sample_ns) t_sample_ns[b] = (uint64_t)llround((double)ms_s * 1e6);
+    if (t_feature_ns) t_feature_ns[b] = (uint64_t)llround((double)ms_f * 1e6);
+    if (status != DCI_OK) return fail((dci_status)status, "dci_presample: invalid or duplicate seed in a batch");
+  }
+  return DCI_OK;
+}
+
+dci_status dci_allocate(dci_ctx* ctx, uint64_t C, const uint64_t* t_sample_ns, const uint64_t* t_feature_ns,
+                        int32_t n, int64_t ratio_num, int64_t ratio_den, uint64_t* c_adj, uint64_t* c_feat) {
+  if (!c_adj || !c_feat || n < 0) return fail(DCI_EINVAL, "bad arguments");
+  if (n > 0 && (!t_sample_ns || !t_feature_ns)) return fail(DCI_EINVAL, "null time arrays");
+  if (C == 0) {
+    // auto budget: free device memory minus the predicted peak workload minus 1 GiB
+    if (!ctx) return fail(DCI_EINVAL, "auto budget needs a context");
+    DeviceGuard g(ctx->device);
+    size_t free_b = 0, total_b = 0;
+    DCI_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // memory the current caches hold is reusable by a refill
+    uint64_t held = (uint64_t)ctx->acache_len * 4 + (uint64_t)ctx->fcache_rows * 4 * ctx->pitch;
+    const uint64_t reserve = 1ull << 30;
+    uint64_t avail = (uint64_t)free_b + held;
+    uint64_t need = ctx->presample_peak + reserve;
+    C = avail > need ? avail - need : 0;
+  }
+  unsigned __int128 adj;
+  if (ratio_den > 0) {
+    if (ratio_num < 0 || ratio_num > ratio_den) return fail(DCI_EINVAL, "ratio must be in [0, 1]");
+    adj = (unsigned __int128)C * (unsigned __int128)ratio_num / (unsigned __int128)ratio_den;
+  } else {
+    unsigned __int128 S = 0, F = 0;
+    for (int32_t k = 0; k < n; ++k) {
+      S += t_sample_ns[k];
+      F += t_feature_ns[k];
+    }
+    adj = (S + F == 0) ? (unsigned __int128)(C / 2) : (unsigned __int128)C * S / (S + F);
+  }
+  *c_adj = (uint64_t)adj;
+  *c_feat = C - (uint64_t)adj;
+  return DCI_OK;
+}
+
+dci_status dci_fill(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
+                    uint64_t c_feat, void* stream) {
+  if (!ctx) return fail(DCI_EINVAL, "null context");
+  if (!node_visits || (ctx->E > 0 && !edge_counts)) return fail(DCI_EINVAL, "null count array");
+  DeviceGuard g(ctx->device);
+  DCI_CUDA(cudaDeviceSynchronize());  // no batch may be in flight while caches change
+  return fill_impl(ctx, node_visits, edge_counts, c_adj, c_feat, static_cast<cudaStream_t>(stream));
+}
+
+dci_status dci_cache_info_get(const dci_ctx* ctx, dci_cache_info* info) {
+  if (!ctx || !info) return fail(DCI_EINVAL, "bad arguments");
+  info->state = ctx->state;
+  info->pitch = ctx->pitch;
+  info->N = ctx->N;
+  info->E = ctx->E;
+  info->D = ctx->D;
+  info->whole_fit = ctx->whole_fit;
+  info->c_adj = ctx->c_adj;
+  info->c_feat = ctx->c_feat;
+  info->adj_elems = ctx->acache_len;
+  info->feat_rows = ctx->fcache_rows;
+  info->presample_peak_bytes = ctx->presample_peak;
+  info->launches = ctx->launches;
+  return DCI_OK;
+}
+
+dci_status dci_cache_state(dci_ctx* ctx, int32_t* cached_len, int64_t* cache_off, int32_t* slot_of,
+                           int32_t* acache, float* fcache, int32_t* indices_cur) {
+  if (!ctx) return fail(DCI_EINVAL, "null context");
+  DeviceGuard g(ctx->device);
+  DCI_CUDA(cudaDeviceSynchronize());
+  const int64_t N = ctx->N;
+  if (cached_len || cache_off || slot_of) {
+    DirEntry* h = static_cast<DirEntry*>(malloc(sizeof(DirEntry) * N));
+    if (!h) return fail(DCI_ENOMEM, "host allocation failed");
+    cudaError_t e = cudaMemcpy(h, ctx->d_dir, sizeof(DirEntry) * N, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      free(h);
+      return cuda_fail(e, "copy directory");
+    }
+    for (int64_t v = 0; v < N; ++v) {
+      if (cached_len) cached_len[v] = h[v].cached_len;
+      if (cache_off) cache_off[v] = h[v].cache_off;
+      if (slot_of) slot_of[v] = h[v].slot;
+    }
+    free(h);
+  }
+  if (acache && ctx->acache_len)
+    DCI_CUDA(cudaMemcpy(acache, ctx->d_acache, sizeof(int32_t) * ctx->acache_len, cudaMemcpyDeviceToHost));
+  if (fcache && ctx->fcache_rows)
+    DCI_CUDA(cudaMemcpy(fcache, ctx->d_fcache, sizeof(float) * ctx->fcache_rows * ctx->pitch,
+                        cudaMemcpyDeviceToHost));
+  if (indices_cur && ctx->E) memcpy(indices_cur, ctx->h_idx_cur, sizeof(int32_t) * ctx->E);
+  return DCI_OK;
+}
+
+dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on) {
+  if (!ws) return fail(DCI_EINVAL, "null workspace");
+  ws->profiling = on ? 1 : 0;
+  return DCI_OK;
+}
+
+dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms) {
+  if (!ws) return fail(DCI_EINVAL, "null workspace");
+  if (!ws->have_times) return fail(DCI_ESTATE, "no profiled batch recorded");
+  DeviceGuard g(ws->ctx->device);
+  DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
+  if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, ws->ev_t[0], ws->ev_t[1]));
+  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[2], ws->ev_t[3]));
+  return DCI_OK;
+}
+
+uint64_t dci_launch_count(const dci_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// Internal declarations shared by the libdci translation units (CUDA path only; the
+// oracle under oracle/ shares nothing with this file).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/dci.h"
+
+namespace dci {
+
+// Per-node device directory entry (32 B = one DRAM sector).  One load gives everything a
+// hop needs for node v: where v's run lives on the host (host_off = indptr[v]), where its
+// cached prefix lives in HBM (cache_off, cached_len; P:206 prefix-hit rule) and its
+// feature-cache slot (P:200 remap table; -1 = miss).
+struct __align__(16) DirEntry {
+  int64_t host_off;
+  int64_t cache_off;
+  int32_t deg;
+  int32_t cached_len;
+  int32_t slot;
+  int32_t pad;
+};
+static_assert(sizeof(DirEntry) == 32, "directory entry must be one 32-byte sector");
+
+constexpr int32_t kPosEmpty = 0x7FFFFFFF;  // node->position table "absent"
+constexpr int kScanTile = 256;             // dst nodes per tile of the per-hop scan
+
+// Device-side per-batch scalars live in one small struct (workspace memory).
+struct BatchScalars {
+  int64_t sizes[DCI_MAX_LAYERS + 1];  // |F_h| (mirrored into out->sizes)
+  uint32_t tickets[DCI_MAX_LAYERS];   // dynamic tile tickets of the per-hop scans
+  unsigned long long counters[4];     // adj_hit, adj_miss, feat_hit, feat_miss
+  uint32_t hit_count;                 // feature route: hit list length
+  uint32_t miss_count;                // feature route: miss list length
+  int32_t status;
+  int32_t pad;
+};
+
+struct dci_ctx_impl;
+
+}  // namespace dci
+
+struct dci_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int64_t N = 0, E = 0;
+  int32_t D = 0, pitch = 0;  // pitch in floats (multiple of 4)
+  int32_t state = 0;
+  // host side
+  int64_t* h_indptr = nullptr;       // malloc'd copy
+  int32_t* h_idx_orig = nullptr;     // pinned+mapped, original CSC order
+  int32_t* h_idx_cur = nullptr;      // pinned+mapped, current order (== orig before fill)
+  float* h_feats = nullptr;          // pinned+mapped, [N][pitch]
+  // device aliases of the mapped host buffers (UVA)
+  const int32_t* u_idx_cur = nullptr;
+  const int32_t* u_idx_orig = nullptr;
+  const float* u_feats = nullptr;
+  // device
+  dci::DirEntry* d_dir = nullptr;
+  int32_t* d_acache = nullptr;
+  int64_t acache_len = 0;
+  float* d_fcache = nullptr;
+  int64_t fcache_rows = 0;
+  int32_t whole_fit = 0;
+  uint64_t c_adj = 0, c_feat = 0;
+  uint64_t presample_peak = 0;
+  uint64_t launches = 0;
+  // lazily created presample workspace + outputs
+  dci_workspace* pre_ws = nullptr;
+  int32_t pre_B = 0;
+  int32_t pre_L = 0;
+  int32_t pre_fan[DCI_MAX_LAYERS] = {0};
+  void* pre_out_mem = nullptr;
+  dci_batch_out pre_out{};
+};
+
+struct dci_workspace {
+  dci_ctx* ctx = nullptr;
+  int32_t max_batch = 0;
+  int32_t L = 0;
+  int32_t max_fan[DCI_MAX_LAYERS] = {0};
+  int64_t hop_cap[DCI_MAX_LAYERS + 1] = {0};
+  int64_t cand_cap = 0;     // max over hops of hop_cap[h] * f_h
+  int64_t tiles_cap = 0;    // sum over hops of ceil(hop_cap[h] / kScanTile)
+  int64_t tile_off[DCI_MAX_LAYERS] = {0};
+  // device buffers
+  int32_t* pos_of = nullptr;          // [N] node -> position in the batch (kPosEmpty)
+  int32_t* cand[2] = {nullptr, nullptr};  // ping-pong [cand_cap] padded candidates
+  int32_t* kcnt[2] = {nullptr, nullptr};  // ping-pong [max hop_cap] samples per dst
+  unsigned long long* tile_state = nullptr;  // [tiles_cap]
+  int64_t* hit_list = nullptr;        // [hop_cap[L]] packed (row i, slot)
+  int64_t* miss_list = nullptr;       // [hop_cap[L]] packed (row i, node v)
+  dci::BatchScalars* scal = nullptr;
+  int32_t* seeds_stage = nullptr;     // [max_batch] device copy for the host-seed variant
+  // streams / events
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
+  int32_t profiling = 0;
+  int32_t have_times = 0;
+};
+
+namespace dci {
+
+// ---- error plumbing (thread-local last error) ----
+void set_error(const std::string& msg);
+dci_status fail(dci_status s, const std::string& msg);
+dci_status cuda_fail(cudaError_t e, const char* what);
+
+#define DCI_CUDA(expr)                                                  \
+  do {                                                                  \
+    cudaError_t _e = (expr);                                            \
+    if (_e != cudaSuccess) return ::dci::cuda_fail(_e, #expr);          \
+  } while (0)
+
+// ---- kernel launchers (sample.cu / gather.cu / fill.cu) ----
+struct HopParams {
+  const int32_t* F_in;      // frontier read by this hop (seeds for hop 0)
+  int32_t* F;               // output frontier array (global ids)
+  int32_t hop;
+  int32_t f;                // fan-out of this hop
+  uint32_t pass;            // 0 inference, 1 presample
+  uint64_t seed;
+  int32_t B;                // batch size (hop 0 only)
+  int32_t* cand;            // [n_h * f]
+  int32_t* kcnt;            // [n_h]
+  // previous hop's relabel work, fused into this hop's sample kernel (h >= 1)
+  const int32_t* prev_cand;
+  const int32_t* prev_kcnt;
+  const int32_t* prev_bptr;
+  int32_t* prev_bsrc;
+  int32_t prev_f;
+  int32_t* bptr;            // this hop's block row pointers (written by the scan)
+  int32_t* edge_counts;     // presample only (nullable)
+};
+
+void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
+void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
+void launch_route(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const int32_t* F, const int32_t* last_cand,
+                  const int32_t* last_kcnt, const int32_t* last_bptr, int32_t* last_bsrc, int32_t last_f,
+                  int32_t* node_visits, cudaStream_t s);
+void launch_gather(dci_ctx* ctx, dci_workspace* ws, bool hits, const int32_t* F, int32_t L, float* X, int64_t ldx,
+                   cudaStream_t s);
+void launch_finish(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
+                   cudaStream_t s);
+
+// fill.cu
+dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
+                     uint64_t c_feat, cudaStream_t s);
+void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t s);
+
+inline int grid_for(const dci_ctx* ctx, int blocks_per_sm) { return ctx->num_sms * blocks_per_sm; }
+
+// Persistent grid: (resident blocks per SM for this kernel at this block size, capped) x SMs.
+int occupancy_blocks(const void* kernel, int block, int cap);
+template <class K>
+inline int persistent_grid(const dci_ctx* ctx, K kernel, int block, int cap = 8) {
+  return ctx->num_sms * occupancy_blocks(reinterpret_cast<const void*>(kernel), block, cap);
+}
+
+}  // namespace dci

@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by element, on the
+same seeded inputs.  Bit-exact for every output (integers and copied fp32 rows)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2503_01281_b200 as dci  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _graph(N, E, seed, D):
+    ip, ix = synth.rmat_csc(N, E, seed=seed)
+    return ip.numpy(), ix.numpy(), synth.features(N, D).numpy()
+
+
+def _assert_batch_equal(g, o, L, with_x=True):
+    assert g["status"] == 0
+    assert np.array_equal(g["sizes"], o.sizes), (g["sizes"], o.sizes)
+    assert np.array_equal(g["F"], o.F)
+    for h in range(L):
+        assert np.array_equal(g["bptr"][h], o.bptr[h]), h
+        assert np.array_equal(g["bsrc"][h], o.bsrc[h]), h
+    assert np.array_equal(g["counters"], o.counters), (g["counters"], o.counters)
+    if with_x:
+        assert np.array_equal(g["X"], o.X)
+
+
+def _run(ctx, ws, seeds, fan, seed, **kw):
+    out = dci.BatchOut(ctx, len(seeds), fan, **kw)
+    dci.sample_gather(ctx, ws, torch.from_numpy(np.ascontiguousarray(seeds, np.int32)).to(DEV), fan, seed, out)
+    return out.result()
+
+
+@pytest.fixture(scope="module")
+def small():
+    ip, ix, ft = _graph(5000, 60000, 21, 13)
+    ctx = dci.load_graph(ip, ix, ft)
+    return ip, ix, ft, ctx
+
+
+@pytest.mark.parametrize("fan", [(2, 2, 2), (15, 10, 5), (8, 4, 2), (1,), (32, 3), (5, 17, 9, 2)])
+def test_nocache_sampling_parity(small, fan):
+    """Before fill: original CSC, no cache (all misses), pass 0."""
+    ip, ix, ft, ctx = small
+    B = 100
+    ws = dci.workspace_create(ctx, B, fan)
+    for bi, seeds in enumerate(synth.inference_batches(ip, B)[:3]):
+        g = _run(ctx, ws, seeds, fan, 4 + bi)
+        o = oracle.sample_gather(ip, ix, ft, seeds, fan, 4 + bi)
+        _assert_batch_equal(g, o, len(fan))
+
+
+def test_ragged_empty_and_degree0(small):
+    ip, ix, ft, ctx = small
+    fan = (3, 3)
+    ws = dci.workspace_create(ctx, 300, fan)
+    zero = np.nonzero(np.diff(ip) == 0)[0].astype(np.int32)
+    for seeds in [synth.inference_batches(ip, 300)[-1], np.zeros(0, np.int32),
+                  np.concatenate([zero[:5], synth.inference_batches(ip, 7)[2]]).astype(np.int32)]:
+        g = _run(ctx, ws, seeds, fan, 9)
+        o = oracle.sample_gather(ip, ix, ft, seeds, fan, 9)
+        _assert_batch_equal(g, o, 2)
+
+
+def test_seed_errors_reported_in_status(small):
+    ip, ix, ft, ctx = small
+    fan = (2, 2)
+    ws = dci.workspace_create(ctx, 8, fan)
+    g = _run(ctx, ws, np.array([1, 2, 1], np.int32), fan, 1)
+    assert g["status"] == dci.EDUP
+    g = _run(ctx, ws, np.array([1, 5000], np.int32), fan, 1)
+    assert g["status"] == dci.ESEED
+    # the workspace stays clean: a valid batch afterwards still matches
+    seeds = synth.inference_batches(ip, 8)[0]
+    g = _run(ctx, ws, seeds, fan, 3)
+    _assert_batch_equal(g, oracle.sample_gather(ip, ix, ft, seeds, fan, 3), 2)
+
+
+def test_x_layouts(small):
+    """ldx = D (unaligned rows, scalar copy path) and X = None (sampling only)."""
+    ip, ix, ft, ctx = small
+    fan = (4, 4)
+    ws = dci.workspace_create(ctx, 50, fan)
+    seeds = synth.inference_batches(ip, 50)[1]
+    o = oracle.sample_gather(ip, ix, ft, seeds, fan, 5)
+    g = _run(ctx, ws, seeds, fan, 5, ldx=13)
+    _assert_batch_equal(g, o, 2)
+    g = _run(ctx, ws, seeds, fan, 5, with_x=False)
+    _assert_batch_equal(g, o, 2, with_x=False)
+
+
+def test_presample_counts_and_times(small):
+    ip, ix, ft, ctx0 = small
+    ctx = dci.load_graph(ip, ix, ft)
+    fan = (5, 3, 2)
+    pre = synth.presample_seeds(ip, 5, 90)
+    nv = torch.zeros(ctx.N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(ctx.E, dtype=torch.int32, device=DEV)
+    ts, tf = dci.presample(ctx, torch.from_numpy(pre).to(DEV), 90, fan, 3, nv, ec)
+    nv_o, ec_o = oracle.presample(ip, ix, pre, 90, fan, 3)
+    assert np.array_equal(nv.cpu().numpy(), nv_o)
+    assert np.array_equal(ec.cpu().numpy(), ec_o)
+    assert len(ts) == 5 and np.all(ts > 0) and np.all(tf > 0)
+    # accumulate: a second call doubles the counts
+    dci.presample(ctx, torch.from_numpy(pre).to(DEV), 90, fan, 3, nv, ec)
+    assert np.array_equal(nv.cpu().numpy(), 2 * nv_o)
+
+
+@pytest.mark.parametrize("r", [0.0, 0.25, 0.5, 0.75, 1.0])
+def test_m1_fill_and_cached_parity(r):
+    """Config M1 (BASELINE configs[0]) at explicit split ratios: every fill branch (SURVEY
+    A.6) — no adjacency cache, partial node-major prefix, whole fit, top-k tie cut."""
+    cfg = synth.CONFIGS["M1"]
+    ip, ix, ft = _graph(cfg.N, cfg.E, synth.GRAPH_SEED, cfg.D)
+    ctx = dci.load_graph(ip, ix, ft)
+    fan, B = cfg.fanouts, cfg.batch
+    pre = synth.presample_seeds(ip, 8, B)
+    nv = torch.zeros(ctx.N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(ctx.E, dtype=torch.int32, device=DEV)
+    ts, tf = dci.presample(ctx, torch.from_numpy(pre).to(DEV), B, fan, synth.PRESAMPLE_SEED, nv, ec)
+    nv_o, ec_o = oracle.presample(ip, ix, pre, B, fan, synth.PRESAMPLE_SEED)
+    assert np.array_equal(nv.cpu().numpy(), nv_o) and np.array_equal(ec.cpu().numpy(), ec_o)
+    Cb = synth.parse_budget(cfg.budget, synth.data_bytes(cfg.N, cfg.E, cfg.D))
+    num, den = int(round(r * 100)), 100
+    c_adj, c_feat = dci.allocate(ctx, Cb, ts, tf, ratio=(num, den))
+    assert (c_adj, c_feat) == oracle.allocate(Cb, ts, tf, ratio=(num, den))
+    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    st = dci.cache_state(ctx)
+    R, cl, co, ac = oracle.adj_fill(ip, ix, ec_o, c_adj)
+    pitch = cfg.pitch_floats()
+    slot_o, adm = oracle.feat_fill(nv_o, c_feat // (4 * pitch))
+    assert np.array_equal(st["indices_cur"], R)
+    assert np.array_equal(st["cached_len"], cl)
+    assert np.array_equal(st["slot_of"], slot_o)
+    # cache contents: per-node prefixes (layout in id order on the GPU) and feature rows
+    for v in np.nonzero(cl)[0]:
+        a = st["cache_off"][v]
+        assert np.array_equal(st["acache"][a:a + cl[v]], ac[co[v]:co[v] + cl[v]])
+    assert st["info"]["adj_elems"] == int(cl.sum())
+    assert np.array_equal(st["fcache"][:, : cfg.D], ft[adm])
+    ws = dci.workspace_create(ctx, B, fan)
+    for seeds in synth.inference_batches(ip, B)[:6]:
+        g = _run(ctx, ws, seeds, fan, synth.SAMPLE_SEED)
+        o = oracle.sample_gather(ip, R, ft, seeds, fan, synth.SAMPLE_SEED, cl, slot_o)
+        _assert_batch_equal(g, o, 3)
+
+
+def test_concurrent_workspaces_on_streams(small):
+    """Several batches in flight on distinct streams/workspaces give the serial results."""
+    ip, ix, ft, ctx = small
+    fan = (10, 5)
+    B = 128
+    batches = synth.inference_batches(ip, B)[:6]
+    wss = [dci.workspace_create(ctx, B, fan) for _ in range(3)]
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = []
+    for i, seeds in enumerate(batches):
+        out = dci.BatchOut(ctx, len(seeds), fan)
+        sd = torch.from_numpy(seeds).to(DEV)
+        torch.cuda.synchronize()
+        dci.sample_gather(ctx, wss[i % 3], sd, fan, 11, out, stream=streams[i % 3])
+        outs.append(out)
+    torch.cuda.synchronize()
+    for seeds, out in zip(batches, outs):
+        _assert_batch_equal(out.result(), oracle.sample_gather(ip, ix, ft, seeds, fan, 11), 2)
+
+
+def test_host_seed_variant(small):
+    ip, ix, ft, ctx = small
+    fan = (6, 3)
+    B = 64
+    ws = dci.workspace_create(ctx, B, fan)
+    seeds = synth.inference_batches(ip, B)[3]
+    out = dci.BatchOut(ctx, B, fan)
+    sh = torch.from_numpy(seeds).pin_memory()
+    sizes = torch.zeros(3, dtype=torch.int64).pin_memory()
+    cnt = torch.zeros(4, dtype=torch.int64).pin_memory()
+    stt = torch.zeros(1, dtype=torch.int32).pin_memory()
+    dci.sample_gather_host(ctx, ws, sh, fan, 2, out, sizes, cnt, stt)
+    torch.cuda.synchronize()
+    o = oracle.sample_gather(ip, ix, ft, seeds, fan, 2)
+    _assert_batch_equal(out.result(), o, 2)
+    assert sizes.numpy().tolist() == o.sizes.tolist()
+    assert cnt.numpy().astype(np.uint64).tolist() == o.counters.tolist() and stt.item() == 0
