@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""DCI hot-path benchmark: seeds/s for sample+gather (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config M2] [--impl reference]
+
+A step is one mini-batch through the whole hot path (S5 sample x L hops -> S6 dedup/relabel
+-> S7 feature route -> S8 gather) on synthetic inputs already resident in HBM; several
+steps are in flight on distinct streams/workspaces.  Setup (graph generation, S0 load,
+S1 presample, S2 allocate, S3/S4 fill) happens before the timed region and is reported
+as preprocessing.  Multi-GPU (torchrun, one rank per GPU): rank g runs batches g, g+G, ...
+of the global list with replicated caches; presample counts are all-reduced over NCCL.
+
+rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the reference arm
+for this paper-only tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "seeds/s for sample+gather"
+UNIT = "seeds/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="M2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--inflight", type=int, default=3, help="workspaces/streams in flight")
+    ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
+    ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle wall time for cpu_baseline")
+    ap.add_argument("--no-check", action="store_true", help="skip the bit-exact spot check vs the oracle")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/check)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while the region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx, self.rows, self.proc, self.th = gpu_index, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for n, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------------------ inputs
+def make_inputs(cfg, device):
+    import torch
+    ip_d, ix_d = synth.rmat_csc(cfg.N, cfg.E, seed=synth.GRAPH_SEED, device=device)
+    ip = ip_d.cpu().numpy()
+    ix = ix_d.cpu().numpy()
+    del ip_d, ix_d
+    ft_d = synth.features(cfg.N, cfg.D, device=device)
+    ft = ft_d.cpu().numpy()
+    del ft_d
+    torch.cuda.empty_cache()
+    return ip, ix, ft
+
+
+# ------------------------------------------------------------------------------ oracle (cpu)
+def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_results=None):
+    """Time the oracle as it stands on host cores: its own presample + fill (reported), then
+    inference batches spread over `threads` threads (ctypes releases the GIL), until about
+    `seconds` of wall time.  Optionally checks the GPU results of the first batches."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    B, fan = cfg.batch, cfg.fanouts
+    t0 = time.time()
+    pre = synth.presample_seeds(ip, 8, B)
+    nv, ec = oracle.presample(ip, ix, pre, B, fan, synth.PRESAMPLE_SEED)
+    R, cl, co, ac = oracle.adj_fill(ip, ix, ec, c_adj)
+    slot, _ = oracle.feat_fill(nv, c_feat // (4 * cfg.pitch_floats()))
+    prep_s = time.time() - t0
+    check = None
+    if gpu_results:
+        ok = True
+        for seeds, g in gpu_results:
+            o = oracle.sample_gather(ip, R, ft, seeds, fan, synth.SAMPLE_SEED, cl, slot)
+            ok &= bool(np.array_equal(g["F"], o.F) and np.array_equal(g["counters"], o.counters)
+                       and all(np.array_equal(g["bsrc"][h], o.bsrc[h]) and np.array_equal(g["bptr"][h], o.bptr[h])
+                               for h in range(len(fan))) and np.array_equal(g["X"], o.X))
+        check = {"batches": len(gpu_results), "bit_exact": ok}
+    # calibrate: one batch single-threaded
+    t1 = time.time()
+    oracle.sample_gather(ip, R, ft, batches[0], fan, synth.SAMPLE_SEED, cl, slot)
+    one = max(time.time() - t1, 1e-3)
+    nb = max(threads, int(seconds * threads / one))
+    nb = min(nb, 4 * threads * max(1, len(batches) // threads + 1))
+    work = [batches[i % len(batches)] for i in range(nb)]
+    t2 = time.time()
+    def one_batch(s):
+        oracle.sample_gather(ip, R, ft, s, fan, synth.SAMPLE_SEED, cl, slot)  # result dropped (memory)
+        return len(s)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one_batch, work))
+    wall = time.time() - t2
+    seeds = sum(len(s) for s in work)
+    return {"value": seeds / wall, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{nb} batches of {B} seeds ({cfg.name}, {','.join(map(str, fan))}) after the oracle's own "
+                      f"presample+fill ({prep_s:.1f} s, not timed); {wall:.1f} s wall on {threads} threads"}, check
+
+
+def run_reference(args):
+    """--impl reference: the oracle as the reference arm (rank 0 only under torchrun)."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    import torch
+    # same generator and device as our arm, so both arms see the identical graph
+    gen_dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))) if torch.cuda.is_available() else "cpu"
+    if gen_dev != "cpu":
+        ip, ix, ft = make_inputs(cfg, gen_dev)
+    else:
+        ip, ix = synth.rmat_csc(cfg.N, cfg.E, seed=synth.GRAPH_SEED)
+        ip, ix = ip.numpy(), ix.numpy()
+        ft = synth.features(cfg.N, cfg.D).numpy()
+    C = synth.parse_budget(args.budget or cfg.budget, synth.data_bytes(cfg.N, cfg.E, cfg.D))
+    if C == 0:  # auto: the GPU's budget holds every byte of this workload
+        C = 2 * synth.data_bytes(cfg.N, cfg.E, cfg.D)
+    import oracle
+    ratio = (int(round(args.ratio * 1000)), 1000) if args.ratio is not None else (1, 2)
+    c_adj, c_feat = oracle.allocate(C, ratio=ratio)
+    batches = synth.inference_batches(ip, cfg.batch)
+    threads = os.cpu_count() or 1
+    per_step = max(1, args.cpu_seconds / max(args.steps + args.warmup, 1))
+    res, _ = oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, per_step * args.steps, threads)
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cfg.batch / res["value"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": cfg.batch, "fanouts": list(cfg.fanouts),
+                       "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget},
+            "cpu_baseline": res, "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import paper_2503_01281_b200 as dci
+    from paper_2503_01281_b200 import parallel
+
+    rank, world, local = parallel.init("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = synth.CONFIGS[args.config]
+    B, fan, L = cfg.batch, cfg.fanouts, len(cfg.fanouts)
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
+
+    clk = ClockSampler(local)
+    if rank == 0:
+        clk.start()
+    t0 = time.time()
+    ip, ix, ft = make_inputs(cfg, dev)
+    t_gen = time.time() - t0
+    log(f"[bench] {cfg.name}: N={cfg.N} E={cfg.E} D={cfg.D} generated in {t_gen:.1f}s")
+
+    # ---- S0 load ----
+    t1 = time.time()
+    ctx = dci.load_graph(ip, ix, ft, device=local)
+    t_load = time.time() - t1
+
+    # ---- S1 presample (global list of 8 batches, sharded), C1 allreduce ----
+    t2 = time.time()
+    pre = synth.presample_seeds(ip, 8, B)
+    pre_batches = [pre[i * B:(i + 1) * B] for i in range(8)]
+    nv = torch.zeros(cfg.N, dtype=torch.int32, device=dev)
+    ec = torch.zeros(cfg.E, dtype=torch.int32, device=dev)
+    ts_all, tf_all = [], []
+    for pb in parallel.shard(pre_batches, rank, world):
+        ts, tf = dci.presample(ctx, torch.from_numpy(pb).to(dev), B, fan, synth.PRESAMPLE_SEED, nv, ec)
+        ts_all += ts.tolist()
+        tf_all += tf.tolist()
+    S, F = parallel.allreduce_presample(nv, ec, ts_all, tf_all)
+    torch.cuda.synchronize()
+    t_pre = time.time() - t2
+
+    # ---- S2 allocate (Eq. 1) + S3/S4 fill ----
+    t3 = time.time()
+    C = synth.parse_budget(args.budget or cfg.budget, synth.data_bytes(cfg.N, cfg.E, cfg.D))
+    ratio = (int(round(args.ratio * 1000)), 1000) if args.ratio is not None else None
+    c_adj, c_feat = dci.allocate(ctx, C, [S], [F], ratio=ratio)
+    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    torch.cuda.synchronize()
+    t_fill = time.time() - t3
+    info = dci.cache_info(ctx)
+    log(f"[bench] load {t_load:.2f}s presample {t_pre:.2f}s fill {t_fill:.2f}s  C_adj={c_adj} C_feat={c_feat} "
+        f"adj_elems={info['adj_elems']}/{cfg.E} feat_rows={info['feat_rows']}/{cfg.N}")
+    del nv, ec
+    torch.cuda.empty_cache()
+
+    # ---- inference batches (sharded), inputs resident in HBM ----
+    batches = parallel.shard(synth.inference_batches(ip, B), rank, world)
+    batches = [b for b in batches if len(b) == B] or batches
+    seeds_dev = [torch.from_numpy(b).to(dev) for b in batches]
+    nws = max(1, args.inflight)
+    wss = [dci.workspace_create(ctx, B, fan) for _ in range(nws)]
+    outs = [dci.BatchOut(ctx, B, fan) for _ in range(nws)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(nws)]
+    for w in wss:
+        w.set_profiling(True)
+    nsteps_total = args.warmup + args.steps
+    sizes_host = torch.zeros((nsteps_total, L + 1), dtype=torch.int64).pin_memory()
+    cnt_host = torch.zeros((nsteps_total, 4), dtype=torch.int64).pin_memory()
+    gather_ms = np.zeros(nsteps_total)
+    sample_ms = np.zeros(nsteps_total)
+    last_on_ws = [-1] * nws
+
+    def harvest(w):
+        j = last_on_ws[w]
+        if j >= 0:
+            s_ms, g_ms = wss[w].stage_ms()
+            sample_ms[j], gather_ms[j] = s_ms, g_ms
+
+    def step(i):
+        w = i % nws
+        harvest(w)
+        sd = seeds_dev[i % len(seeds_dev)]
+        with torch.cuda.stream(streams[w]):
+            dci.sample_gather(ctx, wss[w], sd, fan, synth.SAMPLE_SEED, outs[w], stream=streams[w])
+            sizes_host[i].copy_(outs[w].sizes, non_blocking=True)
+            cnt_host[i].copy_(outs[w].counters, non_blocking=True)
+        last_on_ws[w] = i
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    parallel.barrier(local)
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream(dev)
+    ev_start = torch.cuda.Event(enable_timing=True)
+    ev_end = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    ev_start.record(main)
+    for s in streams:
+        s.wait_event(ev_start)
+    for i in range(args.warmup, nsteps_total):
+        step(i)
+    for s in streams:
+        e = torch.cuda.Event()
+        e.record(s)
+        main.wait_event(e)
+    ev_end.record(main)
+    torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    for w in range(nws):
+        harvest(w)
+    ms_local = ev_start.elapsed_time(ev_end)
+    parallel.barrier(local)
+    ms = parallel.max_over_ranks(ms_local, device=dev)
+    seeds_local = sum(len(seeds_dev[i % len(seeds_dev)]) for i in range(args.warmup, nsteps_total))
+    timed = slice(args.warmup, nsteps_total)
+    fl = sizes_host[timed, L].numpy().astype(np.float64)
+    D = cfg.D
+    alg_bytes = fl * (8.0 * D + 4.0)  # per gather launch: read row + write row + 4 B slot lookup
+    tot = parallel.sum_over_ranks([seeds_local, launches, fl.sum(), alg_bytes.sum(), gather_ms[timed].sum(),
+                                   sample_ms[timed].sum()], device=dev)
+    seeds_all = tot[0]
+    cn = parallel.sum_over_ranks(cnt_host[timed].numpy().sum(axis=0), device=dev)
+    hit_rates = {"adj_hit_rate": cn[0] / max(1, cn[0] + cn[1]), "feat_hit_rate": cn[2] / max(1, cn[2] + cn[3]),
+                 "adj_accesses_per_seed": (cn[0] + cn[1]) / max(1, seeds_all)}
+    value = seeds_all / (ms / 1e3)
+
+    if args.profile_only:
+        clk.stop()
+        print(json.dumps({"profile_only": True, "value": seeds_all / (ms / 1e3), "ms_per_step": ms / args.steps,
+                          **hit_rates}))
+        return
+    # ---- e2e: the same steps through the C-ABI with host seeds + D2H results ----
+    pinned_seeds = [torch.from_numpy(b).pin_memory() for b in batches]
+    e_sizes = torch.zeros((nws, L + 1), dtype=torch.int64).pin_memory()
+    e_cnt = torch.zeros((nws, 4), dtype=torch.int64).pin_memory()
+    e_st = torch.zeros((nws, 1), dtype=torch.int32).pin_memory()
+    for w in wss:
+        w.set_profiling(False)
+
+    def estep(i):
+        w = i % nws
+        dci.sample_gather_host(ctx, wss[w], pinned_seeds[i % len(pinned_seeds)], fan, synth.SAMPLE_SEED, outs[w],
+                               e_sizes[w], e_cnt[w], e_st[w], stream=streams[w])
+
+    for i in range(args.warmup):
+        estep(i)
+    torch.cuda.synchronize()
+    parallel.barrier(local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for s in streams:
+        s.wait_event(e0)
+    for i in range(args.warmup, nsteps_total):
+        estep(i)
+    for s in streams:
+        e = torch.cuda.Event()
+        e.record(s)
+        main.wait_event(e)
+    e1.record(main)
+    torch.cuda.synchronize()
+    ems = parallel.max_over_ranks(e0.elapsed_time(e1), device=dev)
+    clocks = clk.stop() if rank == 0 else None
+    if clocks is not None:
+        clocks["window"] = "sampled every 100 ms from input generation through the e2e region"
+
+    e_value = seeds_all / (ems / 1e3)
+
+    if rank != 0:
+        parallel.barrier(local)
+        return
+    hbm_peak, peak_kind = measured_peaks()
+    achieved_gbs = tot[3] / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None
+    avg_fl = tot[2] / max(1, args.steps * world)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "gather_traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile)).get(cfg.name)
+        if tj:
+            traffic = tj.get("dram_bytes_per_row", 0) * avg_fl or None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
+        "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B, "fanouts": list(fan),
+                   "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
+                   "ratio": args.ratio, "parallelism": f"dp{world} (replicated caches)", "inflight": nws,
+                   "l2": "inputs larger than L2 (feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
+                         % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
+                            avg_fl * D * 4 / 1e6)},
+        "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
+                "d2h_bytes_per_step": 8 * (L + 1) + 8 * 4 + 4},
+        "gpu_launches": int(tot[1]),
+        "roofline": {"bound": "hbm", "kernel": "k_gather_v4 (feature gather, S8)", "achieved": achieved_gbs,
+                     "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved_gbs / hbm_peak) if achieved_gbs else None, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": float(alg_bytes.mean()),
+                     "avg_gather_ms": tot[4] / max(1, args.steps * world),
+                     "avg_sample_ms": tot[5] / max(1, args.steps * world)},
+        "clocks": clocks,
+        "stats": {"avg_F_L": avg_fl, "F_L_per_seed": avg_fl / B, **hit_rates,
+                  "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre, "fill": t_fill},
+                  "c_adj": c_adj, "c_feat": c_feat, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
+                  "e2e_ms_per_step": ems / args.steps},
+    }
+    if not args.profile_only and world == 1 and not args.no_cpu_baseline:
+        gpu_results = None
+        if not args.no_check:
+            gpu_results = []
+            for b in batches[:2]:
+                o = dci.BatchOut(ctx, B, fan)
+                dci.sample_gather(ctx, wss[0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
+                gpu_results.append((b, o.result()))
+        res, check = oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, args.cpu_seconds, os.cpu_count() or 1,
+                                gpu_results)
+        line["cpu_baseline"] = res
+        if check:
+            line["parity_check"] = check
+    print(json.dumps(line), flush=True)
+    parallel.barrier(local)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

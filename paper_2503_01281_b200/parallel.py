@@ -1,0 +1,85 @@
+"""Multi-GPU plumbing for the DCI hot path.
+
+Mini-batches are independent and the sampling key excludes the batch index and the GPU
+(reading C4), so the path shards with no data-path collective: rank g takes batches
+g, g+G, ... ("weak" scaling, one replica of both caches per GPU).  The only real exchange
+is once per run, after pre-sampling: every rank presamples its
+share of the global presample batches, then the per-node visit counts, per-element access
+counts and the two stage-time sums are all-reduced (SUM) so every rank computes the same
+Eq. (1) split and the same fills as a single GPU would.
+
+torch.distributed is the transport (NCCL for CUDA tensors, gloo for CPU tensors in tests).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+
+def dist_env():
+    """(rank, world_size, local_rank) from the torchrun environment (defaults: single process)."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init(backend: str = "nccl"):
+    """Initialise the default process group when launched under torchrun (WORLD_SIZE > 1)."""
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group(backend=backend, rank=rank, world_size=world)
+    return rank, world, local
+
+
+def shard(items, rank: int, world: int):
+    """Round-robin partition of the global batch list: rank g gets items g, g+G, ..."""
+    return list(items)[rank::world]
+
+
+def allreduce_presample(node_visits, edge_counts, t_sample_ns, t_feature_ns, group=None):
+    """C1: SUM-allreduce the presample histograms in place and return the global stage-time
+    sums (S, F) for Eq. (1).  node_visits / edge_counts are int32 tensors on the rank's device
+    (NCCL) or CPU (gloo).  Times are this rank's per-batch uint64 ns arrays."""
+    import torch
+    import torch.distributed as dist
+    S = int(np.asarray(t_sample_ns, np.uint64).sum())
+    F = int(np.asarray(t_feature_ns, np.uint64).sum())
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return S, F
+    dist.all_reduce(node_visits, op=dist.ReduceOp.SUM, group=group)
+    if edge_counts is not None and edge_counts.numel():
+        dist.all_reduce(edge_counts, op=dist.ReduceOp.SUM, group=group)
+    t = torch.tensor([S, F], dtype=torch.int64, device=node_visits.device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t[0].item()), int(t[1].item())
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Max of a per-rank scalar (timing is the max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def sum_over_ranks(values, device=None, group=None):
+    """C2: SUM of per-rank counters (seeds processed, hits/misses, bytes) at the end of a run."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(np.asarray(values, np.float64), dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t.cpu().numpy()
+
+
+def barrier(device_index=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        if dist.get_backend() == "nccl" and device_index is not None:
+            dist.barrier(device_ids=[device_index])
+        else:
+            dist.barrier()

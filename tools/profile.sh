@@ -1,0 +1,14 @@
+#!/bin/bash
+# ncu evidence for the hot path (run under gpurun; 1 GPU).  Usage: tools/profile.sh <tag> [bench args...]
+tag=${1:-run}; shift
+out=gpurun_out/prof_$tag; mkdir -p $out
+args="--profile-only --steps 30 --warmup 3 --no-cpu-baseline --inflight 1 $@"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
+    python bench.py $args > $out/launches.stdout 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_gather_v4 -s 3 -c 2 -o $out/gather \
+    python bench.py $args > $out/gather.stdout 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_sample_hop -s 9 -c 3 -o $out/sample \
+    python bench.py $args > $out/sample.stdout 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_scan_hop -s 9 -c 3 -o $out/scan \
+    python bench.py $args > $out/scan.stdout 2>&1
+ls -la $out
