@@ -299,6 +299,7 @@ def run_ours(args):
     ev_start = torch.cuda.Event(enable_timing=True)
     ev_end = torch.cuda.Event(enable_timing=True)
     launches0 = ctx.launches
+    torch.cuda.nvtx.range_push("timed")
     ev_start.record(main)
     for s in streams:
         s.wait_event(ev_start)
@@ -310,6 +311,7 @@ def run_ours(args):
         main.wait_event(e)
     ev_end.record(main)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     launches = ctx.launches - launches0
     for w in range(nws):
         harvest(w)

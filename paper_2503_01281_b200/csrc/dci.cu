@@ -29,8 +29,6 @@ dci_status cuda_fail(cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? DCI_ENOMEM : DCI_ECUDA;
 }
 
-void launch_fill_i32(dci_ctx* ctx, int32_t* p, int64_t n, int32_t val, cudaStream_t s);
-
 int occupancy_blocks(const void* kernel, int block, int cap) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
@@ -102,6 +100,10 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   if (out->X && out->ldx < ctx->D) return fail(DCI_EINVAL, "ldx < D");
 
   DeviceGuard g(ctx->device);
+  if (++ws->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
+    DCI_CUDA(cudaMemsetAsync(ws->pos_of, 0, sizeof(unsigned long long) * ctx->N, s));
+    ws->epoch = 1;
+  }
   const bool prof = ws->profiling || pass == 1;
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[0], s));
   HopParams prev{};
@@ -130,20 +132,8 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     prev = p;
   }
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[1], s));
-  launch_route(ctx, ws, L, B, out->frontier, prev.cand, prev.kcnt, out->bptr[L - 1], out->bsrc[L - 1], prev.f,
-               node_visits, s);
-  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[2], s));
-  if (out->X) {
-    // misses (PCIe/UVA) on the auxiliary stream, hits (HBM) on the caller's stream
-    DCI_CUDA(cudaEventRecord(ws->ev_fork, s));
-    DCI_CUDA(cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0));
-    launch_gather(ctx, ws, false, out->frontier, L, out->X, out->ldx, ws->aux);
-    launch_gather(ctx, ws, true, out->frontier, L, out->X, out->ldx, s);
-    DCI_CUDA(cudaEventRecord(ws->ev_join, ws->aux));
-    DCI_CUDA(cudaStreamWaitEvent(s, ws->ev_join, 0));
-  }
+  launch_gather_fused(ctx, ws, L, B, out, prev, node_visits, s);
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], s));
-  launch_finish(ctx, ws, L, B, out, s);
   ws->have_times = prof ? 1 : 0;
   DCI_CUDA(cudaGetLastError());
   return DCI_OK;
@@ -297,12 +287,14 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
     w->tile_off[h] = w->tiles_cap;
     w->tiles_cap += (w->hop_cap[h] + kScanTile - 1) / kScanTile + 1;
   }
+  w->tile_off[L] = w->tiles_cap;
   auto bail = [&](cudaError_t e, const char* what) {
     dci_workspace_destroy(w);
     return cuda_fail(e, what);
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&w->pos_of, sizeof(int32_t) * ctx->N)) != cudaSuccess) return bail(e, "cudaMalloc(pos_of)");
+  if ((e = cudaMalloc(&w->pos_of, sizeof(unsigned long long) * ctx->N)) != cudaSuccess)
+    return bail(e, "cudaMalloc(pos_of)");
   for (int i = 0; i < 2; ++i) {
     if ((e = cudaMalloc(&w->cand[i], sizeof(int32_t) * std::max<int64_t>(w->cand_cap, 1))) != cudaSuccess)
       return bail(e, "cudaMalloc(cand)");
@@ -311,18 +303,11 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   }
   if ((e = cudaMalloc(&w->tile_state, sizeof(unsigned long long) * w->tiles_cap)) != cudaSuccess)
     return bail(e, "cudaMalloc(tile_state)");
-  if ((e = cudaMalloc(&w->hit_list, sizeof(int64_t) * std::max<int64_t>(w->hop_cap[L], 1))) != cudaSuccess)
-    return bail(e, "cudaMalloc(hit_list)");
-  if ((e = cudaMalloc(&w->miss_list, sizeof(int64_t) * std::max<int64_t>(w->hop_cap[L], 1))) != cudaSuccess)
-    return bail(e, "cudaMalloc(miss_list)");
   if ((e = cudaMalloc(&w->scal, sizeof(BatchScalars))) != cudaSuccess) return bail(e, "cudaMalloc(scal)");
   if ((e = cudaMalloc(&w->seeds_stage, sizeof(int32_t) * max_batch)) != cudaSuccess) return bail(e, "cudaMalloc");
-  if ((e = cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "stream");
-  if ((e = cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
-  if ((e = cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   for (int i = 0; i < 4; ++i)
     if ((e = cudaEventCreate(&w->ev_t[i])) != cudaSuccess) return bail(e, "event");
-  launch_fill_i32(ctx, w->pos_of, ctx->N, kPosEmpty, 0);
+  cudaMemset(w->pos_of, 0, sizeof(unsigned long long) * ctx->N);
   cudaMemset(w->tile_state, 0, sizeof(unsigned long long) * w->tiles_cap);
   cudaMemset(w->scal, 0, sizeof(BatchScalars));
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "workspace init");
@@ -340,13 +325,8 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     cudaFree(w->kcnt[i]);
   }
   cudaFree(w->tile_state);
-  cudaFree(w->hit_list);
-  cudaFree(w->miss_list);
   cudaFree(w->scal);
   cudaFree(w->seeds_stage);
-  if (w->aux) cudaStreamDestroy(w->aux);
-  if (w->ev_fork) cudaEventDestroy(w->ev_fork);
-  if (w->ev_join) cudaEventDestroy(w->ev_join);
   for (int i = 0; i < 4; ++i)
     if (w->ev_t[i]) cudaEventDestroy(w->ev_t[i]);
   delete w;
@@ -445,9 +425,8 @@ dci_status dci_presample(dci_ctx* ctx, const int32_t* seeds, int64_t num_seeds, 
     ctx->pre_L = L;
     for (int i = 0; i < L; ++i) ctx->pre_fan[i] = fanouts[i];
     // predicted peak per-batch workspace for the auto budget: outputs + scratch
-    uint64_t ws_bytes = bytes + sizeof(int32_t) * (uint64_t)ctx->N +
-                        sizeof(int32_t) * 2 * (uint64_t)(ctx->pre_ws->cand_cap + caps[L]) +
-                        sizeof(int64_t) * 2 * (uint64_t)caps[L];
+    uint64_t ws_bytes = bytes + sizeof(unsigned long long) * (uint64_t)ctx->N +
+                        sizeof(int32_t) * 2 * (uint64_t)(ctx->pre_ws->cand_cap + caps[L]);
     ctx->presample_peak = std::max<uint64_t>(ctx->presample_peak, ws_bytes);
   }
   int32_t status = 0;
@@ -571,7 +550,7 @@ dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* ga
   DeviceGuard g(ws->ctx->device);
   DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
   if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, ws->ev_t[0], ws->ev_t[1]));
-  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[2], ws->ev_t[3]));
+  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[1], ws->ev_t[3]));
   return DCI_OK;
 }
 

@@ -24,7 +24,6 @@ struct __align__(16) DirEntry {
 };
 static_assert(sizeof(DirEntry) == 32, "directory entry must be one 32-byte sector");
 
-constexpr int32_t kPosEmpty = 0x7FFFFFFF;  // node->position table "absent"
 constexpr int kScanTile = 256;             // dst nodes per tile of the per-hop scan
 
 // Device-side per-batch scalars live in one small struct (workspace memory).
@@ -32,10 +31,8 @@ struct BatchScalars {
   int64_t sizes[DCI_MAX_LAYERS + 1];  // |F_h| (mirrored into out->sizes)
   uint32_t tickets[DCI_MAX_LAYERS];   // dynamic tile tickets of the per-hop scans
   unsigned long long counters[4];     // adj_hit, adj_miss, feat_hit, feat_miss
-  uint32_t hit_count;                 // feature route: hit list length
-  uint32_t miss_count;                // feature route: miss list length
+  uint32_t done;                      // blocks of the gather kernel that have finished
   int32_t status;
-  int32_t pad;
 };
 
 struct dci_ctx_impl;
@@ -84,19 +81,18 @@ struct dci_workspace {
   int64_t hop_cap[DCI_MAX_LAYERS + 1] = {0};
   int64_t cand_cap = 0;     // max over hops of hop_cap[h] * f_h
   int64_t tiles_cap = 0;    // sum over hops of ceil(hop_cap[h] / kScanTile)
-  int64_t tile_off[DCI_MAX_LAYERS] = {0};
+  int64_t tile_off[DCI_MAX_LAYERS + 1] = {0};
   // device buffers
-  int32_t* pos_of = nullptr;          // [N] node -> position in the batch (kPosEmpty)
+  // [N] node -> position tag of the current batch: epoch << 32 | ~position (entries with an
+  // older epoch read as absent, so the table is never cleared between batches)
+  unsigned long long* pos_of = nullptr;
+  uint32_t epoch = 0;
   int32_t* cand[2] = {nullptr, nullptr};  // ping-pong [cand_cap] padded candidates
   int32_t* kcnt[2] = {nullptr, nullptr};  // ping-pong [max hop_cap] samples per dst
   unsigned long long* tile_state = nullptr;  // [tiles_cap]
-  int64_t* hit_list = nullptr;        // [hop_cap[L]] packed (row i, slot)
-  int64_t* miss_list = nullptr;       // [hop_cap[L]] packed (row i, node v)
   dci::BatchScalars* scal = nullptr;
   int32_t* seeds_stage = nullptr;     // [max_batch] device copy for the host-seed variant
-  // streams / events
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // stage events
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
   int32_t profiling = 0;
   int32_t have_times = 0;
@@ -138,13 +134,8 @@ struct HopParams {
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
-void launch_route(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const int32_t* F, const int32_t* last_cand,
-                  const int32_t* last_kcnt, const int32_t* last_bptr, int32_t* last_bsrc, int32_t last_f,
-                  int32_t* node_visits, cudaStream_t s);
-void launch_gather(dci_ctx* ctx, dci_workspace* ws, bool hits, const int32_t* F, int32_t L, float* X, int64_t ldx,
-                   cudaStream_t s);
-void launch_finish(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
-                   cudaStream_t s);
+void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
+                         const HopParams& last, int32_t* node_visits, cudaStream_t s);
 
 // fill.cu
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,

@@ -35,11 +35,6 @@ __global__ void k_build_directory(const int64_t* __restrict__ indptr, int64_t N,
   }
 }
 
-__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t val) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = val;
-}
-
 __global__ void k_max_i32(const int32_t* __restrict__ a, int64_t n, int32_t* out) {
   int32_t m = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -409,11 +404,6 @@ dci_status radix_select(dci_ctx* ctx, const K& kf, int64_t N, unsigned long long
 
 void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t s) {
   k_build_directory<<<grid_for(ctx, 4), 256, 0, s>>>(d_indptr, ctx->N, ctx->d_dir);
-  ++ctx->launches;
-}
-
-void launch_fill_i32(dci_ctx* ctx, int32_t* p, int64_t n, int32_t val, cudaStream_t s) {
-  k_fill_i32<<<grid_for(ctx, 4), 256, 0, s>>>(p, n, val);
   ++ctx->launches;
 }
 

@@ -1,8 +1,12 @@
-// S8 feature gather: X[i] = fcache[slot] on a feature-cache hit (HBM -> HBM) and
-// X[i] = feats[v] on a miss (pinned host -> HBM through UVA zero-copy).  One warp per
-// row; every lane issues all of its 16-byte loads for the row before any store, so each
-// warp keeps a whole row (up to 32*VPL*16 B) in flight; the grid is persistent (a multiple
-// of the SM count) and walks the route list written by k_route.
+// S7 + S8 of the hot path, one kernel per batch:
+//  - relabel of the last hop's candidates into its block CSR (table tag -> local id)
+//  - feature-cache route inline through the remap table: slot = dir[F[i]].slot
+//  - feature gather: X[i] = fcache[slot] on a hit (HBM -> HBM) or feats[v] on a
+//    miss (pinned host -> HBM, UVA zero-copy), one warp per row, every lane issuing all of
+//    its 16-byte loads before any store; the next row's (F, slot) lookups are prefetched
+//  - presample: node_visits[v] += 1 (C7)
+//  - the last block to finish publishes sizes / counters / status and resets the
+//    workspace scalars for the next batch.
 #include <cuda_runtime.h>
 
 #include "dci_internal.cuh"
@@ -24,82 +28,175 @@ __device__ __forceinline__ void st_v4(int4* p, const int4& v) {
                : "memory");
 }
 
-struct GatherArgs {
-  const int64_t* list;        // packed (row i << 32 | source row)
-  const uint32_t* count;      // device list length
-  const float* src;           // fcache (hits) or the mapped host feature table (misses)
-  int32_t pitch;              // floats per source row (multiple of 4)
-  float* X;
-  int64_t ldx;                // floats per X row
+struct FusedArgs {
+  const DirEntry* dir;
+  const unsigned long long* pos_of;
+  BatchScalars* sc;
+  int64_t N;
+  int32_t L;
+  int32_t B;
+  const int32_t* F;
+  // last hop (L-1) relabel
+  const int32_t* last_cand;
+  const int32_t* last_kcnt;
+  const int32_t* last_bptr;
+  int32_t* last_bsrc;
+  int32_t last_f;
+  unsigned long long* last_tiles;
+  int64_t last_ntiles;
+  // feature rows
+  const float* fcache;
+  const float* hfeats;  // device alias of the pinned host feature table
+  int32_t pitch;
   int32_t D;
+  float* X;
+  int64_t ldx;
+  int32_t* node_visits;
+  // publication
+  int64_t* out_sizes;
+  uint64_t* out_counters;
+  int32_t* out_status;
 };
 
-// Vector path: ldx % 4 == 0 and ldx >= pitch -> copy whole pitch rows as int4.
-template <int VPL>
-__global__ void __launch_bounds__(256) k_gather_v4(GatherArgs a) {
+// MODE 0: no X (route + counters only); 1: scalar copy of D floats; 2: int4 copy of pitch
+// floats (ldx % 4 == 0, ldx >= pitch), VPL int4 per lane per pass.
+template <int MODE, int VPL>
+__global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
+  BatchScalars* sc = a.sc;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n = *a.count;
-  const int row16 = a.pitch >> 2;
-  for (int64_t r = warp; r < n; r += nwarps) {
-    const int64_t ent = __ldg(a.list + r);
-    const int64_t i = ent >> 32;
-    const int64_t srow = ent & 0xffffffffll;
-    const int4* src = reinterpret_cast<const int4*>(a.src + srow * a.pitch);
-    int4* dst = reinterpret_cast<int4*>(a.X + i * a.ldx);
-    for (int c0 = 0; c0 < row16; c0 += 32 * VPL) {
-      int4 buf[VPL];
+  {
+    const int pf = a.last_f;
+    const int64_t n_prev = (a.L == 1) ? (int64_t)a.B : sc->sizes[a.L - 1];
+    const int64_t nq = n_prev * pf;
+    for (int64_t q = tid; q < nq; q += nthreads) {
+      const int64_t d = q / pf;
+      const int s = (int)(q - d * pf);
+      if (s < a.last_kcnt[d])
+        a.last_bsrc[a.last_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + a.last_cand[q]));
+    }
+    for (int64_t t = tid; t < a.last_ntiles; t += nthreads) a.last_tiles[t] = 0ull;
+    if (tid == 0) sc->tickets[a.L - 1] = 0;
+  }
+  const int64_t n = sc->sizes[a.L];
+  const int64_t warp = tid >> 5;
+  const int64_t nwarps = nthreads >> 5;
+  uint32_t hits = 0, misses = 0;
+  int64_t r = warp;
+  int32_t v = -1, slot = -1;
+  if (r < n) {
+    v = a.F[r];
+    if (v >= 0 && (int64_t)v < a.N) slot = __ldg(&a.dir[v].slot);
+  }
+  while (r < n) {
+    const int64_t nxt = r + nwarps;
+    int32_t vn = -1;
+    if (nxt < n) vn = a.F[nxt];
+    const bool ok = v >= 0 && (int64_t)v < a.N;
+    if (ok) {
+      const float* src = slot >= 0 ? a.fcache + (int64_t)slot * a.pitch : a.hfeats + (int64_t)v * a.pitch;
+      if (MODE == 2) {
+        const int row16 = a.pitch >> 2;
+        const int4* s4 = reinterpret_cast<const int4*>(src);
+        int4* d4 = reinterpret_cast<int4*>(a.X + r * a.ldx);
+        for (int c0 = 0; c0 < row16; c0 += 32 * VPL) {
+          int4 buf[VPL];
 #pragma unroll
-      for (int j = 0; j < VPL; ++j) {
-        const int idx = c0 + lane + 32 * j;
-        if (idx < row16) buf[j] = ld_stream_v4(src + idx);
+          for (int j = 0; j < VPL; ++j) {
+            const int idx = c0 + lane + 32 * j;
+            if (idx < row16) buf[j] = ld_stream_v4(s4 + idx);
+          }
+#pragma unroll
+          for (int j = 0; j < VPL; ++j) {
+            const int idx = c0 + lane + 32 * j;
+            if (idx < row16) st_v4(d4 + idx, buf[j]);
+          }
+        }
+      } else if (MODE == 1) {
+        float* dst = a.X + r * a.ldx;
+        for (int c = lane; c < a.D; c += 32) dst[c] = src[c];
       }
-#pragma unroll
-      for (int j = 0; j < VPL; ++j) {
-        const int idx = c0 + lane + 32 * j;
-        if (idx < row16) st_v4(dst + idx, buf[j]);
+      if (lane == 0) {
+        if (slot >= 0)
+          ++hits;
+        else
+          ++misses;
+        if (a.node_visits) atomicAdd(a.node_visits + v, 1);
       }
     }
+    int32_t sn = -1;
+    if (vn >= 0 && (int64_t)vn < a.N) sn = __ldg(&a.dir[vn].slot);
+    r = nxt;
+    v = vn;
+    slot = sn;
   }
-}
-
-// Scalar path for any ldx >= D (e.g. an unpadded X with D % 4 != 0).
-__global__ void __launch_bounds__(256) k_gather_scalar(GatherArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n = *a.count;
-  for (int64_t r = warp; r < n; r += nwarps) {
-    const int64_t ent = __ldg(a.list + r);
-    const int64_t i = ent >> 32;
-    const int64_t srow = ent & 0xffffffffll;
-    const float* src = a.src + srow * a.pitch;
-    float* dst = a.X + i * a.ldx;
-    for (int c = lane; c < a.D; c += 32) dst[c] = src[c];
+  if (lane == 0 && (hits | misses)) {
+    atomicAdd(&sc->counters[2], (unsigned long long)hits);
+    atomicAdd(&sc->counters[3], (unsigned long long)misses);
+  }
+  // last block publishes the batch scalars and resets them for the next batch
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&sc->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    a.out_sizes[0] = a.B;
+    for (int h = 1; h <= a.L; ++h) a.out_sizes[h] = __ldcg(&sc->sizes[h]);
+    for (int c = 0; c < 4; ++c) {
+      a.out_counters[c] = __ldcg(&sc->counters[c]);
+      sc->counters[c] = 0;
+    }
+    *a.out_status = __ldcg(&sc->status);
+    sc->status = 0;
+    sc->done = 0;
   }
 }
 
 }  // namespace
 
-void launch_gather(dci_ctx* ctx, dci_workspace* ws, bool hits, const int32_t* /*F*/, int32_t /*L*/, float* X,
-                   int64_t ldx, cudaStream_t s) {
-  GatherArgs a;
-  a.list = hits ? ws->hit_list : ws->miss_list;
-  a.count = hits ? &ws->scal->hit_count : &ws->scal->miss_count;
-  a.src = hits ? ctx->d_fcache : ctx->u_feats;
+void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
+                         const HopParams& last, int32_t* node_visits, cudaStream_t s) {
+  FusedArgs a;
+  a.dir = ctx->d_dir;
+  a.pos_of = ws->pos_of;
+  a.sc = ws->scal;
+  a.N = ctx->N;
+  a.L = L;
+  a.B = B;
+  a.F = out->frontier;
+  a.last_cand = last.cand;
+  a.last_kcnt = last.kcnt;
+  a.last_bptr = out->bptr[L - 1];
+  a.last_bsrc = out->bsrc[L - 1];
+  a.last_f = last.f;
+  a.last_tiles = ws->tile_state + ws->tile_off[L - 1];
+  a.last_ntiles = ws->tile_off[L] - ws->tile_off[L - 1];
+  a.fcache = ctx->d_fcache;
+  a.hfeats = ctx->u_feats;
   a.pitch = ctx->pitch;
-  a.X = X;
-  a.ldx = ldx;
   a.D = ctx->D;
-  const bool vec = (ldx % 4 == 0) && ldx >= ctx->pitch && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-  if (!vec) {
-    k_gather_scalar<<<persistent_grid(ctx, k_gather_scalar, 256), 256, 0, s>>>(a);
-  } else if (ctx->pitch <= 32 * 4 * 2) {
-    k_gather_v4<2><<<persistent_grid(ctx, k_gather_v4<2>, 256), 256, 0, s>>>(a);
-  } else {
-    k_gather_v4<5><<<persistent_grid(ctx, k_gather_v4<5>, 256), 256, 0, s>>>(a);
-  }
+  a.X = out->X;
+  a.ldx = out->ldx;
+  a.node_visits = node_visits;
+  a.out_sizes = out->sizes;
+  a.out_counters = out->counters;
+  a.out_status = out->status;
+  auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256), 256, 0, s>>>(a); };
+  const bool vec = out->X && (out->ldx % 4 == 0) && out->ldx >= ctx->pitch &&
+                   (reinterpret_cast<uintptr_t>(out->X) % 16 == 0);
+  if (!out->X)
+    go(k_gather<0, 1>);
+  else if (!vec)
+    go(k_gather<1, 1>);
+  else if (ctx->pitch <= 32 * 4 * 2)
+    go(k_gather<2, 2>);
+  else
+    go(k_gather<2, 5>);
   ++ctx->launches;
 }
 

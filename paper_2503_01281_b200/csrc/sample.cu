@@ -1,8 +1,8 @@
-// S5-S7 of the hot path: per-hop neighbour sampling with the adjacency
-// cache, per-hop dedup/relabel via a node->position table and
-// a single-pass decoupled look-back scan (first-occurrence order, reading C6), and the
-// feature-cache route.  All launches use persistent, SM-count-sized grids
-// that read the frontier size from device memory, so a batch never synchronises the host.
+// S5-S6 of the hot path: per-hop neighbour sampling with the adjacency
+// cache and per-hop dedup/relabel through an epoch-tagged
+// node->position table plus a single-pass decoupled look-back scan (first-occurrence order,
+// reading C6).  All launches use persistent, SM-count-sized grids that read the frontier size
+// from device memory, so a batch never synchronises the host.
 #include <cuda_runtime.h>
 
 #include "dci_internal.cuh"
@@ -11,12 +11,6 @@
 namespace dci {
 
 namespace {
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -41,8 +35,11 @@ struct SampleArgs {
   const int32_t* acache;
   const int32_t* uidx;  // device alias of the pinned host CSC (current order)
   int64_t N;
-  int32_t* pos_of;
+  unsigned long long* pos_of;
+  uint32_t epoch;
   BatchScalars* sc;
+  unsigned long long* prev_tiles;  // previous hop's scan tile state (cleared here)
+  int64_t prev_ntiles;
   HopParams p;
 };
 
@@ -56,11 +53,13 @@ struct SampleArgs {
 //  3. ranks sorted in registers (position = #smaller ranks in the group)
 //  4. element read: HBM cache iff rank < cached_len, else UVA host read
 //  5. cand[d*f + pos] = neighbour, pads -1; kcnt[d] = k
-//  6. insert into the node->position table: atomicMin(pos_of[x], n_h + d*f + pos), so the
-//     table ends with each new node's first (dst-major, rank-ascending) occurrence
+//  6. insert into the node->position table: atomicMax(tag(n_h + d*f + pos)), tag(p) =
+//     epoch << 32 | ~p, so the table keeps each node's first (dst-major, rank-ascending)
+//     occurrence and entries of earlier batches read as absent
 //  7. presample: edge_counts[host_off + rank] += 1 (C8)
 // Fused extra work: hop 0 writes the seeds into F and the table (position = seed index);
-// hop h >= 1 relabels hop h-1's candidates into its block CSR (bsrc[h-1]).
+// hop h >= 1 relabels hop h-1's candidates into its block CSR (bsrc[h-1]) and clears hop
+// h-1's scan tile state.
 // ------------------------------------------------------------------------------------
 template <int G>
 __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
@@ -74,6 +73,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const unsigned long long ehi = (unsigned long long)a.epoch << 32;
 
   const int64_t n_h = (h == 0) ? (int64_t)p.B : sc->sizes[h];
 
@@ -84,18 +84,21 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
       if (s < 0 || (int64_t)s >= a.N)
         atomicCAS(&sc->status, 0, (int32_t)DCI_ESEED);
       else
-        atomicMin(&a.pos_of[s], (int32_t)d);
+        atomicMax(a.pos_of + s, ehi | (0xFFFFFFFFu - (uint32_t)d));
     }
   } else {
-    // relabel of hop h-1 (its scan has completed: kernel boundary)
+    // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
     const int pf = p.prev_f;
     const int64_t n_prev = (h == 1) ? (int64_t)p.B : sc->sizes[h - 1];
     const int64_t nq = n_prev * pf;
     for (int64_t q = tid; q < nq; q += nthreads) {
       const int64_t d = q / pf;
       const int s = (int)(q - d * pf);
-      if (s < p.prev_kcnt[d]) p.prev_bsrc[p.prev_bptr[d] + s] = a.pos_of[p.prev_cand[q]];
+      if (s < p.prev_kcnt[d])
+        p.prev_bsrc[p.prev_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + p.prev_cand[q]));
     }
+    for (int64_t t = tid; t < a.prev_ntiles; t += nthreads) a.prev_tiles[t] = 0ull;
+    if (tid == 0) sc->tickets[h - 1] = 0;
   }
 
   const int GPW = 32 / G;
@@ -163,35 +166,36 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
     if (active && gl < f) p.cand[d * f + (valid ? pos : gl)] = x;
     if (active && gl == 0) p.kcnt[d] = k;
     if (valid) {
-      const int32_t mypos = (int32_t)(n_h + d * f + pos);
-      if (__ldcg(a.pos_of + x) > mypos) atomicMin(a.pos_of + x, mypos);
+      const unsigned long long tag = ehi | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
+      if (__ldcg(a.pos_of + x) < tag) atomicMax(a.pos_of + x, tag);
       if (p.edge_counts) atomicAdd(p.edge_counts + host_off + rank, 1);
     }
   }
   hits = __reduce_add_sync(0xffffffffu, hits);
   misses = __reduce_add_sync(0xffffffffu, misses);
   if (lane == 0 && (hits | misses)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sc->counters[0]), (unsigned long long)hits);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sc->counters[1]), (unsigned long long)misses);
+    atomicAdd(&sc->counters[0], (unsigned long long)hits);
+    atomicAdd(&sc->counters[1], (unsigned long long)misses);
   }
 }
 
 // ------------------------------------------------------------------------------------
 // k_scan_hop: one thread per dst of F_h, kScanTile dsts per tile, tiles taken by dynamic
-// tickets (in-order => deadlock-free look-back).  Per dst: k (samples) and nn (candidates
-// that are the first occurrence of a node not yet in F: pos_of[x] == n_h + q).  One block
-// scan + decoupled look-back over packed (k << 31 | nn) gives
+// tickets (in-order => deadlock-free look-back).  Per dst: k (samples) and the bitmask of
+// candidates that are the first occurrence of a node not yet in F (table tag == tag(n_h +
+// q)).  One block scan + warp-parallel decoupled look-back over packed (k << 31 | nn):
 //   bptr_h[d]            = sum of k over earlier dsts                 (block CSR)
 //   new id of candidate  = n_h + (#new candidates before it)          (F_{h+1} append)
-// and the owner of each new node rewrites pos_of[x] to its final local id, which the next
-// kernel uses to relabel.  Hop 0 also checks seed uniqueness (C22).
+// and the owner of each new node rewrites its table tag to the final local id, which the
+// next kernel uses to relabel.  Hop 0 also checks seed uniqueness (C22).
 // ------------------------------------------------------------------------------------
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 struct ScanArgs {
-  int32_t* pos_of;
+  unsigned long long* pos_of;
+  uint32_t epoch;
   BatchScalars* sc;
   unsigned long long* tile_state;  // this hop's region
   int64_t N;
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
   const int f = p.f;
   const int64_t n_h = (h == 0) ? (int64_t)p.B : sc->sizes[h];
   const int64_t ntiles = (n_h + kScanTile - 1) / kScanTile;
+  const unsigned long long ehi = (unsigned long long)a.epoch << 32;
   __shared__ uint32_t s_ticket;
   __shared__ unsigned long long s_warp[kScanTile / 32];
   __shared__ unsigned long long s_prefix;
@@ -223,18 +228,30 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
     const int64_t tile = s_ticket;
     if (tile >= ntiles) break;
     const int64_t d = tile * kScanTile + threadIdx.x;
-    uint32_t k = 0, nn = 0;
+    uint32_t k = 0, newmask = 0;
     if (d < n_h) {
       k = (uint32_t)p.kcnt[d];
       const int32_t* c = p.cand + d * f;
-      const int32_t base = (int32_t)(n_h + d * f);
-      for (uint32_t s = 0; s < k; ++s) nn += (__ldcg(a.pos_of + c[s]) == base + (int32_t)s) ? 1u : 0u;
+      const uint32_t base = (uint32_t)(n_h + d * f);
+      // which of my candidates own their node's first occurrence (8 loads in flight)
+      for (uint32_t s0 = 0; s0 < k; s0 += 8) {
+        int32_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = (s0 + u < k) ? c[s0 + u] : -1;
+        unsigned long long t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? __ldcg(a.pos_of + x[u]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) newmask |= 1u << (s0 + u);
+      }
       if (h == 0) {
         const int32_t sd = p.F[d];
-        if (sd >= 0 && (int64_t)sd < a.N && __ldcg(a.pos_of + sd) != (int32_t)d)
+        if (sd >= 0 && (int64_t)sd < a.N && __ldcg(a.pos_of + sd) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
           atomicCAS(&sc->status, 0, (int32_t)DCI_EDUP);
       }
     }
+    const uint32_t nn = __popc(newmask);
     // block exclusive scan of packed (k << 31 | nn)
     const unsigned long long mine = ((unsigned long long)k << 31) | nn;
     unsigned long long incl = mine;
@@ -257,176 +274,67 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
     __syncthreads();
     const unsigned long long tile_total = s_warp[kScanTile / 32 - 1];
     const unsigned long long excl = incl - mine + (wid > 0 ? s_warp[wid - 1] : 0ull);
-    // decoupled look-back (thread 0)
-    if (threadIdx.x == 0) {
+    // decoupled look-back, warp-parallel: 32 predecessors per round
+    if (wid == 0) {
       unsigned long long prefix = 0;
       if (tile == 0) {
-        st_volatile_u64(a.tile_state, kFlagIncl | tile_total);
+        if (lane == 0) st_volatile_u64(a.tile_state, kFlagIncl | tile_total);
       } else {
-        st_volatile_u64(a.tile_state + tile, kFlagAgg | tile_total);
-        int64_t t = tile - 1;
+        if (lane == 0) st_volatile_u64(a.tile_state + tile, kFlagAgg | tile_total);
+        int64_t base = tile - 1;
         for (;;) {
-          const unsigned long long s = ld_volatile_u64(a.tile_state + t);
-          const unsigned long long flag = s & ~kValMask;
-          if (flag == 0) continue;
-          prefix += s & kValMask;
-          if (flag == kFlagIncl) break;
-          --t;
+          const int64_t t = base - lane;
+          unsigned long long st = t >= 0 ? ld_volatile_u64(a.tile_state + t) : kFlagIncl;
+          while (__any_sync(0xffffffffu, (st & ~kValMask) == 0)) {
+            if ((st & ~kValMask) == 0) st = ld_volatile_u64(a.tile_state + t);
+          }
+          const unsigned incl_mask = __ballot_sync(0xffffffffu, (st & ~kValMask) == kFlagIncl);
+          const int stop = incl_mask ? (__ffs(incl_mask) - 1) : 31;
+          unsigned long long v = (lane <= stop) ? (st & kValMask) : 0ull;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          prefix += v;
+          if (incl_mask) break;
+          base -= 32;
         }
-        st_volatile_u64(a.tile_state + tile, kFlagIncl | (prefix + tile_total));
+        if (lane == 0) st_volatile_u64(a.tile_state + tile, kFlagIncl | (prefix + tile_total));
       }
-      s_prefix = prefix;
-      if (tile == ntiles - 1) {
-        const unsigned long long tot = prefix + tile_total;
-        p.bptr[n_h] = (int32_t)(tot >> 31);
-        sc->sizes[h + 1] = n_h + (int64_t)(tot & ((1ull << 31) - 1));
+      if (lane == 0) {
+        s_prefix = prefix;
+        if (tile == ntiles - 1) {
+          const unsigned long long tot = prefix + tile_total;
+          p.bptr[n_h] = (int32_t)(tot >> 31);
+          sc->sizes[h + 1] = n_h + (int64_t)(tot & ((1ull << 31) - 1));
+        }
       }
     }
     __syncthreads();
     if (d < n_h) {
       const unsigned long long pre = s_prefix + excl;
       p.bptr[d] = (int32_t)(pre >> 31);
-      int32_t nid = (int32_t)(n_h + (int64_t)(pre & ((1ull << 31) - 1)));
-      if (nn) {
-        const int32_t* c = p.cand + d * f;
-        const int32_t base = (int32_t)(n_h + d * f);
-        for (uint32_t s = 0; s < k; ++s) {
-          const int32_t x = c[s];
-          if (__ldcg(a.pos_of + x) == base + (int32_t)s) {
-            p.F[nid] = x;
-            a.pos_of[x] = nid;
-            ++nid;
-          }
-        }
+      uint32_t nid = (uint32_t)(n_h + (int64_t)(pre & ((1ull << 31) - 1)));
+      const int32_t* c = p.cand + d * f;
+      for (uint32_t m = newmask; m; m &= m - 1) {
+        const int s = __ffs(m) - 1;
+        const int32_t x = c[s];
+        p.F[nid] = x;
+        a.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+        ++nid;
       }
     }
     __syncthreads();  // s_ticket / s_prefix reuse
   }
 }
 
-// ------------------------------------------------------------------------------------
-// k_route: relabel of the last hop + feature-cache route (S7).  For i < |F_L|:
-// slot = dir[F[i]].slot; hit -> hit list (i, slot), miss -> miss list (i, v), appended
-// with one atomic per warp (ballot + popc).  Presample: node_visits[v] += 1 (C7).
-// ------------------------------------------------------------------------------------
-struct RouteArgs {
-  const DirEntry* dir;
-  int32_t* pos_of;
-  BatchScalars* sc;
-  int64_t N;
-  int32_t L;
-  int32_t B;
-  const int32_t* F;
-  const int32_t* last_cand;
-  const int32_t* last_kcnt;
-  const int32_t* last_bptr;
-  int32_t* last_bsrc;
-  int32_t last_f;
-  int64_t* hit_list;
-  int64_t* miss_list;
-  int32_t* node_visits;
-};
-
-__global__ void __launch_bounds__(256) k_route(RouteArgs a) {
-  BatchScalars* sc = a.sc;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  {
-    const int pf = a.last_f;
-    const int64_t n_prev = (a.L == 1) ? (int64_t)a.B : sc->sizes[a.L - 1];
-    const int64_t nq = n_prev * pf;
-    for (int64_t q = tid; q < nq; q += nthreads) {
-      const int64_t d = q / pf;
-      const int s = (int)(q - d * pf);
-      if (s < a.last_kcnt[d]) a.last_bsrc[a.last_bptr[d] + s] = a.pos_of[a.last_cand[q]];
-    }
-  }
-  const int64_t n_L = sc->sizes[a.L];
-  uint32_t hits = 0, misses = 0;
-  const int64_t nwarps = nthreads >> 5;
-  for (int64_t base = (tid >> 5) * 32; base < n_L; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    int32_t v = -1, slot = -1;
-    bool ok = false;
-    if (i < n_L) {
-      v = a.F[i];
-      ok = v >= 0 && (int64_t)v < a.N;
-      if (ok) slot = __ldg(&a.dir[v].slot);
-    }
-    const bool is_hit = ok && slot >= 0;
-    const bool is_miss = ok && slot < 0;
-    const unsigned mh = __ballot_sync(0xffffffffu, is_hit);
-    const unsigned mm = __ballot_sync(0xffffffffu, is_miss);
-    uint32_t bh = 0, bm = 0;
-    if (lane == 0) {
-      if (mh) bh = atomicAdd(&sc->hit_count, (uint32_t)__popc(mh));
-      if (mm) bm = atomicAdd(&sc->miss_count, (uint32_t)__popc(mm));
-    }
-    bh = __shfl_sync(0xffffffffu, bh, 0);
-    bm = __shfl_sync(0xffffffffu, bm, 0);
-    if (is_hit) a.hit_list[bh + __popc(mh & lanemask_lt())] = (i << 32) | (uint32_t)slot;
-    if (is_miss) a.miss_list[bm + __popc(mm & lanemask_lt())] = (i << 32) | (uint32_t)v;
-    if (ok && a.node_visits) atomicAdd(a.node_visits + v, 1);
-    hits += is_hit ? 1u : 0u;
-    misses += is_miss ? 1u : 0u;
-  }
-  hits = __reduce_add_sync(0xffffffffu, hits);
-  misses = __reduce_add_sync(0xffffffffu, misses);
-  if (lane == 0 && (hits | misses)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sc->counters[2]), (unsigned long long)hits);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sc->counters[3]), (unsigned long long)misses);
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// k_finish: publish sizes / counters / status to the caller's buffers, clear the
-// node->position table over F_L (every key inserted this batch is in F_L), and reset the
-// workspace scalars and scan tile state for the next batch.
-// ------------------------------------------------------------------------------------
-struct FinishArgs {
-  int32_t* pos_of;
-  BatchScalars* sc;
-  unsigned long long* tile_state;
-  int64_t tiles_total;
-  int64_t N;
-  int32_t L;
-  int32_t B;
-  const int32_t* F;
-  int64_t* out_sizes;
-  uint64_t* out_counters;
-  int32_t* out_status;
-};
-
-__global__ void __launch_bounds__(256) k_finish(FinishArgs a) {
-  BatchScalars* sc = a.sc;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t n_L = sc->sizes[a.L];
-  for (int64_t i = tid; i < n_L; i += nthreads) {
-    const int32_t v = a.F[i];
-    if (v >= 0 && (int64_t)v < a.N) a.pos_of[v] = kPosEmpty;
-  }
-  for (int64_t i = tid; i < a.tiles_total; i += nthreads) a.tile_state[i] = 0ull;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.out_sizes[0] = a.B;
-    for (int h = 1; h <= a.L; ++h) a.out_sizes[h] = sc->sizes[h];
-    for (int c = 0; c < 4; ++c) {
-      a.out_counters[c] = sc->counters[c];
-      sc->counters[c] = 0;
-    }
-    *a.out_status = sc->status;
-    sc->status = 0;
-    for (int h = 0; h < DCI_MAX_LAYERS; ++h) sc->tickets[h] = 0;
-    sc->hit_count = 0;
-    sc->miss_count = 0;
-  }
-}
-
 }  // namespace
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
-  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->scal, p};
+  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->epoch, ws->scal,
+               nullptr, 0, p};
+  if (p.hop > 0) {
+    a.prev_tiles = ws->tile_state + ws->tile_off[p.hop - 1];
+    a.prev_ntiles = ws->tile_off[p.hop] - ws->tile_off[p.hop - 1];
+  }
   // sub-warp group width: next power of two >= f
   auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256), 256, 0, s>>>(a); };
   if (p.f <= 1)
@@ -445,28 +353,11 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cuda
 }
 
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
-  ScanArgs a{ws->pos_of, ws->scal, ws->tile_state + ws->tile_off[p.hop], ctx->N, p};
+  ScanArgs a{ws->pos_of, ws->epoch, ws->scal, ws->tile_state + ws->tile_off[p.hop], ctx->N, p};
   const int64_t tiles = (ws->hop_cap[p.hop] + kScanTile - 1) / kScanTile;
   int64_t grid = persistent_grid(ctx, k_scan_hop, kScanTile, 8);
   if (tiles < grid) grid = tiles > 0 ? tiles : 1;
   k_scan_hop<<<(unsigned)grid, kScanTile, 0, s>>>(a);
-  ++ctx->launches;
-}
-
-void launch_route(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const int32_t* F, const int32_t* last_cand,
-                  const int32_t* last_kcnt, const int32_t* last_bptr, int32_t* last_bsrc, int32_t last_f,
-                  int32_t* node_visits, cudaStream_t s) {
-  RouteArgs a{ctx->d_dir, ws->pos_of, ws->scal, ctx->N, L, B, F, last_cand, last_kcnt, last_bptr, last_bsrc,
-              last_f, ws->hit_list, ws->miss_list, node_visits};
-  k_route<<<persistent_grid(ctx, k_route, 256), 256, 0, s>>>(a);
-  ++ctx->launches;
-}
-
-void launch_finish(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
-                   cudaStream_t s) {
-  FinishArgs a{ws->pos_of, ws->scal, ws->tile_state, ws->tiles_cap, ctx->N, L, B, out->frontier, out->sizes,
-               out->counters, out->status};
-  k_finish<<<persistent_grid(ctx, k_finish, 256, 2), 256, 0, s>>>(a);
   ++ctx->launches;
 }
 
