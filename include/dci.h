@@ -108,8 +108,8 @@ dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanou
                              int64_t* frontier_caps, int64_t* bsrc_caps, int32_t* pitch);
 
 /* --------------------------------------------------------------------------------------
- * Workspace: per-stream scratch for one in-flight batch (node->position table of N int32,
- * candidate / count arrays, scan tile state, hit/miss lists, events, an auxiliary stream).
+ * Workspace: per-stream scratch for one in-flight batch (epoch-tagged node->position table
+ * of N uint64, candidate / count arrays, scan tile state, batch scalars, stage events).
  * Sized for batches of up to max_batch seeds with fan-outs up to max_fanouts[.] (L hops).
  * Use one workspace per concurrently in-flight batch.
  * ------------------------------------------------------------------------------------ */
@@ -207,9 +207,28 @@ dci_status dci_cache_state(dci_ctx* ctx, int32_t* cached_len, int64_t* cache_off
                            int32_t* acache, float* fcache, int32_t* indices_cur);
 
 /* Stage times of the workspace's last batch, in ms (CUDA events recorded on the launch
- * stream around the sampling hops and around the gather; requires profiling on). */
+ * stream around the sampling hops and around the gather; requires profiling on).  With
+ * profiling on, dci_sample_gather first waits (host) for the previous batch of the same
+ * workspace to finish so its stage times can be accumulated (see dci_workspace_stats). */
 dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on);
 dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms);
+
+/* Running totals of a workspace since its last reset (synchronises the device):
+ * batches finished, seeds, sum of |F_L| (feature rows gathered), summed counters, and -
+ * with profiling on - the number of event-timed batches and their summed stage times
+ * (sampling hops S5-S6; the fused route+gather kernel S7-S8), in ms.  reset != 0 zeroes
+ * the totals after reading them. */
+typedef struct dci_ws_stats {
+  uint64_t batches;
+  uint64_t seeds;
+  uint64_t frontier_rows;
+  uint64_t counters[4];
+  uint64_t timed_batches;
+  double sample_ms;
+  double gather_ms;
+} dci_ws_stats;
+
+dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset);
 
 /* Kernels launched by this context so far (all workspaces). */
 uint64_t dci_launch_count(const dci_ctx* ctx);

@@ -29,7 +29,7 @@ OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
             "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
             "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
-            "dci_launch_count", "dci_last_error", "dci_version"]
+            "dci_workspace_stats", "dci_launch_count", "dci_last_error", "dci_version"]
 
 
 class DciError(RuntimeError):
@@ -43,6 +43,12 @@ class dci_batch_out(C.Structure):
                 ("bptr", C.c_void_p * MAX_LAYERS), ("bsrc", C.c_void_p * MAX_LAYERS),
                 ("hop_cap", C.c_int64 * MAX_LAYERS), ("bsrc_cap", C.c_int64 * MAX_LAYERS),
                 ("X", C.c_void_p), ("ldx", C.c_int64), ("counters", C.c_void_p), ("status", C.c_void_p)]
+
+
+class dci_ws_stats(C.Structure):
+    _fields_ = [("batches", C.c_uint64), ("seeds", C.c_uint64), ("frontier_rows", C.c_uint64),
+                ("counters", C.c_uint64 * 4), ("timed_batches", C.c_uint64), ("sample_ms", C.c_double),
+                ("gather_ms", C.c_double)]
 
 
 class dci_cache_info(C.Structure):
@@ -78,6 +84,7 @@ def lib():
         "dci_cache_state": [vp, vp, vp, vp, vp, vp, vp],
         "dci_workspace_set_profiling": [vp, i32],
         "dci_workspace_stage_ms": [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)],
+        "dci_workspace_stats": [vp, C.POINTER(dci_ws_stats), i32],
         "dci_launch_count": [vp],
         "dci_last_error": [],
         "dci_version": [],
@@ -190,6 +197,14 @@ class Workspace:
 
     def set_profiling(self, on: bool = True):
         _check(lib().dci_workspace_set_profiling(self.handle, 1 if on else 0), "dci_workspace_set_profiling")
+
+    def stats(self, reset: bool = False) -> dict:
+        """dci_workspace_stats: running totals (batches, seeds, rows, counters, stage ms)."""
+        st = dci_ws_stats()
+        _check(lib().dci_workspace_stats(self.handle, C.byref(st), 1 if reset else 0), "dci_workspace_stats")
+        return {"batches": st.batches, "seeds": st.seeds, "frontier_rows": st.frontier_rows,
+                "counters": [int(c) for c in st.counters], "timed_batches": st.timed_batches,
+                "sample_ms": st.sample_ms, "gather_ms": st.gather_ms}
 
     def stage_ms(self):
         s, g = C.c_float(), C.c_float()

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <mutex>
@@ -43,6 +44,15 @@ int occupancy_blocks(const void* kernel, int block, int cap) {
 }
 
 namespace {
+
+bool graph_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("DCI_GRAPH");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -100,39 +110,144 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   if (out->X && out->ldx < ctx->D) return fail(DCI_EINVAL, "ldx < D");
 
   DeviceGuard g(ctx->device);
+  const bool prof = ws->profiling || pass == 1;
+  if (ws->have_times && pass == 0) {
+    // the previous profiled batch on this workspace: fold its stage times into the totals
+    DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
+    float ms_s = 0.f, ms_g = 0.f;
+    DCI_CUDA(cudaEventElapsedTime(&ms_s, ws->ev_t[0], ws->ev_t[1]));
+    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[1], ws->ev_t[3]));
+    ws->acc_sample_ms += ms_s;
+    ws->acc_gather_ms += ms_g;
+    ws->acc_timed += 1;
+    ws->have_times = 0;
+  }
+  // ---- per-batch header: seeds pointer, B, seed, epoch (pinned ring -> device) ----
   if (++ws->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
     DCI_CUDA(cudaMemsetAsync(ws->pos_of, 0, sizeof(unsigned long long) * ctx->N, s));
     ws->epoch = 1;
   }
-  const bool prof = ws->profiling || pass == 1;
-  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[0], s));
-  HopParams prev{};
-  for (int h = 0; h < L; ++h) {
-    HopParams p{};
-    p.F_in = (h == 0) ? seeds : out->frontier;
-    p.F = out->frontier;
-    p.hop = h;
-    p.f = fanouts[L - 1 - h];
-    p.pass = pass;
-    p.seed = seed;
-    p.B = B;
-    p.cand = ws->cand[h & 1];
-    p.kcnt = ws->kcnt[h & 1];
-    if (h > 0) {
-      p.prev_cand = prev.cand;
-      p.prev_kcnt = prev.kcnt;
-      p.prev_bptr = out->bptr[h - 1];
-      p.prev_bsrc = out->bsrc[h - 1];
-      p.prev_f = prev.f;
+  const int slot = (int)(ws->calls++ % dci_workspace::kHdrRing);
+  DCI_CUDA(cudaEventSynchronize(ws->hdr_ev[slot]));  // the copy that last used this slot is done
+  BatchHeader* hh = ws->hdr_ring + slot;
+  hh->seeds = seeds;
+  hh->seed = seed;
+  hh->B = B;
+  hh->epoch = ws->epoch;
+  DCI_CUDA(cudaMemcpyAsync(&ws->scal->hdr, hh, sizeof(BatchHeader), cudaMemcpyHostToDevice, s));
+  DCI_CUDA(cudaEventRecord(ws->hdr_ev[slot], s));
+
+  // ---- kernels: a CUDA graph per workspace, re-captured only when the signature changes ----
+  struct Sig {
+    int32_t L, pass, prof;
+    int32_t fan[DCI_MAX_LAYERS];
+    dci_batch_out out;
+    const int32_t* nv;
+    const int32_t* ec;
+    const void* acache;
+    const void* fcache;
+    const void* uidx;
+  } sig;
+  memset(&sig, 0, sizeof(sig));
+  sig.L = L;
+  sig.pass = (int32_t)pass;
+  sig.prof = prof ? 1 : 0;
+  for (int i = 0; i < L; ++i) sig.fan[i] = fanouts[i];
+  sig.out = *out;
+  sig.nv = node_visits;
+  sig.ec = edge_counts;
+  sig.acache = ctx->d_acache;
+  sig.fcache = ctx->d_fcache;
+  sig.uidx = ctx->u_idx_cur;
+  static_assert(sizeof(Sig) <= sizeof(ws->graph_sig), "signature buffer too small");
+  const bool use_graph = graph_mode();
+  const bool need_capture =
+      use_graph && !(ws->n_graphs && ws->graph_sig_len == sizeof(Sig) && !memcmp(ws->graph_sig, &sig, sizeof(Sig)));
+  // part 0: the L sampling hops; part 1: the fused route + gather kernel
+  auto enqueue_part = [&](int part, cudaStream_t es) {
+    if (part == 0) {
+      HopParams prev{};
+      for (int h = 0; h < L; ++h) {
+        HopParams p{};
+        p.F = out->frontier;
+        p.hop = h;
+        p.f = fanouts[L - 1 - h];
+        p.pass = pass;
+        p.cand = ws->cand[h & 1];
+        p.kcnt = ws->kcnt[h & 1];
+        if (h > 0) {
+          p.prev_cand = prev.cand;
+          p.prev_kcnt = prev.kcnt;
+          p.prev_bptr = out->bptr[h - 1];
+          p.prev_bsrc = out->bsrc[h - 1];
+          p.prev_f = prev.f;
+        }
+        p.bptr = out->bptr[h];
+        p.edge_counts = edge_counts;
+        launch_sample_hop(ctx, ws, p, es);
+        launch_scan_hop(ctx, ws, p, es);
+        prev = p;
+      }
+    } else {
+      HopParams last{};
+      last.f = fanouts[0];
+      last.cand = ws->cand[(L - 1) & 1];
+      last.kcnt = ws->kcnt[(L - 1) & 1];
+      launch_gather_fused(ctx, ws, L, out, last, node_visits, es);
     }
-    p.bptr = out->bptr[h];
-    p.edge_counts = edge_counts;
-    launch_sample_hop(ctx, ws, p, s);
-    launch_scan_hop(ctx, ws, p, s);
-    prev = p;
+  };
+  if (need_capture) {
+    // one graph per part when profiling (stage events go between them), else one graph
+    const int ngraphs = prof ? 2 : 1;
+    for (int gi = 0; gi < 2; ++gi) {
+      if (ws->graph_exec[gi]) cudaGraphExecDestroy(ws->graph_exec[gi]);
+      ws->graph_exec[gi] = nullptr;
+    }
+    ws->n_graphs = 0;
+    for (int gi = 0; gi < ngraphs; ++gi) {
+      const uint64_t launches0 = ctx->launches;
+      DCI_CUDA(cudaStreamBeginCapture(ws->cap_stream, cudaStreamCaptureModeThreadLocal));
+      if (ngraphs == 2) {
+        enqueue_part(gi, ws->cap_stream);
+      } else {
+        enqueue_part(0, ws->cap_stream);
+        enqueue_part(1, ws->cap_stream);
+      }
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(ws->cap_stream, &graph);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      ws->graph_kernels[gi] = ctx->launches - launches0;
+      ctx->launches = launches0;  // counted when the graph actually runs
+      e = cudaGraphInstantiate(&ws->graph_exec[gi], graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        ws->graph_sig_len = 0;
+        return cuda_fail(e, "cudaGraphInstantiate");
+      }
+      ws->n_graphs = gi + 1;
+    }
+    memcpy(ws->graph_sig, &sig, sizeof(Sig));
+    ws->graph_sig_len = sizeof(Sig);
   }
+  auto run_part = [&](int part) -> cudaError_t {
+    if (!use_graph) {
+      enqueue_part(part, s);
+      return cudaSuccess;
+    }
+    if (ws->n_graphs == 2) {
+      ctx->launches += ws->graph_kernels[part];
+      return cudaGraphLaunch(ws->graph_exec[part], s);
+    }
+    if (part == 0) {
+      ctx->launches += ws->graph_kernels[0];
+      return cudaGraphLaunch(ws->graph_exec[0], s);
+    }
+    return cudaSuccess;  // single graph holds both parts
+  };
+  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[0], s));
+  DCI_CUDA(run_part(0));
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[1], s));
-  launch_gather_fused(ctx, ws, L, B, out, prev, node_visits, s);
+  DCI_CUDA(run_part(1));
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], s));
   ws->have_times = prof ? 1 : 0;
   DCI_CUDA(cudaGetLastError());
@@ -307,6 +422,12 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   if ((e = cudaMalloc(&w->seeds_stage, sizeof(int32_t) * max_batch)) != cudaSuccess) return bail(e, "cudaMalloc");
   for (int i = 0; i < 4; ++i)
     if ((e = cudaEventCreate(&w->ev_t[i])) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
+                         cudaHostAllocPortable)) != cudaSuccess)
+    return bail(e, "cudaHostAlloc(header ring)");
+  for (int i = 0; i < dci_workspace::kHdrRing; ++i)
+    if ((e = cudaEventCreateWithFlags(&w->hdr_ev[i], cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "stream");
   cudaMemset(w->pos_of, 0, sizeof(unsigned long long) * ctx->N);
   cudaMemset(w->tile_state, 0, sizeof(unsigned long long) * w->tiles_cap);
   cudaMemset(w->scal, 0, sizeof(BatchScalars));
@@ -329,6 +450,12 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
   cudaFree(w->seeds_stage);
   for (int i = 0; i < 4; ++i)
     if (w->ev_t[i]) cudaEventDestroy(w->ev_t[i]);
+  for (int i = 0; i < dci_workspace::kHdrRing; ++i)
+    if (w->hdr_ev[i]) cudaEventDestroy(w->hdr_ev[i]);
+  if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
+  for (int i = 0; i < 2; ++i)
+    if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
+  if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   delete w;
   return DCI_OK;
 }
@@ -551,6 +678,38 @@ dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* ga
   DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
   if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, ws->ev_t[0], ws->ev_t[1]));
   if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[1], ws->ev_t[3]));
+  return DCI_OK;
+}
+
+dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset) {
+  if (!ws || !out) return fail(DCI_EINVAL, "bad arguments");
+  DeviceGuard g(ws->ctx->device);
+  DCI_CUDA(cudaDeviceSynchronize());
+  if (ws->have_times) {
+    float ms_s = 0.f, ms_g = 0.f;
+    DCI_CUDA(cudaEventElapsedTime(&ms_s, ws->ev_t[0], ws->ev_t[1]));
+    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[1], ws->ev_t[3]));
+    ws->acc_sample_ms += ms_s;
+    ws->acc_gather_ms += ms_g;
+    ws->acc_timed += 1;
+    ws->have_times = 0;
+  }
+  BatchScalars h;
+  DCI_CUDA(cudaMemcpy(&h, ws->scal, sizeof(h), cudaMemcpyDeviceToHost));
+  out->batches = h.acc_batches;
+  out->seeds = h.acc_seeds;
+  out->frontier_rows = h.acc_rows;
+  for (int c = 0; c < 4; ++c) out->counters[c] = h.acc_counters[c];
+  out->timed_batches = ws->acc_timed;
+  out->sample_ms = ws->acc_sample_ms;
+  out->gather_ms = ws->acc_gather_ms;
+  if (reset) {
+    h.acc_batches = h.acc_seeds = h.acc_rows = 0;
+    for (int c = 0; c < 4; ++c) h.acc_counters[c] = 0;
+    DCI_CUDA(cudaMemcpy(ws->scal, &h, sizeof(h), cudaMemcpyHostToDevice));
+    ws->acc_timed = 0;
+    ws->acc_sample_ms = ws->acc_gather_ms = 0.0;
+  }
   return DCI_OK;
 }
 

@@ -26,13 +26,26 @@ static_assert(sizeof(DirEntry) == 32, "directory entry must be one 32-byte secto
 
 constexpr int kScanTile = 256;             // dst nodes per tile of the per-hop scan
 
+// Per-batch values that change every call; written by one host->device copy before the
+// batch's kernels (or CUDA graph) run, so a captured graph never needs re-capturing for them.
+struct BatchHeader {
+  const int32_t* seeds;  // device int32[B]
+  unsigned long long seed;
+  int32_t B;
+  uint32_t epoch;        // position-table tag of this batch
+};
+
 // Device-side per-batch scalars live in one small struct (workspace memory).
 struct BatchScalars {
+  BatchHeader hdr;
   int64_t sizes[DCI_MAX_LAYERS + 1];  // |F_h| (mirrored into out->sizes)
   uint32_t tickets[DCI_MAX_LAYERS];   // dynamic tile tickets of the per-hop scans
   unsigned long long counters[4];     // adj_hit, adj_miss, feat_hit, feat_miss
   uint32_t done;                      // blocks of the gather kernel that have finished
   int32_t status;
+  // running totals since the last dci_workspace_stats(reset): batches, seeds, |F_L| rows,
+  // counters (updated by the gather kernel's last block)
+  unsigned long long acc_batches, acc_seeds, acc_rows, acc_counters[4];
 };
 
 struct dci_ctx_impl;
@@ -92,10 +105,27 @@ struct dci_workspace {
   unsigned long long* tile_state = nullptr;  // [tiles_cap]
   dci::BatchScalars* scal = nullptr;
   int32_t* seeds_stage = nullptr;     // [max_batch] device copy for the host-seed variant
+  // pinned ring of batch headers (host side of the per-batch H2D header copy)
+  static constexpr int kHdrRing = 16;
+  dci::BatchHeader* hdr_ring = nullptr;
+  cudaEvent_t hdr_ev[kHdrRing] = {nullptr};
+  uint64_t calls = 0;
+  // CUDA graph of the batch (captured once per signature, relaunched while it matches)
+  // with profiling on, two graphs (sampling hops | gather) so the stage events can be
+  // recorded on the stream between them (events captured inside a graph cannot be timed)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
+  int32_t n_graphs = 0;
+  unsigned char graph_sig[512] = {0};
+  size_t graph_sig_len = 0;
+  uint64_t graph_kernels[2] = {0, 0};
   // stage events
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
   int32_t profiling = 0;
   int32_t have_times = 0;
+  // host-side running totals of the event-timed stages (profiling on)
+  uint64_t acc_timed = 0;
+  double acc_sample_ms = 0.0, acc_gather_ms = 0.0;
 };
 
 namespace dci {
@@ -113,13 +143,10 @@ dci_status cuda_fail(cudaError_t e, const char* what);
 
 // ---- kernel launchers (sample.cu / gather.cu / fill.cu) ----
 struct HopParams {
-  const int32_t* F_in;      // frontier read by this hop (seeds for hop 0)
-  int32_t* F;               // output frontier array (global ids)
+  int32_t* F;               // output frontier array (global ids); hop 0 reads the seeds
   int32_t hop;
   int32_t f;                // fan-out of this hop
   uint32_t pass;            // 0 inference, 1 presample
-  uint64_t seed;
-  int32_t B;                // batch size (hop 0 only)
   int32_t* cand;            // [n_h * f]
   int32_t* kcnt;            // [n_h]
   // previous hop's relabel work, fused into this hop's sample kernel (h >= 1)
@@ -134,7 +161,7 @@ struct HopParams {
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
-void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
+void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
 
 // fill.cu

@@ -9,6 +9,8 @@
 //    workspace scalars for the next batch.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "dci_internal.cuh"
 
 namespace dci {
@@ -34,7 +36,6 @@ struct FusedArgs {
   BatchScalars* sc;
   int64_t N;
   int32_t L;
-  int32_t B;
   const int32_t* F;
   // last hop (L-1) relabel
   const int32_t* last_cand;
@@ -66,9 +67,10 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
+  const int32_t B = sc->hdr.B;
   {
     const int pf = a.last_f;
-    const int64_t n_prev = (a.L == 1) ? (int64_t)a.B : sc->sizes[a.L - 1];
+    const int64_t n_prev = (a.L == 1) ? (int64_t)B : sc->sizes[a.L - 1];
     const int64_t nq = n_prev * pf;
     for (int64_t q = tid; q < nq; q += nthreads) {
       const int64_t d = q / pf;
@@ -145,13 +147,17 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     __threadfence();
-    a.out_sizes[0] = a.B;
+    a.out_sizes[0] = B;
     for (int h = 1; h <= a.L; ++h) a.out_sizes[h] = __ldcg(&sc->sizes[h]);
     for (int c = 0; c < 4; ++c) {
       a.out_counters[c] = __ldcg(&sc->counters[c]);
       sc->counters[c] = 0;
     }
     *a.out_status = __ldcg(&sc->status);
+    sc->acc_batches += 1;
+    sc->acc_seeds += (unsigned long long)B;
+    sc->acc_rows += (unsigned long long)__ldcg(&sc->sizes[a.L]);
+    for (int c = 0; c < 4; ++c) sc->acc_counters[c] += a.out_counters[c];
     sc->status = 0;
     sc->done = 0;
   }
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 
 }  // namespace
 
-void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, const dci_batch_out* out,
+void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s) {
   FusedArgs a;
   a.dir = ctx->d_dir;
@@ -167,7 +173,6 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, 
   a.sc = ws->scal;
   a.N = ctx->N;
   a.L = L;
-  a.B = B;
   a.F = out->frontier;
   a.last_cand = last.cand;
   a.last_kcnt = last.kcnt;
@@ -186,7 +191,13 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, int32_t B, 
   a.out_sizes = out->sizes;
   a.out_counters = out->counters;
   a.out_status = out->status;
-  auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256), 256, 0, s>>>(a); };
+  // Blocks per SM for the gather: a small cap leaves registers / warp slots for the
+  // sampling kernels of other in-flight batches (the gather is HBM-bound, not occupancy-bound).
+  static int bps = [] {
+    const char* e = getenv("DCI_GATHER_BPS");
+    return e ? atoi(e) : 1;
+  }();
+  auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };
   const bool vec = out->X && (out->ldx % 4 == 0) && out->ldx >= ctx->pitch &&
                    (reinterpret_cast<uintptr_t>(out->X) % 16 == 0);
   if (!out->X)

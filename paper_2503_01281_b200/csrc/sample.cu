@@ -5,6 +5,8 @@
 // from device memory, so a batch never synchronises the host.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "dci_internal.cuh"
 #include "philox.cuh"
 
@@ -36,7 +38,6 @@ struct SampleArgs {
   const int32_t* uidx;  // device alias of the pinned host CSC (current order)
   int64_t N;
   unsigned long long* pos_of;
-  uint32_t epoch;
   BatchScalars* sc;
   unsigned long long* prev_tiles;  // previous hop's scan tile state (cleared here)
   int64_t prev_ntiles;
@@ -73,13 +74,16 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const unsigned long long ehi = (unsigned long long)a.epoch << 32;
+  const int64_t B = sc->hdr.B;
+  const unsigned long long seed = sc->hdr.seed;
+  const unsigned long long ehi = (unsigned long long)sc->hdr.epoch << 32;
+  const int32_t* F_in = (h == 0) ? sc->hdr.seeds : p.F;
 
-  const int64_t n_h = (h == 0) ? (int64_t)p.B : sc->sizes[h];
+  const int64_t n_h = (h == 0) ? B : sc->sizes[h];
 
   if (h == 0) {
-    for (int64_t d = tid; d < p.B; d += nthreads) {
-      const int32_t s = p.F_in[d];
+    for (int64_t d = tid; d < B; d += nthreads) {
+      const int32_t s = F_in[d];
       p.F[d] = s;
       if (s < 0 || (int64_t)s >= a.N)
         atomicCAS(&sc->status, 0, (int32_t)DCI_ESEED);
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
   } else {
     // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
     const int pf = p.prev_f;
-    const int64_t n_prev = (h == 1) ? (int64_t)p.B : sc->sizes[h - 1];
+    const int64_t n_prev = (h == 1) ? B : sc->sizes[h - 1];
     const int64_t nq = n_prev * pf;
     for (int64_t q = tid; q < nq; q += nthreads) {
       const int64_t d = q / pf;
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
     int32_t v = -1;
     int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
     if (active) {
-      v = p.F_in[d];
+      v = F_in[d];
       if (v >= 0 && (int64_t)v < a.N) {
         const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
         e0 = __ldg(ep);
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
       int32_t chosen = 0, j = 0;
       if (floyd && gl < f) {
         j = deg - f + gl;
-        const uint64_t u = philox_u64(p.seed, p.pass, (uint32_t)h, (uint32_t)v, (uint32_t)gl);
+        const uint64_t u = philox_u64(seed, p.pass, (uint32_t)h, (uint32_t)v, (uint32_t)gl);
         chosen = (int32_t)__umul64hi(u, (uint64_t)(j + 1));
       }
       // Floyd: slot i keeps t_i unless an earlier slot already chose it, then takes j_i.
@@ -195,7 +199,6 @@ constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 struct ScanArgs {
   unsigned long long* pos_of;
-  uint32_t epoch;
   BatchScalars* sc;
   unsigned long long* tile_state;  // this hop's region
   int64_t N;
@@ -207,9 +210,9 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
   BatchScalars* sc = a.sc;
   const int h = p.hop;
   const int f = p.f;
-  const int64_t n_h = (h == 0) ? (int64_t)p.B : sc->sizes[h];
+  const int64_t n_h = (h == 0) ? (int64_t)sc->hdr.B : sc->sizes[h];
   const int64_t ntiles = (n_h + kScanTile - 1) / kScanTile;
-  const unsigned long long ehi = (unsigned long long)a.epoch << 32;
+  const unsigned long long ehi = (unsigned long long)sc->hdr.epoch << 32;
   __shared__ uint32_t s_ticket;
   __shared__ unsigned long long s_warp[kScanTile / 32];
   __shared__ unsigned long long s_prefix;
@@ -329,14 +332,17 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
 }  // namespace
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
-  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->epoch, ws->scal,
-               nullptr, 0, p};
+  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->scal, nullptr, 0, p};
   if (p.hop > 0) {
     a.prev_tiles = ws->tile_state + ws->tile_off[p.hop - 1];
     a.prev_ntiles = ws->tile_off[p.hop] - ws->tile_off[p.hop - 1];
   }
+  static int bps = [] {
+    const char* e = getenv("DCI_SAMPLE_BPS");
+    return e ? atoi(e) : 8;
+  }();
   // sub-warp group width: next power of two >= f
-  auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256), 256, 0, s>>>(a); };
+  auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };
   if (p.f <= 1)
     go(k_sample_hop<1>);
   else if (p.f <= 2)
@@ -353,7 +359,7 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cuda
 }
 
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
-  ScanArgs a{ws->pos_of, ws->epoch, ws->scal, ws->tile_state + ws->tile_off[p.hop], ctx->N, p};
+  ScanArgs a{ws->pos_of, ws->scal, ws->tile_state + ws->tile_off[p.hop], ctx->N, p};
   const int64_t tiles = (ws->hop_cap[p.hop] + kScanTile - 1) / kScanTile;
   int64_t grid = persistent_grid(ctx, k_scan_hop, kScanTile, 8);
   if (tiles < grid) grid = tiles > 0 ? tiles : 1;

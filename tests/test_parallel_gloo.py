@@ -1,0 +1,87 @@
+"""Multi-process host logic on CPU (gloo, world size 2): batch sharding, the presample-count
+allreduce (C1) and max/sum over ranks.  The per-rank counting is done by the oracle here (the
+CUDA path does it on GPUs); what is tested is that sharding + allreduce reproduce the
+single-process presample exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2503_01281_b200 import parallel
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    try:
+        import oracle
+        import synth
+        r, w, _ = parallel.init("gloo")
+        assert (r, w) == (rank, world)
+        ip, ix = synth.rmat_csc(1500, 16000, seed=5)
+        ip, ix = ip.numpy(), ix.numpy()
+        B, fan = 40, (4, 3)
+        pre = synth.presample_seeds(ip, 6, B)
+        batches = [pre[i * B:(i + 1) * B] for i in range(6)]
+        mine = parallel.shard(batches, rank, world)
+        nv = np.zeros(len(ip) - 1, np.int32)
+        ec = np.zeros(len(ix), np.int32)
+        ts, tf = [], []
+        for b in mine:
+            oracle.presample(ip, ix, b, B, fan, 3, nv, ec)
+            ts.append(1000 + rank)
+            tf.append(3000 + rank)
+        nv_t, ec_t = torch.from_numpy(nv), torch.from_numpy(ec)
+        S, F = parallel.allreduce_presample(nv_t, ec_t, ts, tf)
+        mx = parallel.max_over_ranks(float(rank + 1))
+        sm = parallel.sum_over_ranks([1.0, rank])
+        ok = True
+        if rank == 0:
+            nv1, ec1 = oracle.presample(ip, ix, pre, B, fan, 3)
+            ok = bool(np.array_equal(nv_t.numpy(), nv1) and np.array_equal(ec_t.numpy(), ec1))
+        q.put((rank, ok, S, F, mx, sm.tolist(), len(mine)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+        raise
+
+
+def test_sharded_presample_allreduce_equals_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    res = sorted(res)
+    for r in res:
+        assert len(r) == 7, r
+    (_, ok0, S0, F0, mx0, sm0, n0), (_, ok1, S1, F1, mx1, sm1, n1) = res
+    assert ok0
+    assert n0 == 3 and n1 == 3
+    assert S0 == S1 == 3 * 1000 + 3 * 1001 and F0 == F1 == 3 * 3000 + 3 * 3001
+    assert mx0 == mx1 == 2.0
+    assert sm0 == sm1 == [2.0, 1.0]
+
+
+def test_shard_round_robin():
+    items = list(range(10))
+    assert parallel.shard(items, 0, 3) == [0, 3, 6, 9]
+    assert parallel.shard(items, 2, 3) == [2, 5, 8]
+    assert sorted(sum((parallel.shard(items, r, 4) for r in range(4)), [])) == items
