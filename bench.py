@@ -109,6 +109,15 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def host_link_peaks():
+    """Host-link peaks measured on the B200 box by tools/probe (profiles/hostlink_peaks.json)."""
+    p = os.path.join(ROOT, "profiles", "hostlink_peaks.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["uva_stream_read_GBps"]), float(d["uva_random4_Mreq_per_s"]), "measured (tools/probe)"
+    return 51.5, 90.0, "assumed"
+
+
 # ------------------------------------------------------------------------------ inputs
 def make_inputs(cfg, device):
     import torch
@@ -364,8 +373,21 @@ def run_ours(args):
         parallel.barrier(local)
         return
     hbm_peak, peak_kind = measured_peaks()
-    achieved_gbs = tot[3] / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per-launch (live events)
-    aggregate_gbs = tot[3] / (ms / 1e3) / 1e9  # all gather launches over the timed wall time
+    # Binding resource of the gather kernel: HBM (hit rows read + every row written + 4 B
+    # slot lookup) vs the host link (miss rows read through UVA).
+    host_peak, host_req_peak, host_kind = host_link_peaks()
+    hits_rows, miss_rows = cn[2], cn[3]
+    hbm_b = hits_rows * 4.0 * D + (hits_rows + miss_rows) * (4.0 * D + 4.0)
+    host_b = miss_rows * 4.0 * D
+    host_bound = host_b / host_peak > hbm_b / hbm_peak
+    bind_b = host_b if host_bound else hbm_b
+    bind_peak = host_peak if host_bound else hbm_peak
+    achieved_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per-launch (live events)
+    aggregate_gbs = bind_b / (ms / 1e3) / 1e9  # all gather launches over the timed wall time
+    host_link = {"feature_miss_GBps": host_b / (ms / 1e3) / 1e9, "peak_GBps": host_peak,
+                 "feature_frac": host_b / (ms / 1e3) / 1e9 / host_peak,
+                 "adj_miss_Mreads_per_s": cn[1] / (ms / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
+                 "peak_kind": host_kind}
     avg_fl = tot[2] / max(1, args.steps * world)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gather_traffic.json")
@@ -386,16 +408,19 @@ def run_ours(args):
         "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
                 "d2h_bytes_per_step": 8 * (L + 1) + 8 * 4 + 4},
         "gpu_launches": int(tot[1]),
-        "roofline": {"bound": "hbm", "kernel": "k_gather (fused route + relabel + feature gather, S7-S8)",
-                     "achieved": achieved_gbs, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (achieved_gbs / hbm_peak) if achieved_gbs else None, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": tot[3] / max(1, tot[6]),
+        "roofline": {"bound": "host-link" if host_bound else "hbm",
+                     "kernel": "k_gather (fused route + relabel + feature gather, S7-S8)",
+                     "achieved": achieved_gbs, "peak": bind_peak,
+                     "peak_kind": host_kind if host_bound else peak_kind, "unit": "GB/s",
+                     "frac": (achieved_gbs / bind_peak) if achieved_gbs else None, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": bind_b / max(1, tot[6]),
                      "avg_gather_ms": tot[4] / max(1, tot[6]), "avg_sample_ms": tot[5] / max(1, tot[6]),
                      "concurrent_batches": (tot[4] + tot[5]) / ms if ms > 0 else None,
-                     "aggregate_achieved": aggregate_gbs, "aggregate_frac": aggregate_gbs / hbm_peak,
+                     "aggregate_achieved": aggregate_gbs, "aggregate_frac": aggregate_gbs / bind_peak,
                      "note": "achieved = algorithmic bytes per launch / mean live launch time (CUDA events on the "
                              "launch stream); with several batches in flight launches overlap, so "
                              "aggregate_achieved = all gather bytes / timed wall time is the device-level rate"},
+        "host_link": host_link,
         "clocks": clocks,
         "stats": {"avg_F_L": avg_fl, "F_L_per_seed": avg_fl / B, **hit_rates,
                   "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre, "fill": t_fill},
