@@ -44,10 +44,15 @@ def parse():
     ap.add_argument("--inflight", type=int, default=6, help="workspaces/streams in flight")
     ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
     ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
+    ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's batch size")
+    ap.add_argument("--presample-batches", type=int, default=8, help="n pre-sampling batches (Fig. 11)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle wall time for cpu_baseline")
     ap.add_argument("--no-check", action="store_true", help="skip the bit-exact spot check vs the oracle")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/check)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo only to test several ranks on one GPU)")
     return ap.parse_args()
 
 
@@ -118,6 +123,16 @@ def host_link_peaks():
     return 51.5, 90.0, "assumed"
 
 
+def _cfg(args):
+    import dataclasses
+    cfg = synth.CONFIGS[args.config]
+    if args.fanouts:
+        cfg = dataclasses.replace(cfg, fanouts=tuple(int(x) for x in args.fanouts.split(",")))
+    if args.batch:
+        cfg = dataclasses.replace(cfg, batch=args.batch)
+    return cfg
+
+
 # ------------------------------------------------------------------------------ inputs
 def make_inputs(cfg, device):
     import torch
@@ -133,7 +148,7 @@ def make_inputs(cfg, device):
 
 
 # ------------------------------------------------------------------------------ oracle (cpu)
-def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_results=None):
+def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_results=None, npre=8):
     """Time the oracle as it stands on host cores: its own presample + fill (reported), then
     inference batches spread over `threads` threads (ctypes releases the GIL), until about
     `seconds` of wall time.  Optionally checks the GPU results of the first batches."""
@@ -141,7 +156,7 @@ def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_re
     from concurrent.futures import ThreadPoolExecutor
     B, fan = cfg.batch, cfg.fanouts
     t0 = time.time()
-    pre = synth.presample_seeds(ip, 8, B)
+    pre = synth.presample_seeds(ip, npre, B)
     nv, ec = oracle.presample(ip, ix, pre, B, fan, synth.PRESAMPLE_SEED)
     R, cl, co, ac = oracle.adj_fill(ip, ix, ec, c_adj)
     slot, _ = oracle.feat_fill(nv, c_feat // (4 * cfg.pitch_floats()))
@@ -181,7 +196,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    cfg = synth.CONFIGS[args.config]
+    cfg = _cfg(args)
     import torch
     # same generator and device as our arm, so both arms see the identical graph
     gen_dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))) if torch.cuda.is_available() else "cpu"
@@ -217,10 +232,12 @@ def run_ours(args):
     import paper_2503_01281_b200 as dci
     from paper_2503_01281_b200 import parallel
 
-    rank, world, local = parallel.init("nccl")
+    rank, world, local = parallel.init(args.backend)
+    # one rank per GPU; (testing only) more ranks than GPUs share devices round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = synth.CONFIGS[args.config]
+    cfg = _cfg(args)
     B, fan, L = cfg.batch, cfg.fanouts, len(cfg.fanouts)
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
 
@@ -236,11 +253,14 @@ def run_ours(args):
     t1 = time.time()
     ctx = dci.load_graph(ip, ix, ft, device=local)
     t_load = time.time() - t1
+    if args.no_cpu_baseline or world > 1 or args.profile_only:
+        ft = None  # the library holds its own pinned copy; free host RAM (papers100M-shaped: 57 GB)
 
     # ---- S1 presample (global list of 8 batches, sharded), C1 allreduce ----
     t2 = time.time()
-    pre = synth.presample_seeds(ip, 8, B)
-    pre_batches = [pre[i * B:(i + 1) * B] for i in range(8)]
+    npre = args.presample_batches
+    pre = synth.presample_seeds(ip, npre, B)
+    pre_batches = [pre[i * B:(i + 1) * B] for i in range(npre)]
     nv = torch.zeros(cfg.N, dtype=torch.int32, device=dev)
     ec = torch.zeros(cfg.E, dtype=torch.int32, device=dev)
     ts_all, tf_all = [], []
@@ -256,6 +276,8 @@ def run_ours(args):
     t3 = time.time()
     C = synth.parse_budget(args.budget or cfg.budget, synth.data_bytes(cfg.N, cfg.E, cfg.D))
     ratio = (int(round(args.ratio * 1000)), 1000) if args.ratio is not None else None
+    if C == 0 and world > 1:  # auto budget: the same C on every replica
+        C = parallel.min_over_ranks_int(sum(dci.allocate(ctx, 0, [S], [F])), device=dev)
     c_adj, c_feat = dci.allocate(ctx, C, [S], [F], ratio=ratio)
     dci.fill(ctx, nv, ec, c_adj, c_feat)
     torch.cuda.synchronize()
@@ -436,7 +458,7 @@ def run_ours(args):
                 dci.sample_gather(ctx, wss[0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
                 gpu_results.append((b, o.result()))
         res, check = oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, args.cpu_seconds, os.cpu_count() or 1,
-                                gpu_results)
+                                gpu_results, npre=args.presample_batches)
         line["cpu_baseline"] = res
         if check:
             line["parity_check"] = check

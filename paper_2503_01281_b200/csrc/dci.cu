@@ -45,6 +45,15 @@ int occupancy_blocks(const void* kernel, int block, int cap) {
 
 namespace {
 
+bool gather_serial() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("DCI_GATHER_SERIAL");
+    mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  return mode == 1;
+}
+
 bool graph_mode() {
   static int mode = -1;
   if (mode < 0) {
@@ -116,7 +125,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
     float ms_s = 0.f, ms_g = 0.f;
     DCI_CUDA(cudaEventElapsedTime(&ms_s, ws->ev_t[0], ws->ev_t[1]));
-    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[1], ws->ev_t[3]));
+    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[2], ws->ev_t[3]));
     ws->acc_sample_ms += ms_s;
     ws->acc_gather_ms += ms_g;
     ws->acc_timed += 1;
@@ -139,7 +148,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
 
   // ---- kernels: a CUDA graph per workspace, re-captured only when the signature changes ----
   struct Sig {
-    int32_t L, pass, prof;
+    int32_t L, pass, prof, serial;
     int32_t fan[DCI_MAX_LAYERS];
     dci_batch_out out;
     const int32_t* nv;
@@ -152,6 +161,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   sig.L = L;
   sig.pass = (int32_t)pass;
   sig.prof = prof ? 1 : 0;
+  sig.serial = gather_serial() && pass == 0 ? 1 : 0;
   for (int i = 0; i < L; ++i) sig.fan[i] = fanouts[i];
   sig.out = *out;
   sig.nv = node_visits;
@@ -161,6 +171,9 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   sig.uidx = ctx->u_idx_cur;
   static_assert(sizeof(Sig) <= sizeof(ws->graph_sig), "signature buffer too small");
   const bool use_graph = graph_mode();
+  // serial gathers: every batch's gather kernel goes through one context-wide stream, so
+  // gathers run one at a time at full bandwidth while other batches sample alongside
+  const bool serial = gather_serial() && pass == 0;
   const bool need_capture =
       use_graph && !(ws->n_graphs && ws->graph_sig_len == sizeof(Sig) && !memcmp(ws->graph_sig, &sig, sizeof(Sig)));
   // part 0: the L sampling hops; part 1: the fused route + gather kernel
@@ -198,7 +211,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   };
   if (need_capture) {
     // one graph per part when profiling (stage events go between them), else one graph
-    const int ngraphs = prof ? 2 : 1;
+    const int ngraphs = (prof || serial) ? 2 : 1;
     for (int gi = 0; gi < 2; ++gi) {
       if (ws->graph_exec[gi]) cudaGraphExecDestroy(ws->graph_exec[gi]);
       ws->graph_exec[gi] = nullptr;
@@ -229,14 +242,14 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     memcpy(ws->graph_sig, &sig, sizeof(Sig));
     ws->graph_sig_len = sizeof(Sig);
   }
-  auto run_part = [&](int part) -> cudaError_t {
+  auto run_part = [&](int part, cudaStream_t rs) -> cudaError_t {
     if (!use_graph) {
-      enqueue_part(part, s);
+      enqueue_part(part, rs);
       return cudaSuccess;
     }
     if (ws->n_graphs == 2) {
       ctx->launches += ws->graph_kernels[part];
-      return cudaGraphLaunch(ws->graph_exec[part], s);
+      return cudaGraphLaunch(ws->graph_exec[part], rs);
     }
     if (part == 0) {
       ctx->launches += ws->graph_kernels[0];
@@ -245,10 +258,22 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     return cudaSuccess;  // single graph holds both parts
   };
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[0], s));
-  DCI_CUDA(run_part(0));
+  DCI_CUDA(run_part(0, s));
   if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[1], s));
-  DCI_CUDA(run_part(1));
-  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], s));
+  if (serial) {
+    if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    DCI_CUDA(cudaEventRecord(ws->ev_mid, s));
+    DCI_CUDA(cudaStreamWaitEvent(ctx->gstream, ws->ev_mid, 0));
+    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[2], ctx->gstream));
+    DCI_CUDA(run_part(1, ctx->gstream));
+    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], ctx->gstream));
+    DCI_CUDA(cudaEventRecord(ws->ev_done, ctx->gstream));
+    DCI_CUDA(cudaStreamWaitEvent(s, ws->ev_done, 0));
+  } else {
+    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[2], s));
+    DCI_CUDA(run_part(1, s));
+    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], s));
+  }
   ws->have_times = prof ? 1 : 0;
   DCI_CUDA(cudaGetLastError());
   return DCI_OK;
@@ -258,6 +283,7 @@ void free_ctx(dci_ctx* c) {
   if (!c) return;
   if (c->pre_ws) dci_workspace_destroy(c->pre_ws);
   if (c->pre_out_mem) cudaFree(c->pre_out_mem);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->d_dir) cudaFree(c->d_dir);
   if (c->d_acache) cudaFree(c->d_acache);
   if (c->d_fcache) cudaFree(c->d_fcache);
@@ -422,6 +448,8 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   if ((e = cudaMalloc(&w->seeds_stage, sizeof(int32_t) * max_batch)) != cudaSuccess) return bail(e, "cudaMalloc");
   for (int i = 0; i < 4; ++i)
     if ((e = cudaEventCreate(&w->ev_t[i])) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_mid, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
                          cudaHostAllocPortable)) != cudaSuccess)
     return bail(e, "cudaHostAlloc(header ring)");
@@ -452,6 +480,8 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     if (w->ev_t[i]) cudaEventDestroy(w->ev_t[i]);
   for (int i = 0; i < dci_workspace::kHdrRing; ++i)
     if (w->hdr_ev[i]) cudaEventDestroy(w->hdr_ev[i]);
+  if (w->ev_mid) cudaEventDestroy(w->ev_mid);
+  if (w->ev_done) cudaEventDestroy(w->ev_done);
   if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
   for (int i = 0; i < 2; ++i)
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
@@ -677,7 +707,7 @@ dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* ga
   DeviceGuard g(ws->ctx->device);
   DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
   if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, ws->ev_t[0], ws->ev_t[1]));
-  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[1], ws->ev_t[3]));
+  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[2], ws->ev_t[3]));
   return DCI_OK;
 }
 
@@ -688,7 +718,7 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   if (ws->have_times) {
     float ms_s = 0.f, ms_g = 0.f;
     DCI_CUDA(cudaEventElapsedTime(&ms_s, ws->ev_t[0], ws->ev_t[1]));
-    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[1], ws->ev_t[3]));
+    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[2], ws->ev_t[3]));
     ws->acc_sample_ms += ms_s;
     ws->acc_gather_ms += ms_g;
     ws->acc_timed += 1;

@@ -77,6 +77,7 @@ struct dci_ctx {
   uint64_t c_adj = 0, c_feat = 0;
   uint64_t presample_peak = 0;
   uint64_t launches = 0;
+  cudaStream_t gstream = nullptr;  // shared gather stream (serial-gather mode)
   // lazily created presample workspace + outputs
   dci_workspace* pre_ws = nullptr;
   int32_t pre_B = 0;
@@ -119,7 +120,8 @@ struct dci_workspace {
   unsigned char graph_sig[512] = {0};
   size_t graph_sig_len = 0;
   uint64_t graph_kernels[2] = {0, 0};
-  // stage events
+  // stage events; ev_mid / ev_done hand the gather to and from the shared gather stream
+  cudaEvent_t ev_mid = nullptr, ev_done = nullptr;
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
   int32_t profiling = 0;
   int32_t have_times = 0;

@@ -66,6 +66,17 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     return float(t.item())
 
 
+def min_over_ranks_int(value: int, device=None, group=None) -> int:
+    """Min of a per-rank integer (e.g. the auto budget, so every replica fills identically)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return int(value)
+    t = torch.tensor([int(value)], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return int(t.item())
+
+
 def sum_over_ranks(values, device=None, group=None):
     """C2: SUM of per-rank counters (seeds processed, hits/misses, bytes) at the end of a run."""
     import torch
@@ -76,10 +87,15 @@ def sum_over_ranks(values, device=None, group=None):
     return t.cpu().numpy()
 
 
+def _ndev():
+    import torch
+    return torch.cuda.device_count()
+
+
 def barrier(device_index=None):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        if dist.get_backend() == "nccl" and device_index is not None:
+        if dist.get_backend() == "nccl" and device_index is not None and dist.get_world_size() <= _ndev():
             dist.barrier(device_ids=[device_index])
         else:
             dist.barrier()

@@ -54,6 +54,8 @@ CONFIGS = {
     "M3": Config("M3-products", 2_449_029, 61_859_140, 100, (8, 4, 2), 1024, "frac:0.25"),
     # configs[3]: papers100M-shaped (host-resident, 8-GPU sharded seeds)
     "M4": Config("M4-papers100M", 111_059_956, 1_615_685_872, 128, (15, 10, 5), 1024, "frac:0.25"),
+    # configs[3] at 1/10 scale: same average in-degree 14.5, host-resident parity case
+    "M4s": Config("M4s-papers100M-tenth", 11_105_996, 161_568_588, 128, (15, 10, 5), 1024, "frac:0.25"),
     # configs[4]: split sweep on products-shaped, r = C_adj/C in 0..1
     "M5": Config("M5-products-sweep", 2_449_029, 61_859_140, 100, (8, 4, 2), 1024, "frac:0.25",
                  tuple(i / 10 for i in range(11))),
