@@ -230,6 +230,18 @@ typedef struct dci_ws_stats {
 
 dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset);
 
+/* --------------------------------------------------------------------------------------
+ * dci_mean_aggregate — NEXT F2: the GraphSAGE mean aggregator the prepared mini-batch feeds
+ * (BJ north_star's optional consumer; O-13):
+ *   H[d][c] = (1/k_d) * sum_{j=bptr[d]}^{bptr[d+1]-1} Xsrc[bsrc[j]][c] for c < D, k_d = 0 -> 0,
+ * for d < *n_dst.  All pointers DEVICE memory: bptr int32[n+1], bsrc int32[...], n_dst int64[1]
+ * (e.g. out->sizes + h, so no host sync is needed), Xsrc fp32 rows of stride ldx (e.g. the
+ * batch's X for the input layer h = L-1), H fp32 rows of stride ldh (caller-owned, >= n
+ * rows).  fp32 accumulation in bsrc order.  Asynchronous on `stream`.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                              const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, void* stream);
+
 /* Kernels launched by this context so far (all workspaces). */
 uint64_t dci_launch_count(const dci_ctx* ctx);
 

@@ -71,6 +71,9 @@ def lib():
         L.oracle_adj_fill.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _i32p, C.c_uint64, _i32p, _i32p, _i64p,
                                       _i32p]
         L.oracle_adj_fill.restype = C.c_int64
+        _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        L.oracle_mean_aggregate.argtypes = [_i32p, _i32p, C.c_int64, _f32p, C.c_int64, C.c_int32, _f64p]
+        L.oracle_mean_aggregate.restype = None
         L.oracle_sample_gather.argtypes = [C.c_int64, _i64p, _i32p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                            _i32p, C.c_int32, _i32p, C.c_int32, C.c_uint64, _i32p, C.c_int64, _i64p,
                                            pp, pp, _i64p, C.c_void_p, C.c_int64, _u64p]
@@ -279,3 +282,17 @@ def adj_fill(indptr, indices, edge_counts, c_adj_bytes: int):
     ac = np.zeros(max(cap_e, 1), np.int32)
     n = lib().oracle_adj_fill(N, E, indptr, indices, cnt, c_adj_bytes, R, cl, co, ac)
     return R[:E], cl[:N], co[:N], ac[:n]
+
+
+def mean_aggregate(bptr, bsrc, X):
+    """O-13 GraphSAGE mean over a block: H[d] = mean of X[bsrc[bptr[d]:bptr[d+1]]] (fp64)."""
+    bptr = np.ascontiguousarray(bptr, np.int32)
+    bsrc = np.ascontiguousarray(bsrc, np.int32)
+    X = np.ascontiguousarray(X, np.float32)
+    n = len(bptr) - 1
+    D = X.shape[1]
+    H = np.zeros((max(n, 1), D), np.float64)
+    if len(bsrc) == 0:
+        bsrc = np.zeros(1, np.int32)
+    lib().oracle_mean_aggregate(bptr, bsrc, n, X, D, D, H)
+    return H[:n]

@@ -355,6 +355,22 @@ int64_t oracle_adj_fill(int64_t N, int64_t E, const int64_t* indptr, const int32
     return off;
 }
 
+// O-13 GraphSAGE mean aggregator over one sampled block (P:107
+// "aggregating" the neighbours' features; BJ north_star's optional consumer; reading C23):
+// H[d][c] = (1 / k_d) * sum_{j = bptr[d]}^{bptr[d+1]-1} X[bsrc[j]][c], accumulated in double;
+// k_d = 0 -> H[d] = 0.
+void oracle_mean_aggregate(const int32_t* bptr, const int32_t* bsrc, int64_t n_dst, const float* X,
+                           int64_t ldx, int32_t D, double* H) {
+    for (int64_t d = 0; d < n_dst; ++d) {
+        int64_t k = bptr[d + 1] - bptr[d];
+        for (int32_t c = 0; c < D; ++c) {
+            double acc = 0.0;
+            for (int64_t j = bptr[d]; j < bptr[d + 1]; ++j) acc += (double)X[(int64_t)bsrc[j] * ldx + c];
+            H[d * D + c] = k > 0 ? acc / (double)k : 0.0;
+        }
+    }
+}
+
 // One inference step on the CPU (bench.py cpu_baseline): O-6 with pass 0 over the
 // current CSC and the adjacency cache, then O-7.  Thin composition, no new arithmetic.
 int32_t oracle_sample_gather(int64_t N, const int64_t* indptr, const int32_t* indices_cur,

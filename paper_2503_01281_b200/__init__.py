@@ -29,7 +29,7 @@ OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
             "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
             "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
-            "dci_workspace_stats", "dci_launch_count", "dci_last_error", "dci_version"]
+            "dci_workspace_stats", "dci_mean_aggregate", "dci_launch_count", "dci_last_error", "dci_version"]
 
 
 class DciError(RuntimeError):
@@ -85,6 +85,7 @@ def lib():
         "dci_workspace_set_profiling": [vp, i32],
         "dci_workspace_stage_ms": [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)],
         "dci_workspace_stats": [vp, C.POINTER(dci_ws_stats), i32],
+        "dci_mean_aggregate": [vp, vp, vp, vp, vp, i64, i32, vp, i64, vp],
         "dci_launch_count": [vp],
         "dci_last_error": [],
         "dci_version": [],
@@ -286,6 +287,24 @@ def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: i
                                         _np_ptr(fan), len(fan), seed, C.byref(out.struct),
                                         sizes_host.data_ptr(), counters_host.data_ptr(), status_host.data_ptr(),
                                         _stream_ptr(stream)), "dci_sample_gather_host")
+
+
+def mean_aggregate(ctx: Context, out: BatchOut, hop: int | None = None, H=None, stream=None):
+    """dci_mean_aggregate (NEXT F2): GraphSAGE mean over block `hop` (default the input
+    layer L-1, whose sources are the rows of out.X).  Returns H [hop_cap, D] (device)."""
+    import torch
+    hop = out.L - 1 if hop is None else hop
+    if hop != out.L - 1:
+        raise ValueError("only the input-layer block has its source rows in out.X")
+    if out.X is None:
+        raise ValueError("out has no X")
+    rows = out.bptr[hop].numel() - 1
+    if H is None:
+        H = torch.empty((max(rows, 1), out.ldx), dtype=torch.float32, device=out.X.device)
+    _check(lib().dci_mean_aggregate(ctx.handle, out.bptr[hop].data_ptr(), out.bsrc[hop].data_ptr(),
+                                    out.sizes.data_ptr() + 8 * hop, out.X.data_ptr(), out.ldx, out.D,
+                                    H.data_ptr(), H.shape[1], _stream_ptr(stream)), "dci_mean_aggregate")
+    return H
 
 
 def presample(ctx: Context, seeds, batch: int, fanouts, seed: int, node_visits, edge_counts, stream=None):

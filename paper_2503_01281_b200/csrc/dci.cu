@@ -743,6 +743,14 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   return DCI_OK;
 }
 
+dci_status dci_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                              const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, void* stream) {
+  if (!ctx || !bptr || !bsrc || !n_dst || !Xsrc || !H) return fail(DCI_EINVAL, "null argument");
+  if (D < 1 || ldx < D || ldh < D) return fail(DCI_EINVAL, "need D >= 1, ldx >= D, ldh >= D");
+  DeviceGuard g(ctx->device);
+  return launch_mean_aggregate(ctx, bptr, bsrc, n_dst, Xsrc, ldx, D, H, ldh, static_cast<cudaStream_t>(stream));
+}
+
 uint64_t dci_launch_count(const dci_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 }  // extern "C"

@@ -166,6 +166,10 @@ void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaSt
 void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
 
+// aggregate.cu
+dci_status launch_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                                 const float* X, int64_t ldx, int32_t D, float* H, int64_t ldh, cudaStream_t s);
+
 // fill.cu
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
                      uint64_t c_feat, cudaStream_t s);

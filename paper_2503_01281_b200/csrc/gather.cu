@@ -17,16 +17,26 @@ namespace dci {
 
 namespace {
 
-__device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
+// L2 policy for the streaming feature traffic (rows read once per batch, X written once):
+// evict-first, so ~700 MB/batch of streaming bytes do not flush the small hot structures
+// (directory, adjacency cache lines, position tables) out of the 126 MB L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ int4 ld_stream_v4(const int4* p, uint64_t pol) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
   return r;
 }
 
-__device__ __forceinline__ void st_v4(int4* p, const int4& v) {
-  asm volatile("st.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+__device__ __forceinline__ void st_v4(int4* p, const int4& v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
 }
 
@@ -82,6 +92,7 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
     if (tid == 0) sc->tickets[a.L - 1] = 0;
   }
   const int64_t n = sc->sizes[a.L];
+  const uint64_t pol = policy_evict_first();
   const int64_t warp = tid >> 5;
   const int64_t nwarps = nthreads >> 5;
   uint32_t hits = 0, misses = 0;
@@ -107,12 +118,12 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 #pragma unroll
           for (int j = 0; j < VPL; ++j) {
             const int idx = c0 + lane + 32 * j;
-            if (idx < row16) buf[j] = ld_stream_v4(s4 + idx);
+            if (idx < row16) buf[j] = ld_stream_v4(s4 + idx, pol);
           }
 #pragma unroll
           for (int j = 0; j < VPL; ++j) {
             const int idx = c0 + lane + 32 * j;
-            if (idx < row16) st_v4(d4 + idx, buf[j]);
+            if (idx < row16) st_v4(d4 + idx, buf[j], pol);
           }
         }
       } else if (MODE == 1) {

@@ -191,3 +191,31 @@ def test_host_seed_variant(small):
     _assert_batch_equal(out.result(), o, 2)
     assert sizes.numpy().tolist() == o.sizes.tolist()
     assert cnt.numpy().astype(np.uint64).tolist() == o.counters.tolist() and stt.item() == 0
+
+
+def _agg_tol(bp, X, H_ref):
+    """|g - r| <= 1e-5 |r| + k_d * 2^-23 * max|x| (fp32 sequential sum of k_d terms, then one
+    division)."""
+    k = np.diff(bp).astype(np.float64)[:, None]
+    return 1e-5 * np.abs(H_ref) + k * 2.0 ** -23 * float(np.abs(X).max() if X.size else 0.0)
+
+
+@pytest.mark.parametrize("D,ldx", [(13, None), (13, 13), (64, None), (602, None)])
+def test_mean_aggregate_parity(D, ldx):
+    """NEXT F2: GraphSAGE mean over the input-layer block vs the fp64 oracle (O-13)."""
+    ip, ix, ft = _graph(6000, 70000, 31, D)
+    ctx = dci.load_graph(ip, ix, ft)
+    fan = (10, 5)
+    ws = dci.workspace_create(ctx, 80, fan)
+    seeds = np.concatenate([np.nonzero(np.diff(ip) == 0)[0][:4], synth.inference_batches(ip, 76)[0]]).astype(np.int32)
+    out = dci.BatchOut(ctx, len(seeds), fan, ldx=ldx)
+    dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(DEV), fan, 5, out)
+    H = dci.mean_aggregate(ctx, out)
+    g = out.result()
+    o = oracle.sample_gather(ip, ix, ft, seeds, fan, 5)
+    _assert_batch_equal(g, o, 2)
+    L = 2
+    Hr = oracle.mean_aggregate(o.bptr[L - 1], o.bsrc[L - 1], o.X)
+    Hg = H[: len(o.bptr[L - 1]) - 1, :D].cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(Hg - Hr) <= _agg_tol(o.bptr[L - 1], o.X, Hr))
+    assert np.all(Hg[np.diff(o.bptr[L - 1]) == 0] == 0)

@@ -192,3 +192,26 @@ def test_presample_ledger_identities(tiny_graph):
     assert int(ec.sum()) == samples and int(nv.sum()) == fl
     assert np.array_equal(nv, nv2)
     assert np.all(ec <= 4 * 2)  # at most once per hop per batch
+
+
+def test_mean_aggregate_equals_sparse_normalised_product(tiny_graph):
+    """O-13 against scipy.sparse: H = diag(1/k) . A_block . X, with A_block the sampled block
+    (bptr, bsrc) as a 0/1 matrix with multiplicity; zero-degree dst rows give 0."""
+    indptr, indices = tiny_graph
+    N = len(indptr) - 1
+    feats = synth.features(N, 11).numpy()
+    seeds = np.concatenate([np.nonzero(np.diff(indptr) == 0)[0][:3], synth.inference_batches(indptr, 40)[0]])
+    b = oracle.sample_gather(indptr, indices, feats, seeds.astype(np.int32), (4, 3), seed=4)
+    L = 2
+    bp, bs = b.bptr[L - 1], b.bsrc[L - 1]
+    n_dst = len(bp) - 1
+    H = oracle.mean_aggregate(bp, bs, b.X)
+    A = sp.csr_matrix((np.ones(len(bs)), bs, bp.astype(np.int64)), shape=(n_dst, len(b.F)))
+    k = np.diff(bp).astype(np.float64)
+    ref = sp.diags(np.where(k > 0, 1.0 / np.maximum(k, 1), 0.0)) @ (A @ b.X.astype(np.float64))
+    assert np.allclose(H, ref, rtol=1e-12, atol=1e-12)
+    assert np.all(H[k == 0] == 0) and np.any(k == 0)
+    # identical source rows -> the mean is that row
+    Xc = np.tile(b.X[:1], (len(b.F), 1))
+    Hc = oracle.mean_aggregate(bp, bs, Xc)
+    assert np.allclose(Hc[k > 0], np.tile(b.X[:1].astype(np.float64), (int((k > 0).sum()), 1)), rtol=0, atol=0)
