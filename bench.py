@@ -114,12 +114,24 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def host_link_peaks():
-    """Host-link peaks measured on the B200 box by tools/probe (profiles/hostlink_peaks.json)."""
+def host_link_peaks(region_bytes: float = 0.0):
+    """Host-link peaks measured on the B200 box by tools/probe (profiles/hostlink_peaks.json):
+    the random-row read rate for a pinned region of this size (it falls from ~51 GB/s at 1 GB
+    to ~22 GB/s at 64 GB), else the streaming read rate."""
     p = os.path.join(ROOT, "profiles", "hostlink_peaks.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["uva_stream_read_GBps"]), float(d["uva_random4_Mreq_per_s"]), "measured (tools/probe)"
+        peak, kind = float(d["uva_stream_read_GBps"]), "measured streaming UVA read (tools/probe)"
+        tab = d.get("random_512B_rows_GBps_by_region_GB")
+        if tab and region_bytes > 0:
+            pts = sorted((float(k), float(v)) for k, v in tab.items())
+            gb = region_bytes / 2 ** 30
+            peak = pts[0][1] if gb <= pts[0][0] else pts[-1][1]
+            for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+                if x0 <= gb <= x1:
+                    peak = y0 + (y1 - y0) * (gb - x0) / (x1 - x0)
+            kind = f"measured random-row UVA read for a {gb:.1f} GB pinned region (tools/probe)"
+        return peak, float(d["uva_random4_Mreq_per_s"]), kind
     return 51.5, 90.0, "assumed"
 
 
@@ -397,7 +409,7 @@ def run_ours(args):
     hbm_peak, peak_kind = measured_peaks()
     # Binding resource of the gather kernel: HBM (hit rows read + every row written + 4 B
     # slot lookup) vs the host link (miss rows read through UVA).
-    host_peak, host_req_peak, host_kind = host_link_peaks()
+    host_peak, host_req_peak, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats())
     hits_rows, miss_rows = cn[2], cn[3]
     hbm_b = hits_rows * 4.0 * D + (hits_rows + miss_rows) * (4.0 * D + 4.0)
     host_b = miss_rows * 4.0 * D
