@@ -1,0 +1,96 @@
+"""Randomised GPU parity: many small random configurations (graph shape, hubs, fan-outs 1..32,
+1..4 hops, ragged batch sizes, budgets and explicit splits, presample sizes), each compared bit
+for bit against the oracle — presample counts, fill (cache state), and several batches."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._util import random_csc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2503_01281_b200 as dci  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _graph(rng, kind):
+    if kind == "rmat":
+        N = int(rng.integers(50, 4000))
+        E = 2 * int(rng.integers(N // 2, 12 * N))
+        ip, ix = synth.rmat_csc(N, E, seed=int(rng.integers(1, 1 << 30)))
+        return ip.numpy(), ix.numpy()
+    if kind == "hub":  # a few very high in-degree nodes (Floyd path with deg >> f)
+        N = int(rng.integers(100, 2000))
+        deg = rng.integers(0, 6, N)
+        deg[rng.choice(N, 3, replace=False)] = rng.integers(500, 3000, 3)
+        ip = np.zeros(N + 1, np.int64)
+        ip[1:] = np.cumsum(deg)
+        ix = rng.integers(0, N, int(ip[-1])).astype(np.int32)
+        return ip, ix
+    N = int(rng.integers(5, 300))
+    return random_csc(rng, N, int(rng.integers(1, 40)))
+
+
+@pytest.mark.parametrize("trial", range(24))
+def test_random_configuration(trial):
+    rng = np.random.default_rng(1000 + trial)
+    ip, ix = _graph(rng, ["rmat", "hub", "uniform"][trial % 3])
+    N, E = len(ip) - 1, len(ix)
+    D = int(rng.choice([1, 3, 4, 8, 33, 100]))
+    ft = synth.features(N, D).numpy()
+    L = int(rng.integers(1, 5))
+    fan = tuple(int(x) for x in rng.integers(1, 33, L))
+    B = int(rng.integers(1, min(N, 300) + 1))
+    ctx = dci.load_graph(ip, ix, ft)
+    # presample (random number of batches, ragged last batch)
+    el = synth.eligible_nodes(ip)
+    if len(el) == 0:
+        pytest.skip("graph without edges")
+    npre = int(rng.integers(1, min(len(el), 4 * B) + 1))
+    pre = rng.permutation(el)[:npre].astype(np.int32)
+    pb = int(rng.integers(1, B + 1))
+    nv = torch.zeros(N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(max(E, 1), dtype=torch.int32, device=DEV)
+    ts, tf = dci.presample(ctx, torch.from_numpy(pre).to(DEV), pb, fan, 77, nv, ec)
+    nv_o, ec_o = oracle.presample(ip, ix, pre, pb, fan, 77)
+    assert np.array_equal(nv.cpu().numpy(), nv_o)
+    assert np.array_equal(ec.cpu().numpy()[:E], ec_o)
+    # random budget and split
+    C = int(rng.integers(0, 2 * synth.data_bytes(N, E, D) + 64)) + 1
+    r = int(rng.integers(0, 101))
+    c_adj, c_feat = dci.allocate(ctx, C, ts, tf, ratio=(r, 100))
+    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    st = dci.cache_state(ctx)
+    R, cl, co, ac = oracle.adj_fill(ip, ix, ec_o, c_adj)
+    slot_o, adm = oracle.feat_fill(nv_o, c_feat // (4 * ((D + 3) // 4 * 4)))
+    assert np.array_equal(st["indices_cur"], R)
+    assert np.array_equal(st["cached_len"], cl)
+    assert np.array_equal(st["slot_of"], slot_o)
+    for v in np.nonzero(cl)[0]:
+        a = st["cache_off"][v]
+        assert np.array_equal(st["acache"][a:a + cl[v]], ac[co[v]:co[v] + cl[v]])
+    if len(adm):
+        assert np.array_equal(st["fcache"][:, :D], ft[adm])
+    ws = dci.workspace_create(ctx, B, fan)
+    seed = int(rng.integers(0, 1 << 62))
+    for _ in range(3):
+        b = int(rng.integers(0, B + 1))
+        seeds = rng.choice(N, size=min(b, N), replace=False).astype(np.int32)
+        out = dci.BatchOut(ctx, len(seeds), fan)
+        dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(DEV), fan, seed, out)
+        g = out.result()
+        o = oracle.sample_gather(ip, R, ft, seeds, fan, seed, cl, slot_o)
+        assert g["status"] == 0
+        assert np.array_equal(g["F"], o.F)
+        assert np.array_equal(g["sizes"], o.sizes)
+        for h in range(L):
+            assert np.array_equal(g["bptr"][h], o.bptr[h])
+            assert np.array_equal(g["bsrc"][h], o.bsrc[h])
+        assert np.array_equal(g["counters"], o.counters)
+        assert np.array_equal(g["X"], o.X)
