@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch size")
     ap.add_argument("--presample-batches", type=int, default=8, help="n pre-sampling batches (Fig. 11)")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="NEXT F1: partition the feature cache across ranks (peer reads over NVLink)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle wall time for cpu_baseline")
     ap.add_argument("--no-check", action="store_true", help="skip the bit-exact spot check vs the oracle")
@@ -291,7 +293,14 @@ def run_ours(args):
     if C == 0 and world > 1:  # auto budget: the same C on every replica
         C = parallel.min_over_ranks_int(sum(dci.allocate(ctx, 0, [S], [F])), device=dev)
     c_adj, c_feat = dci.allocate(ctx, C, [S], [F], ratio=ratio)
-    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    if args.partitioned and world > 1:
+        dci.fill_partitioned(ctx, nv, ec, c_adj, c_feat, world, rank)
+        torch.cuda.synchronize()
+        parallel.barrier(local)
+        parallel.exchange_feature_partitions(ctx)
+        parallel.barrier(local)
+    else:
+        dci.fill(ctx, nv, ec, c_adj, c_feat)
     torch.cuda.synchronize()
     t_fill = time.time() - t3
     info = dci.cache_info(ctx)
@@ -435,7 +444,10 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
         "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B, "fanouts": list(fan),
                    "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
-                   "ratio": args.ratio, "parallelism": f"dp{world} (replicated caches)", "inflight": nws,
+                   "ratio": args.ratio,
+                   "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
+                                                    if args.partitioned and world > 1 else "replicated caches") + ")",
+                   "inflight": nws,
                    "l2": "inputs larger than L2 (feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
                          % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
                             avg_fl * D * 4 / 1e6)},

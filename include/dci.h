@@ -183,10 +183,32 @@ dci_status dci_fill(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edg
                     uint64_t c_feat, void* stream);
 
 /* --------------------------------------------------------------------------------------
+ * NEXT F1 — NVLink-partitioned feature cache (BJ north_star: "a partitioned cache read over
+ * NVLink peer access").  All `world` ranks fill with the same (allreduced) counts; the admitted
+ * set is the top min(N, world * floor(c_feat / (4*pitch))) nodes (O-11 with that capacity,
+ * slots in ascending id), and global slot s is stored on rank s % world at row s / world.
+ * c_feat is the budget of ONE partition (one GPU).  The adjacency cache stays replicated.
+ *  rank in [0, world): this device holds only its partition; exchange partitions with
+ *    dci_feature_partition_handle (a 64-byte CUDA IPC handle of the local rows) and
+ *    dci_attach_feature_partitions (all ranks' handles, rank-major) before sampling; hits on
+ *    other partitions are then peer loads over NVLink (P2P through CUDA IPC mappings).
+ *  rank == -1: all partitions live on this device (single-device emulation / testing).
+ * Synchronises `stream`.  Errors: DCI_EINVAL (world not in 1..16, rank out of range).
+ * ------------------------------------------------------------------------------------ */
+#define DCI_IPC_HANDLE_BYTES 64
+dci_status dci_fill_partitioned(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts,
+                                uint64_t c_adj, uint64_t c_feat, int32_t world, int32_t rank, void* stream);
+dci_status dci_feature_partition_handle(dci_ctx* ctx, void* handle /* DCI_IPC_HANDLE_BYTES */);
+dci_status dci_attach_feature_partitions(dci_ctx* ctx, const void* handles /* world * 64 bytes */,
+                                         int32_t world);
+
+/* --------------------------------------------------------------------------------------
  * Introspection (parity tests).  Every output pointer is HOST memory and may be NULL.
  *  cached_len int32[N], cache_off int64[N] (element offset of v's prefix in acache),
- *  slot_of int32[N] (-1 = not cached), acache int32[info.adj_elems] (prefixes laid out in
- *  ascending node id), fcache fp32[info.feat_rows * pitch], indices_cur int32[E] (the
+ *  slot_of int32[N] (-1 = not cached; a global slot when partitioned), acache
+ *  int32[info.adj_elems] (prefixes laid out in ascending node id), fcache
+ *  fp32[info.feat_rows * pitch] (this device's rows; partition by partition when emulated),
+ *  indices_cur int32[E] (the
  *  current host CSC: original before fill, level-2 reordered after).
  * ------------------------------------------------------------------------------------ */
 typedef struct dci_cache_info {
@@ -197,7 +219,10 @@ typedef struct dci_cache_info {
   int32_t whole_fit;      /* 1 if the whole CSC is cached (Alg. 1 lines 1-3) */
   uint64_t c_adj, c_feat; /* bytes granted by the last fill */
   int64_t adj_elems;      /* elements in the adjacency cache */
-  int64_t feat_rows;      /* rows in the feature cache */
+  int64_t feat_rows;      /* feature-cache rows held on this device */
+  int64_t feat_rows_total; /* rows over all feature partitions (== feat_rows unless partitioned) */
+  int32_t feat_partitions; /* 1, or the partition count of dci_fill_partitioned */
+  int32_t pad_;
   uint64_t presample_peak_bytes;
   uint64_t launches;      /* kernels this context has launched so far */
 } dci_cache_info;

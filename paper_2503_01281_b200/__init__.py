@@ -29,7 +29,9 @@ OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
             "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
             "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
-            "dci_workspace_stats", "dci_mean_aggregate", "dci_launch_count", "dci_last_error", "dci_version"]
+            "dci_workspace_stats", "dci_mean_aggregate", "dci_fill_partitioned", "dci_feature_partition_handle",
+            "dci_attach_feature_partitions", "dci_launch_count", "dci_last_error", "dci_version"]
+IPC_HANDLE_BYTES = 64
 
 
 class DciError(RuntimeError):
@@ -54,7 +56,8 @@ class dci_ws_stats(C.Structure):
 class dci_cache_info(C.Structure):
     _fields_ = [("state", C.c_int32), ("pitch", C.c_int32), ("N", C.c_int64), ("E", C.c_int64), ("D", C.c_int32),
                 ("whole_fit", C.c_int32), ("c_adj", C.c_uint64), ("c_feat", C.c_uint64), ("adj_elems", C.c_int64),
-                ("feat_rows", C.c_int64), ("presample_peak_bytes", C.c_uint64), ("launches", C.c_uint64)]
+                ("feat_rows", C.c_int64), ("feat_rows_total", C.c_int64), ("feat_partitions", C.c_int32),
+                ("pad_", C.c_int32), ("presample_peak_bytes", C.c_uint64), ("launches", C.c_uint64)]
 
 
 _lib = None
@@ -80,6 +83,9 @@ def lib():
         "dci_presample": [vp, vp, i64, i32, vp, i32, u64, vp, vp, vp, vp, vp],
         "dci_allocate": [vp, u64, vp, vp, i32, i64, i64, C.POINTER(u64), C.POINTER(u64)],
         "dci_fill": [vp, vp, vp, u64, u64, vp],
+        "dci_fill_partitioned": [vp, vp, vp, u64, u64, i32, i32, vp],
+        "dci_feature_partition_handle": [vp, vp],
+        "dci_attach_feature_partitions": [vp, vp, i32],
         "dci_cache_info_get": [vp, C.POINTER(dci_cache_info)],
         "dci_cache_state": [vp, vp, vp, vp, vp, vp, vp],
         "dci_workspace_set_profiling": [vp, i32],
@@ -340,6 +346,28 @@ def fill(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat: int, stream
     """dci_fill (S3 + S4)."""
     _check(lib().dci_fill(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None, c_adj,
                           c_feat, _stream_ptr(stream)), "dci_fill")
+
+
+def fill_partitioned(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat: int, world: int, rank: int,
+                     stream=None):
+    """dci_fill_partitioned (NEXT F1): the feature cache spans `world` partitions (c_feat per
+    partition); rank -1 = all partitions on this device (emulation)."""
+    _check(lib().dci_fill_partitioned(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None,
+                                      c_adj, c_feat, world, rank, _stream_ptr(stream)), "dci_fill_partitioned")
+
+
+def feature_partition_handle(ctx: Context) -> bytes:
+    """dci_feature_partition_handle: 64-byte CUDA IPC handle of this device's partition."""
+    buf = (C.c_char * IPC_HANDLE_BYTES)()
+    _check(lib().dci_feature_partition_handle(ctx.handle, buf), "dci_feature_partition_handle")
+    return bytes(buf)
+
+
+def attach_feature_partitions(ctx: Context, handles):
+    """dci_attach_feature_partitions: open the other ranks' partitions (rank-major handles)."""
+    blob = b"".join(handles)
+    buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+    _check(lib().dci_attach_feature_partitions(ctx.handle, buf, len(handles)), "dci_attach_feature_partitions")
 
 
 def cache_info(ctx: Context) -> dict:

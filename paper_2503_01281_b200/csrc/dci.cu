@@ -156,6 +156,8 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     const void* acache;
     const void* fcache;
     const void* uidx;
+    const void* fbases;
+    int32_t G;
   } sig;
   memset(&sig, 0, sizeof(sig));
   sig.L = L;
@@ -169,6 +171,8 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   sig.acache = ctx->d_acache;
   sig.fcache = ctx->d_fcache;
   sig.uidx = ctx->u_idx_cur;
+  sig.fbases = ctx->d_fbases;
+  sig.G = ctx->fpart_world;
   static_assert(sizeof(Sig) <= sizeof(ws->graph_sig), "signature buffer too small");
   const bool use_graph = graph_mode();
   // serial gathers: every batch's gather kernel goes through one context-wide stream, so
@@ -286,6 +290,8 @@ void free_ctx(dci_ctx* c) {
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->d_dir) cudaFree(c->d_dir);
   if (c->d_acache) cudaFree(c->d_acache);
+  release_feature_partitions(c);
+  if (c->d_fbases) cudaFree(c->d_fbases);
   if (c->d_fcache) cudaFree(c->d_fcache);
   if (c->h_idx_cur && c->h_idx_cur != c->h_idx_orig) cudaFreeHost(c->h_idx_cur);
   if (c->h_idx_orig) cudaFreeHost(c->h_idx_orig);
@@ -645,7 +651,48 @@ dci_status dci_fill(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edg
   if (!node_visits || (ctx->E > 0 && !edge_counts)) return fail(DCI_EINVAL, "null count array");
   DeviceGuard g(ctx->device);
   DCI_CUDA(cudaDeviceSynchronize());  // no batch may be in flight while caches change
-  return fill_impl(ctx, node_visits, edge_counts, c_adj, c_feat, static_cast<cudaStream_t>(stream));
+  return fill_impl(ctx, node_visits, edge_counts, c_adj, c_feat, 1, 0, static_cast<cudaStream_t>(stream));
+}
+
+dci_status dci_fill_partitioned(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts,
+                                uint64_t c_adj, uint64_t c_feat, int32_t world, int32_t rank, void* stream) {
+  if (!ctx) return fail(DCI_EINVAL, "null context");
+  if (!node_visits || (ctx->E > 0 && !edge_counts)) return fail(DCI_EINVAL, "null count array");
+  if (world < 1 || world > dci_ctx::kMaxParts || rank < -1 || rank >= world)
+    return fail(DCI_EINVAL, "need 1 <= world <= 16 and -1 <= rank < world");
+  DeviceGuard g(ctx->device);
+  DCI_CUDA(cudaDeviceSynchronize());
+  return fill_impl(ctx, node_visits, edge_counts, c_adj, c_feat, world, rank, static_cast<cudaStream_t>(stream));
+}
+
+dci_status dci_feature_partition_handle(dci_ctx* ctx, void* handle) {
+  if (!ctx || !handle) return fail(DCI_EINVAL, "bad arguments");
+  if (!ctx->d_fcache) return fail(DCI_ESTATE, "no feature partition on this device (fill first)");
+  static_assert(sizeof(cudaIpcMemHandle_t) == DCI_IPC_HANDLE_BYTES, "IPC handle size");
+  DeviceGuard g(ctx->device);
+  cudaIpcMemHandle_t h;
+  DCI_CUDA(cudaIpcGetMemHandle(&h, ctx->d_fcache));
+  memcpy(handle, &h, sizeof(h));
+  return DCI_OK;
+}
+
+dci_status dci_attach_feature_partitions(dci_ctx* ctx, const void* handles, int32_t world) {
+  if (!ctx || !handles) return fail(DCI_EINVAL, "bad arguments");
+  if (ctx->fpart_rank < 0 || world != ctx->fpart_world)
+    return fail(DCI_ESTATE, "context was not filled with dci_fill_partitioned(world, rank >= 0)");
+  DeviceGuard g(ctx->device);
+  for (int p = 0; p < world; ++p) {
+    if (p == ctx->fpart_rank) continue;
+    if (ctx->ipc_opened[p]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + (size_t)p * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    DCI_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->ipc_opened[p] = ptr;
+    ctx->h_fbases[p] = static_cast<const float*>(ptr);
+  }
+  DCI_CUDA(cudaMemcpy(ctx->d_fbases, ctx->h_fbases, sizeof(float*) * dci_ctx::kMaxParts, cudaMemcpyHostToDevice));
+  return DCI_OK;
 }
 
 dci_status dci_cache_info_get(const dci_ctx* ctx, dci_cache_info* info) {
@@ -660,6 +707,8 @@ dci_status dci_cache_info_get(const dci_ctx* ctx, dci_cache_info* info) {
   info->c_feat = ctx->c_feat;
   info->adj_elems = ctx->acache_len;
   info->feat_rows = ctx->fcache_rows;
+  info->feat_rows_total = ctx->fcache_total_rows;
+  info->feat_partitions = ctx->fpart_world;
   info->presample_peak_bytes = ctx->presample_peak;
   info->launches = ctx->launches;
   return DCI_OK;

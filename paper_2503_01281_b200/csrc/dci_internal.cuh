@@ -73,6 +73,16 @@ struct dci_ctx {
   int64_t acache_len = 0;
   float* d_fcache = nullptr;
   int64_t fcache_rows = 0;
+  // feature-cache partitions (NEXT F1): global slot s lives in partition s % fpart_world at
+  // row s / fpart_world; d_fbases[p] = that partition's rows (local, or a peer GPU's rows
+  // opened through CUDA IPC and read over NVLink).  fpart_world = 1: one local cache.
+  static constexpr int kMaxParts = 16;
+  int32_t fpart_world = 1;
+  int32_t fpart_rank = 0;          // -1: all partitions emulated on this device
+  int64_t fcache_total_rows = 0;   // rows over all partitions
+  const float* h_fbases[kMaxParts] = {nullptr};
+  void* ipc_opened[kMaxParts] = {nullptr};
+  const float** d_fbases = nullptr;
   int32_t whole_fit = 0;
   uint64_t c_adj = 0, c_feat = 0;
   uint64_t presample_peak = 0;
@@ -172,8 +182,9 @@ dci_status launch_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_
 
 // fill.cu
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
-                     uint64_t c_feat, cudaStream_t s);
+                     uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s);
 void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t s);
+void release_feature_partitions(dci_ctx* ctx);
 
 inline int grid_for(const dci_ctx* ctx, int blocks_per_sm) { return ctx->num_sms * blocks_per_sm; }
 

@@ -364,6 +364,29 @@ __global__ void k_copy_rows_from_host(const int64_t* __restrict__ list, int64_t 
   }
 }
 
+// Copy admitted rows host -> this device's partition(s).  Global slot s belongs to partition
+// s % G at row s / G; rank >= 0 copies only its own partition's rows, rank = -1 (emulation)
+// copies every partition into one buffer laid out partition by partition.
+__global__ void k_copy_rows_partitioned(const int64_t* __restrict__ list, int64_t n, const float* __restrict__ src,
+                                        int32_t pitch, float* __restrict__ dst, int32_t G, int32_t rank) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int row16 = pitch >> 2;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const int64_t ent = list[r];
+    const int64_t slot = ent >> 32, v = ent & 0xffffffffll;
+    const int32_t part = (int32_t)(slot % G);
+    if (rank >= 0 && part != rank) continue;
+    int64_t row = slot / G;
+    if (rank < 0)
+      for (int32_t q = 0; q < part; ++q) row += (n - q + G - 1) / G;  // rows of earlier partitions
+    const int4* sp = reinterpret_cast<const int4*>(src + v * pitch);
+    int4* dp = reinterpret_cast<int4*>(dst + row * pitch);
+    for (int c = lane; c < row16; c += 32) dp[c] = sp[c];
+  }
+}
+
 __global__ void k_dir_reset_caches(DirEntry* dir, int64_t N) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x) {
     dir[v].cached_len = 0;
@@ -407,11 +430,21 @@ void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t 
   ++ctx->launches;
 }
 
+void release_feature_partitions(dci_ctx* ctx) {
+  for (int p = 0; p < dci_ctx::kMaxParts; ++p) {
+    if (ctx->ipc_opened[p]) cudaIpcCloseMemHandle(ctx->ipc_opened[p]);
+    ctx->ipc_opened[p] = nullptr;
+    ctx->h_fbases[p] = nullptr;
+  }
+}
+
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
-                     uint64_t c_feat, cudaStream_t s) {
+                     uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s) {
   const int64_t N = ctx->N, E = ctx->E;
   const int64_t row_bytes = 4ll * ctx->pitch;
-  const int64_t cap_rows = (int64_t)std::min<uint64_t>((uint64_t)N, c_feat / (uint64_t)row_bytes);
+  // c_feat is the budget of ONE partition; the admitted set spans all `world` partitions
+  const int64_t cap_part = (int64_t)std::min<uint64_t>((uint64_t)N, c_feat / (uint64_t)row_bytes);
+  const int64_t cap_rows = std::min<int64_t>(N, cap_part * (int64_t)world);
   const uint64_t cap_e_raw = c_adj / 4;
   const bool whole_fit = (uint64_t)E <= cap_e_raw;
   const int64_t cap_e = whole_fit ? E : (int64_t)cap_e_raw;
@@ -485,10 +518,14 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
   DCI_CUDA(cudaStreamSynchronize(s));
   if (ctx->d_acache) cudaFree(ctx->d_acache);
   if (ctx->d_fcache) cudaFree(ctx->d_fcache);
+  release_feature_partitions(ctx);
   ctx->d_acache = nullptr;
   ctx->d_fcache = nullptr;
   ctx->acache_len = 0;
   ctx->fcache_rows = 0;
+  ctx->fcache_total_rows = 0;
+  ctx->fpart_world = world;
+  ctx->fpart_rank = rank;
   k_dir_reset_caches<<<grid_for(ctx, 4), 256, 0, s>>>(ctx->d_dir, N);
   ++ctx->launches;
 
@@ -529,14 +566,36 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     FeatSlotOp op{fk, stp, ctx->d_dir, d_list};
     dci_status r = scan_nodes(ctx, op, N, d_sum, s);
     if (r != DCI_OK) return r;
-    DCI_CUDA(cudaMalloc(&ctx->d_fcache, (size_t)row_bytes * cap_rows));
-    k_copy_rows_from_host<<<grid_for(ctx, 8), 256, 0, s>>>(d_list, cap_rows, ctx->u_feats, ctx->pitch,
-                                                            ctx->d_fcache);
+    // rows held on this device: all of them (world 1 or emulation), else this rank's share
+    const int64_t local_rows = rank < 0 || world == 1 ? cap_rows : (cap_rows - rank + world - 1) / world;
+    DCI_CUDA(cudaMalloc(&ctx->d_fcache, (size_t)row_bytes * std::max<int64_t>(local_rows, 1)));
+    if (world == 1) {
+      k_copy_rows_from_host<<<grid_for(ctx, 8), 256, 0, s>>>(d_list, cap_rows, ctx->u_feats, ctx->pitch,
+                                                              ctx->d_fcache);
+    } else {
+      k_copy_rows_partitioned<<<grid_for(ctx, 8), 256, 0, s>>>(d_list, cap_rows, ctx->u_feats, ctx->pitch,
+                                                                ctx->d_fcache, world, rank);
+    }
     ++ctx->launches;
     DCI_CUDA(cudaStreamSynchronize(s));
     cudaFree(d_list);
-    ctx->fcache_rows = cap_rows;
+    ctx->fcache_rows = local_rows;
+    ctx->fcache_total_rows = cap_rows;
   }
+  // partition base pointers (peers are attached later through dci_attach_feature_partitions)
+  int64_t off = 0;
+  for (int p = 0; p < world; ++p) {
+    const int64_t rows_p = (cap_rows - p + world - 1) / world;
+    if (rank < 0)
+      ctx->h_fbases[p] = ctx->d_fcache + off * ctx->pitch;
+    else if (p == rank)
+      ctx->h_fbases[p] = ctx->d_fcache;
+    off += rows_p;
+  }
+  if (world == 1) ctx->h_fbases[0] = ctx->d_fcache;
+  if (!ctx->d_fbases) DCI_CUDA(cudaMalloc(&ctx->d_fbases, sizeof(float*) * dci_ctx::kMaxParts));
+  DCI_CUDA(cudaMemcpyAsync(ctx->d_fbases, ctx->h_fbases, sizeof(float*) * dci_ctx::kMaxParts,
+                           cudaMemcpyHostToDevice, s));
   DCI_CUDA(cudaGetLastError());
   DCI_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_indptr);

@@ -57,6 +57,8 @@ struct FusedArgs {
   int64_t last_ntiles;
   // feature rows
   const float* fcache;
+  const float* const* fbases;  // feature partitions (G > 1): slot s -> fbases[s % G] + (s / G) rows
+  int32_t G;
   const float* hfeats;  // device alias of the pinned host feature table
   int32_t pitch;
   int32_t D;
@@ -108,7 +110,15 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
     if (nxt < n) vn = a.F[nxt];
     const bool ok = v >= 0 && (int64_t)v < a.N;
     if (ok) {
-      const float* src = slot >= 0 ? a.fcache + (int64_t)slot * a.pitch : a.hfeats + (int64_t)v * a.pitch;
+      const float* src;
+      if (slot < 0)
+        src = a.hfeats + (int64_t)v * a.pitch;
+      else if (a.G == 1)
+        src = a.fcache + (int64_t)slot * a.pitch;
+      else  // partitioned cache: local or peer (NVLink) rows
+        src = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(a.fbases) +
+                                                   slot % a.G)) +
+              (int64_t)(slot / a.G) * a.pitch;
       if (MODE == 2) {
         const int row16 = a.pitch >> 2;
         const int4* s4 = reinterpret_cast<const int4*>(src);
@@ -193,6 +203,8 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
   a.last_tiles = ws->tile_state + ws->tile_off[L - 1];
   a.last_ntiles = ws->tile_off[L] - ws->tile_off[L - 1];
   a.fcache = ctx->d_fcache;
+  a.fbases = ctx->d_fbases;
+  a.G = ctx->fpart_world;
   a.hfeats = ctx->u_feats;
   a.pitch = ctx->pitch;
   a.D = ctx->D;

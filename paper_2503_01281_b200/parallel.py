@@ -99,3 +99,19 @@ def barrier(device_index=None):
             dist.barrier(device_ids=[device_index])
         else:
             dist.barrier()
+
+
+def exchange_feature_partitions(ctx, group=None):
+    """NEXT F1: after dci_fill_partitioned(world, rank) on every rank, all-gather the 64-byte
+    CUDA IPC handles of the feature partitions and attach the peers' rows (NVLink P2P)."""
+    import torch.distributed as dist
+    import paper_2503_01281_b200 as dci
+    mine = dci.feature_partition_handle(ctx)
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    handles = [None] * world
+    if world > 1:
+        dist.all_gather_object(handles, mine, group=group)
+    else:
+        handles = [mine]
+    dci.attach_feature_partitions(ctx, handles)
+    return handles
