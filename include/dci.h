@@ -193,6 +193,8 @@ dci_status dci_fill(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edg
  *    dci_attach_feature_partitions (all ranks' handles, rank-major) before sampling; hits on
  *    other partitions are then peer loads over NVLink (P2P through CUDA IPC mappings).
  *  rank == -1: all partitions live on this device (single-device emulation / testing).
+ * A re-fill frees this rank's partition and closes the peers' mappings: exchange and attach
+ * again (on every rank, after all ranks have filled) before the next batch.
  * Synchronises `stream`.  Errors: DCI_EINVAL (world not in 1..16, rank out of range).
  * ------------------------------------------------------------------------------------ */
 #define DCI_IPC_HANDLE_BYTES 64

@@ -430,6 +430,25 @@ void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t 
   ++ctx->launches;
 }
 
+// Device temporaries of one fill: freed on every exit path.
+struct TempAllocs {
+  std::vector<void*> ptrs;
+  template <class T>
+  cudaError_t alloc(T** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+  void forget(const void* p) {  // ownership moved elsewhere
+    for (auto& q : ptrs)
+      if (q == p) q = nullptr;
+  }
+  ~TempAllocs() {
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+  }
+};
+
 void release_feature_partitions(dci_ctx* ctx) {
   for (int p = 0; p < dci_ctx::kMaxParts; ++p) {
     if (ctx->ipc_opened[p]) cudaIpcCloseMemHandle(ctx->ipc_opened[p]);
@@ -452,13 +471,34 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
   int64_t *d_indptr = nullptr, *d_total = nullptr, *d_sum = nullptr;
   int32_t *d_idx = nullptr, *d_idxR = nullptr, *d_scal = nullptr;
   RSState* d_st = nullptr;
-  DCI_CUDA(cudaMalloc(&d_indptr, sizeof(int64_t) * (N + 1)));
-  DCI_CUDA(cudaMalloc(&d_total, sizeof(int64_t) * std::max<int64_t>(N, 1)));
-  DCI_CUDA(cudaMalloc(&d_sum, sizeof(int64_t)));
-  DCI_CUDA(cudaMalloc(&d_idx, sizeof(int32_t) * std::max<int64_t>(E, 1)));
-  DCI_CUDA(cudaMalloc(&d_idxR, sizeof(int32_t) * std::max<int64_t>(E, 1)));
-  DCI_CUDA(cudaMalloc(&d_scal, sizeof(int32_t) * 4));
-  DCI_CUDA(cudaMalloc(&d_st, sizeof(RSState)));
+  TempAllocs tmp;
+  // If the fill stops part-way, leave a consistent "no cache" state behind.
+  struct Rollback {
+    dci_ctx* ctx;
+    cudaStream_t s;
+    bool armed = false, committed = false;
+    ~Rollback() {
+      if (!armed || committed) return;
+      cudaStreamSynchronize(s);
+      if (ctx->d_acache) cudaFree(ctx->d_acache);
+      if (ctx->d_fcache) cudaFree(ctx->d_fcache);
+      release_feature_partitions(ctx);
+      ctx->d_acache = nullptr;
+      ctx->d_fcache = nullptr;
+      ctx->acache_len = ctx->fcache_rows = ctx->fcache_total_rows = 0;
+      ctx->fpart_world = 1;
+      ctx->fpart_rank = 0;
+      k_dir_reset_caches<<<grid_for(ctx, 4), 256, 0, s>>>(ctx->d_dir, ctx->N);
+      cudaStreamSynchronize(s);
+    }
+  } rollback{ctx, s};
+  DCI_CUDA(tmp.alloc(&d_indptr, sizeof(int64_t) * (N + 1)));
+  DCI_CUDA(tmp.alloc(&d_total, sizeof(int64_t) * std::max<int64_t>(N, 1)));
+  DCI_CUDA(tmp.alloc(&d_sum, sizeof(int64_t)));
+  DCI_CUDA(tmp.alloc(&d_idx, sizeof(int32_t) * std::max<int64_t>(E, 1)));
+  DCI_CUDA(tmp.alloc(&d_idxR, sizeof(int32_t) * std::max<int64_t>(E, 1)));
+  DCI_CUDA(tmp.alloc(&d_scal, sizeof(int32_t) * 4));
+  DCI_CUDA(tmp.alloc(&d_st, sizeof(RSState)));
   DCI_CUDA(cudaMemcpyAsync(d_indptr, ctx->h_indptr, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
   if (E) DCI_CUDA(cudaMemcpyAsync(d_idx, ctx->h_idx_orig, sizeof(int32_t) * E, cudaMemcpyHostToDevice, s));
   DCI_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(int32_t) * 4, s));
@@ -486,8 +526,8 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
   l2.range_err = d_scal + 1;
   if (npass > 1) {
     for (int i = 0; i < 2; ++i) {
-      DCI_CUDA(cudaMalloc(&l2.tmp_idx[i], sizeof(int32_t) * E));
-      DCI_CUDA(cudaMalloc(&l2.tmp_key[i], sizeof(uint32_t) * E));
+      DCI_CUDA(tmp.alloc(&l2.tmp_idx[i], sizeof(int32_t) * E));
+      DCI_CUDA(tmp.alloc(&l2.tmp_key[i], sizeof(uint32_t) * E));
     }
   }
   k_level2<<<grid_for(ctx, 8), 32 * kL2Warps, 0, s>>>(l2);
@@ -495,10 +535,6 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
   DCI_CUDA(cudaGetLastError());
   DCI_CUDA(cudaMemcpyAsync(h_scal, d_scal, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, s));
   DCI_CUDA(cudaStreamSynchronize(s));
-  for (int i = 0; i < 2; ++i) {
-    if (l2.tmp_idx[i]) cudaFree(l2.tmp_idx[i]);
-    if (l2.tmp_key[i]) cudaFree(l2.tmp_key[i]);
-  }
   if (h_scal[1]) return fail(DCI_ERANGE, "dci_fill: a node's total access count is >= 2^32");
 
   // reordered host CSC (pinned + mapped), separate from the original so refills restart
@@ -516,6 +552,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
 
   // ---- drop old caches, reset the directory's cache fields ----
   DCI_CUDA(cudaStreamSynchronize(s));
+  rollback.armed = true;
   if (ctx->d_acache) cudaFree(ctx->d_acache);
   if (ctx->d_fcache) cudaFree(ctx->d_fcache);
   release_feature_partitions(ctx);
@@ -543,6 +580,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     if (r != DCI_OK) return r;
     if (whole_fit) {
       ctx->d_acache = d_idxR;  // the whole reordered CSC, cache_off == indptr
+      tmp.forget(d_idxR);
       d_idxR = nullptr;
     } else {
       DCI_CUDA(cudaMalloc(&ctx->d_acache, sizeof(int32_t) * cap_e));
@@ -562,7 +600,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
       stp = d_st;
     }
     int64_t* d_list = nullptr;
-    DCI_CUDA(cudaMalloc(&d_list, sizeof(int64_t) * cap_rows));
+    DCI_CUDA(tmp.alloc(&d_list, sizeof(int64_t) * cap_rows));
     FeatSlotOp op{fk, stp, ctx->d_dir, d_list};
     dci_status r = scan_nodes(ctx, op, N, d_sum, s);
     if (r != DCI_OK) return r;
@@ -578,7 +616,6 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     }
     ++ctx->launches;
     DCI_CUDA(cudaStreamSynchronize(s));
-    cudaFree(d_list);
     ctx->fcache_rows = local_rows;
     ctx->fcache_total_rows = cap_rows;
   }
@@ -598,13 +635,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
                            cudaMemcpyHostToDevice, s));
   DCI_CUDA(cudaGetLastError());
   DCI_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_indptr);
-  cudaFree(d_total);
-  cudaFree(d_sum);
-  cudaFree(d_idx);
-  if (d_idxR) cudaFree(d_idxR);
-  cudaFree(d_scal);
-  cudaFree(d_st);
+  rollback.committed = true;
   ctx->whole_fit = whole_fit ? 1 : 0;
   ctx->c_adj = c_adj;
   ctx->c_feat = c_feat;

@@ -32,6 +32,26 @@ __device__ __forceinline__ int32_t ld_host_i32(const int32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ int32_t ld_keep_i32(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ int4 ld_keep_v4(const int4* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 struct SampleArgs {
   const DirEntry* dir;
   const int32_t* acache;
@@ -109,6 +129,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
   const int64_t warp_id = tid >> 5;
   const int64_t nwarps = nthreads >> 5;
   uint32_t hits = 0, misses = 0;
+  const uint64_t keep = policy_evict_last();
   for (int64_t dbase = warp_id * GPW; dbase < n_h; dbase += nwarps * GPW) {
     const int64_t d = dbase + lane / G;
     const bool active = d < n_h;
@@ -118,8 +139,8 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
       v = F_in[d];
       if (v >= 0 && (int64_t)v < a.N) {
         const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
-        e0 = __ldg(ep);
-        e1 = __ldg(ep + 1);
+        e0 = ld_keep_v4(ep, keep);
+        e1 = ld_keep_v4(ep + 1, keep);
       }
     }
     const int64_t host_off = ((int64_t)(uint32_t)e0.y << 32) | (uint32_t)e0.x;
@@ -160,7 +181,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
     int32_t x = -1;
     if (valid) {
       if (rank < cached_len) {
-        x = __ldg(a.acache + cache_off + rank);
+        x = ld_keep_i32(a.acache + cache_off + rank, keep);
         ++hits;
       } else {
         x = ld_host_i32(a.uidx + host_off + rank);
