@@ -219,3 +219,50 @@ def test_mean_aggregate_parity(D, ldx):
     Hg = H[: len(o.bptr[L - 1]) - 1, :D].cpu().numpy().astype(np.float64)
     assert np.all(np.abs(Hg - Hr) <= _agg_tol(o.bptr[L - 1], o.X, Hr))
     assert np.all(Hg[np.diff(o.bptr[L - 1]) == 0] == 0)
+
+
+def test_abi_error_paths(small):
+    """DCI_ESTATE / DCI_ECAP / DCI_EINVAL are returned (and raised by the binding) without
+    corrupting the context: a valid batch afterwards still matches the oracle."""
+    ip, ix, ft, ctx0 = small
+    ctx = dci.load_graph(ip, ix, ft)
+    fan = (4, 4)
+    ws = dci.workspace_create(ctx, 64, fan)
+    seeds = synth.inference_batches(ip, 64)[0]
+    sd = torch.from_numpy(seeds).to(DEV)
+    # output smaller than dci_output_bounds -> ECAP
+    small_out = dci.BatchOut(ctx, 8, fan)
+    with pytest.raises(dci.DciError) as e:
+        dci.sample_gather(ctx, ws, sd, fan, 1, small_out)
+    assert e.value.code in (dci.ECAP, dci.EINVAL)
+    # fan-out above the workspace's maximum / above 32 / wrong L
+    out = dci.BatchOut(ctx, 64, fan)
+    with pytest.raises(dci.DciError) as e:
+        dci.sample_gather(ctx, ws, sd, (5, 4), 1, out)
+    assert e.value.code == dci.EINVAL
+    with pytest.raises(dci.DciError) as e:
+        dci.workspace_create(ctx, 64, (33,))
+    assert e.value.code == dci.EINVAL
+    with pytest.raises(dci.DciError) as e:
+        dci.sample_gather(ctx, ws, sd, (4,), 1, out)
+    assert e.value.code == dci.EINVAL
+    # workspace of another context
+    other = dci.load_graph(ip, ix, ft)
+    with pytest.raises(dci.DciError) as e:
+        dci.sample_gather(other, ws, sd, fan, 1, out)
+    assert e.value.code == dci.EINVAL
+    # presample after fill -> ESTATE
+    nv = torch.zeros(ctx.N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(ctx.E, dtype=torch.int32, device=DEV)
+    dci.fill(ctx, nv, ec, 0, 0)
+    with pytest.raises(dci.DciError) as e:
+        dci.presample(ctx, sd, 64, fan, 3, nv, ec)
+    assert e.value.code == dci.ESTATE
+    # partition arguments
+    with pytest.raises(dci.DciError) as e:
+        dci.fill_partitioned(ctx, nv, ec, 0, 0, 17, 0)
+    assert e.value.code == dci.EINVAL
+    # still consistent (fill with C = 0: reordered CSC, no caches)
+    R, cl, co, ac = oracle.adj_fill(ip, ix, np.zeros(len(ix), np.int32), 0)
+    g = _run(ctx, ws, seeds, fan, 2)
+    _assert_batch_equal(g, oracle.sample_gather(ip, R, ft, seeds, fan, 2, cl, np.full(len(ip) - 1, -1, np.int32)), 2)
