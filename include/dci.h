@@ -29,7 +29,7 @@ extern "C" {
 
 #define DCI_VERSION 100          /* 1.0.0 */
 #define DCI_MAX_LAYERS 8         /* L <= 8 hops */
-#define DCI_MAX_FANOUT 32        /* per-hop fan-out 1..32 (warp-register selection) */
+#define DCI_MAX_FANOUT 1024      /* per-hop fan-out 1..1024 (<= 32: registers, else shared memory) */
 
 typedef enum dci_status {
   DCI_OK = 0,
@@ -122,7 +122,7 @@ dci_status dci_workspace_destroy(dci_workspace* ws);
  * inference), P:170 (hit -> GPU memory, miss -> host memory through UVA)
  * (adjacency prefix-hit rule), P:200 (feature cache lookup).
  *  seeds  device int32[B] (unique ids in [0, N)); B >= 0, B <= the workspace's max_batch.
- *  fanouts host int32[L] (DGL order, each 1..32, each <= the workspace's max_fanouts).
+ *  fanouts host int32[L] (DGL order, each 1..1024, each <= the workspace's max_fanouts).
  *  seed   64-bit sampling seed; draws are Philox(ctr=(node, slot, hop, pass=0),
  *         key=seed) (O-2), so results do not depend on batch composition or GPU count.
  * Asynchronous on `stream`; enqueues only device work (no host sync, no allocation).

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdci.so")
 MAX_LAYERS = 8
-MAX_FANOUT = 32
+MAX_FANOUT = 1024
 
 STATUS = {0: "DCI_OK", 1: "DCI_EINVAL", 2: "DCI_ESTATE", 3: "DCI_ECUDA", 4: "DCI_ENOMEM", 5: "DCI_ESEED",
           6: "DCI_EDUP", 7: "DCI_ECAP", 8: "DCI_ERANGE"}

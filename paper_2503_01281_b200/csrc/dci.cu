@@ -89,7 +89,7 @@ void frontier_bounds(int64_t N, int64_t B, const int32_t* fan, int32_t L, int64_
 dci_status check_fanouts(const int32_t* fanouts, int32_t L) {
   if (!fanouts || L < 1 || L > DCI_MAX_LAYERS) return fail(DCI_EINVAL, "L must be in [1, DCI_MAX_LAYERS]");
   for (int i = 0; i < L; ++i)
-    if (fanouts[i] < 1 || fanouts[i] > DCI_MAX_FANOUT) return fail(DCI_EINVAL, "fan-out must be in [1, 32]");
+    if (fanouts[i] < 1 || fanouts[i] > DCI_MAX_FANOUT) return fail(DCI_EINVAL, "fan-out must be in [1, 1024]");
   return DCI_OK;
 }
 
@@ -398,7 +398,8 @@ dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanou
   if (st != DCI_OK) return st;
   int64_t caps[DCI_MAX_LAYERS + 1];
   frontier_bounds(ctx->N, B, fanouts, L, caps);
-  if (caps[L] * 32 >= (1ll << 31)) return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
+  for (int h = 0; h < L; ++h)
+    if (caps[h] * fanouts[L - 1 - h] >= (1ll << 31)) return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
   for (int h = 0; h <= L; ++h)
     if (frontier_caps) frontier_caps[h] = caps[h];
   for (int h = 0; h < L; ++h)
@@ -423,10 +424,11 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   frontier_bounds(ctx->N, max_batch, max_fanouts, L, w->hop_cap);
   int64_t max_front = 0;
   for (int h = 0; h <= L; ++h) max_front = std::max(max_front, w->hop_cap[h]);
-  if (max_front * 32 >= (1ll << 31)) {
-    delete w;
-    return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
-  }
+  for (int h = 0; h < L; ++h)
+    if (w->hop_cap[h] * max_fanouts[L - 1 - h] >= (1ll << 31)) {
+      delete w;
+      return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
+    }
   w->cand_cap = 0;
   w->tiles_cap = 0;
   for (int h = 0; h < L; ++h) {

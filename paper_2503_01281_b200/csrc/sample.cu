@@ -64,6 +64,39 @@ struct SampleArgs {
   HopParams p;
 };
 
+// Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
+// (position = seed index); hop h >= 1 relabels hop h-1's candidates into its block CSR
+// (tag -> final local id) and clears hop h-1's scan tile state.
+__device__ __forceinline__ void hop_prologue(const SampleArgs& a, int64_t tid, int64_t nthreads, int64_t B,
+                                             unsigned long long ehi, const int32_t* F_in) {
+  const HopParams& p = a.p;
+  BatchScalars* sc = a.sc;
+  const int h = p.hop;
+  if (h == 0) {
+    for (int64_t d = tid; d < B; d += nthreads) {
+      const int32_t s = F_in[d];
+      p.F[d] = s;
+      if (s < 0 || (int64_t)s >= a.N)
+        atomicCAS(&sc->status, 0, (int32_t)DCI_ESEED);
+      else
+        atomicMax(a.pos_of + s, ehi | (0xFFFFFFFFu - (uint32_t)d));
+    }
+  } else {
+    // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
+    const int pf = p.prev_f;
+    const int64_t n_prev = (h == 1) ? B : sc->sizes[h - 1];
+    const int64_t nq = n_prev * pf;
+    for (int64_t q = tid; q < nq; q += nthreads) {
+      const int64_t d = q / pf;
+      const int s = (int)(q - d * pf);
+      if (s < p.prev_kcnt[d])
+        p.prev_bsrc[p.prev_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + p.prev_cand[q]));
+    }
+    for (int64_t t = tid; t < a.prev_ntiles; t += nthreads) a.prev_tiles[t] = 0ull;
+    if (tid == 0) sc->tickets[h - 1] = 0;
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // k_sample_hop<G>: one group of G lanes (G = next pow2 >= f) per dst node of F_h.
 //  1. one broadcast 32 B directory load (host_off, cache_off, deg, cached_len)
@@ -101,29 +134,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
 
   const int64_t n_h = (h == 0) ? B : sc->sizes[h];
 
-  if (h == 0) {
-    for (int64_t d = tid; d < B; d += nthreads) {
-      const int32_t s = F_in[d];
-      p.F[d] = s;
-      if (s < 0 || (int64_t)s >= a.N)
-        atomicCAS(&sc->status, 0, (int32_t)DCI_ESEED);
-      else
-        atomicMax(a.pos_of + s, ehi | (0xFFFFFFFFu - (uint32_t)d));
-    }
-  } else {
-    // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
-    const int pf = p.prev_f;
-    const int64_t n_prev = (h == 1) ? B : sc->sizes[h - 1];
-    const int64_t nq = n_prev * pf;
-    for (int64_t q = tid; q < nq; q += nthreads) {
-      const int64_t d = q / pf;
-      const int s = (int)(q - d * pf);
-      if (s < p.prev_kcnt[d])
-        p.prev_bsrc[p.prev_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + p.prev_cand[q]));
-    }
-    for (int64_t t = tid; t < a.prev_ntiles; t += nthreads) a.prev_tiles[t] = 0ull;
-    if (tid == 0) sc->tickets[h - 1] = 0;
-  }
+  hop_prologue(a, tid, nthreads, B, ehi, F_in);
 
   const int GPW = 32 / G;
   const int64_t warp_id = tid >> 5;
@@ -204,6 +215,119 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
   }
 }
 
+
+// ------------------------------------------------------------------------------------
+// k_sample_hop_wide: fan-outs 33..1024, one warp per dst, chosen ranks in shared memory.
+// Floyd is resolved chunk by chunk: a lane's draw is first checked against every rank fixed by
+// earlier chunks (parallel scan of shared memory), then the chunk's 32 slots are resolved in
+// order with shuffles/ballots exactly as in k_sample_hop.  Ranks are then sorted ascending by
+// a bitonic network in shared memory (padded to a power of two with INT_MAX).
+// ------------------------------------------------------------------------------------
+constexpr int kWideWarps = 4;
+
+__global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(SampleArgs a) {
+  extern __shared__ int32_t s_wide[];
+  const HopParams& p = a.p;
+  BatchScalars* sc = a.sc;
+  const int h = p.hop;
+  const int f = p.f;
+  int fp2 = 1;
+  while (fp2 < f) fp2 <<= 1;
+  int32_t* chosen = s_wide + (threadIdx.x >> 5) * fp2;
+  const int lane = threadIdx.x & 31;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t B = sc->hdr.B;
+  const unsigned long long seed = sc->hdr.seed;
+  const unsigned long long ehi = (unsigned long long)sc->hdr.epoch << 32;
+  const int32_t* F_in = (h == 0) ? sc->hdr.seeds : p.F;
+  const int64_t n_h = (h == 0) ? B : sc->sizes[h];
+  hop_prologue(a, tid, nthreads, B, ehi, F_in);
+  const uint64_t keep = policy_evict_last();
+  uint32_t hits = 0, misses = 0;
+  for (int64_t d = tid >> 5; d < n_h; d += nthreads >> 5) {
+    const int32_t v = F_in[d];
+    int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
+    if (v >= 0 && (int64_t)v < a.N) {
+      const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
+      e0 = ld_keep_v4(ep, keep);
+      e1 = ld_keep_v4(ep + 1, keep);
+    }
+    const int64_t host_off = ((int64_t)(uint32_t)e0.y << 32) | (uint32_t)e0.x;
+    const int64_t cache_off = ((int64_t)(uint32_t)e0.w << 32) | (uint32_t)e0.z;
+    const int32_t deg = e1.x;
+    const int32_t cached_len = e1.y;
+    const int k = deg < f ? deg : f;
+    if (deg > f) {
+      for (int c0 = 0; c0 < f; c0 += 32) {
+        const int i = c0 + lane;
+        const bool in = i < f;
+        int32_t t = 0, j = 0;
+        bool coll_prev = false;
+        if (in) {
+          j = deg - f + i;
+          const uint64_t u = philox_u64(seed, p.pass, (uint32_t)h, (uint32_t)v, (uint32_t)i);
+          t = (int32_t)__umul64hi(u, (uint64_t)(j + 1));
+          for (int m = 0; m < c0; ++m) coll_prev |= chosen[m] == t;
+        }
+        int32_t res = 0;
+        for (int i2 = 0; i2 < 32; ++i2) {
+          const int32_t ti = __shfl_sync(0xffffffffu, t, i2);
+          const bool coll = __ballot_sync(0xffffffffu, lane < i2 && res == ti) != 0;
+          if (lane == i2) res = (coll_prev || coll) ? j : t;
+        }
+        if (in) chosen[i] = res;
+        __syncwarp();
+      }
+      for (int i = f + lane; i < fp2; i += 32) chosen[i] = 0x7FFFFFFF;
+      __syncwarp();
+      // bitonic sort of chosen[0..fp2) ascending
+      for (int kk = 2; kk <= fp2; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int i = lane; i < fp2; i += 32) {
+            const int ixj = i ^ jj;
+            if (ixj > i) {
+              const int32_t x = chosen[i], y = chosen[ixj];
+              const bool up = (i & kk) == 0;
+              if ((x > y) == up) {
+                chosen[i] = y;
+                chosen[ixj] = x;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    // element reads in sorted-rank order: pos -> rank
+    for (int pos = lane; pos < f; pos += 32) {
+      int32_t x = -1;
+      if (pos < k) {
+        const int32_t rank = deg > f ? chosen[pos] : pos;
+        if (rank < cached_len) {
+          x = ld_keep_i32(a.acache + cache_off + rank, keep);
+          ++hits;
+        } else {
+          x = ld_host_i32(a.uidx + host_off + rank);
+          ++misses;
+        }
+        const unsigned long long tag = ehi | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
+        if (__ldcg(a.pos_of + x) < tag) atomicMax(a.pos_of + x, tag);
+        if (p.edge_counts) atomicAdd(p.edge_counts + host_off + rank, 1);
+      }
+      p.cand[d * f + pos] = x;
+    }
+    if (lane == 0) p.kcnt[d] = k;
+    __syncwarp();
+  }
+  hits = __reduce_add_sync(0xffffffffu, hits);
+  misses = __reduce_add_sync(0xffffffffu, misses);
+  if (lane == 0 && (hits | misses)) {
+    atomicAdd(&sc->counters[0], (unsigned long long)hits);
+    atomicAdd(&sc->counters[1], (unsigned long long)misses);
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // k_scan_hop: one thread per dst of F_h, kScanTile dsts per tile, tiles taken by dynamic
 // tickets (in-order => deadlock-free look-back).  Per dst: k (samples) and the bitmask of
@@ -252,12 +376,13 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
     const int64_t tile = s_ticket;
     if (tile >= ntiles) break;
     const int64_t d = tile * kScanTile + threadIdx.x;
-    uint32_t k = 0, newmask = 0;
+    uint32_t k = 0, newmask = 0, nwide = 0;
     if (d < n_h) {
       k = (uint32_t)p.kcnt[d];
       const int32_t* c = p.cand + d * f;
       const uint32_t base = (uint32_t)(n_h + d * f);
-      // which of my candidates own their node's first occurrence (8 loads in flight)
+      // which of my candidates own their node's first occurrence (8 loads in flight); a
+      // 32-bit mask for f <= 32, else counted here and re-checked when appending
       for (uint32_t s0 = 0; s0 < k; s0 += 8) {
         int32_t x[8];
 #pragma unroll
@@ -267,7 +392,12 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
         for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? __ldcg(a.pos_of + x[u]) : 0ull;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) newmask |= 1u << (s0 + u);
+          if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) {
+            if (f <= 32)
+              newmask |= 1u << (s0 + u);
+            else
+              ++nwide;
+          }
       }
       if (h == 0) {
         const int32_t sd = p.F[d];
@@ -275,7 +405,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
           atomicCAS(&sc->status, 0, (int32_t)DCI_EDUP);
       }
     }
-    const uint32_t nn = __popc(newmask);
+    const uint32_t nn = f <= 32 ? __popc(newmask) : nwide;
     // block exclusive scan of packed (k << 31 | nn)
     const unsigned long long mine = ((unsigned long long)k << 31) | nn;
     unsigned long long incl = mine;
@@ -338,12 +468,25 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
       p.bptr[d] = (int32_t)(pre >> 31);
       uint32_t nid = (uint32_t)(n_h + (int64_t)(pre & ((1ull << 31) - 1)));
       const int32_t* c = p.cand + d * f;
-      for (uint32_t m = newmask; m; m &= m - 1) {
-        const int s = __ffs(m) - 1;
-        const int32_t x = c[s];
-        p.F[nid] = x;
-        a.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
-        ++nid;
+      if (f <= 32) {
+        for (uint32_t m = newmask; m; m &= m - 1) {
+          const int s = __ffs(m) - 1;
+          const int32_t x = c[s];
+          p.F[nid] = x;
+          a.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+          ++nid;
+        }
+      } else if (nwide) {
+        // only this candidate's owner rewrites its tag, so the check is stable (see above)
+        const uint32_t base = (uint32_t)(n_h + d * f);
+        for (uint32_t s = 0; s < k; ++s) {
+          const int32_t x = c[s];
+          if (x >= 0 && __ldcg(a.pos_of + x) == (ehi | (0xFFFFFFFFu - (base + s)))) {
+            p.F[nid] = x;
+            a.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+            ++nid;
+          }
+        }
       }
     }
     __syncthreads();  // s_ticket / s_prefix reuse
@@ -364,7 +507,12 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cuda
   }();
   // sub-warp group width: next power of two >= f
   auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };
-  if (p.f <= 1)
+  if (p.f > 32) {
+    int fp2 = 1;
+    while (fp2 < p.f) fp2 <<= 1;
+    const size_t smem = (size_t)kWideWarps * fp2 * sizeof(int32_t);
+    k_sample_hop_wide<<<persistent_grid(ctx, k_sample_hop_wide, 32 * kWideWarps, 16), 32 * kWideWarps, smem, s>>>(a);
+  } else if (p.f <= 1)
     go(k_sample_hop<1>);
   else if (p.f <= 2)
     go(k_sample_hop<2>);

@@ -241,7 +241,7 @@ def test_abi_error_paths(small):
         dci.sample_gather(ctx, ws, sd, (5, 4), 1, out)
     assert e.value.code == dci.EINVAL
     with pytest.raises(dci.DciError) as e:
-        dci.workspace_create(ctx, 64, (33,))
+        dci.workspace_create(ctx, 64, (1025,))
     assert e.value.code == dci.EINVAL
     with pytest.raises(dci.DciError) as e:
         dci.sample_gather(ctx, ws, sd, (4,), 1, out)
@@ -266,3 +266,35 @@ def test_abi_error_paths(small):
     R, cl, co, ac = oracle.adj_fill(ip, ix, np.zeros(len(ix), np.int32), 0)
     g = _run(ctx, ws, seeds, fan, 2)
     _assert_batch_equal(g, oracle.sample_gather(ip, R, ft, seeds, fan, 2, cl, np.full(len(ip) - 1, -1, np.int32)), 2)
+
+
+@pytest.mark.parametrize("fan", [(40,), (100, 7), (33, 64), (1024,), (2, 300)])
+def test_wide_fanout_parity(fan):
+    """Fan-outs 33..1024 (shared-memory Floyd + bitonic sort) on a graph with hubs of degree
+    far above and nodes far below the fan-out; presample counts and a filled cache too."""
+    rng = np.random.default_rng(len(fan) * 1000 + fan[-1])
+    N = 3000
+    deg = rng.integers(0, 20, N)
+    deg[rng.choice(N, 40, replace=False)] = rng.integers(1100, 5000, 40)
+    ip = np.zeros(N + 1, np.int64)
+    ip[1:] = np.cumsum(deg)
+    ix = rng.integers(0, N, int(ip[-1])).astype(np.int32)
+    ft = synth.features(N, 12).numpy()
+    ctx = dci.load_graph(ip, ix, ft)
+    B = 48
+    pre = rng.permutation(np.nonzero(deg)[0])[:3 * B].astype(np.int32)
+    nv = torch.zeros(N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(len(ix), dtype=torch.int32, device=DEV)
+    dci.presample(ctx, torch.from_numpy(pre).to(DEV), B, fan, 3, nv, ec)
+    nv_o, ec_o = oracle.presample(ip, ix, pre, B, fan, 3)
+    assert np.array_equal(nv.cpu().numpy(), nv_o) and np.array_equal(ec.cpu().numpy(), ec_o)
+    c_adj, c_feat = 4 * len(ix) // 3, 64 * 4 * 300
+    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    R, cl, co, ac = oracle.adj_fill(ip, ix, ec_o, c_adj)
+    slot_o, _ = oracle.feat_fill(nv_o, c_feat // (4 * 12))
+    ws = dci.workspace_create(ctx, B, fan)
+    hubs = np.nonzero(deg > 1000)[0].astype(np.int32)
+    for seeds in [hubs[:B], rng.choice(N, B, replace=False).astype(np.int32)]:
+        g = _run(ctx, ws, seeds, fan, 21)
+        o = oracle.sample_gather(ip, R, ft, seeds, fan, 21, cl, slot_o)
+        _assert_batch_equal(g, o, len(fan))
