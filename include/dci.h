@@ -269,6 +269,13 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
 dci_status dci_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
                               const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, void* stream);
 
+/* The same with the aggregator of Table III: DCI_AGG_MEAN ("avg", GCN) as above, or
+ * DCI_AGG_SUM (GraphSAGE's "sum": H[d] = sum_j Xsrc[bsrc[j]], no 1/k_d). */
+enum { DCI_AGG_MEAN = 0, DCI_AGG_SUM = 1 };
+dci_status dci_block_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                               const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, int32_t op,
+                               void* stream);
+
 /* Kernels launched by this context so far (all workspaces). */
 uint64_t dci_launch_count(const dci_ctx* ctx);
 

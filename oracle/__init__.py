@@ -72,8 +72,9 @@ def lib():
                                       _i32p]
         L.oracle_adj_fill.restype = C.c_int64
         _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
-        L.oracle_mean_aggregate.argtypes = [_i32p, _i32p, C.c_int64, _f32p, C.c_int64, C.c_int32, _f64p]
-        L.oracle_mean_aggregate.restype = None
+        L.oracle_block_aggregate.argtypes = [_i32p, _i32p, C.c_int64, _f32p, C.c_int64, C.c_int32, C.c_int32,
+                                             _f64p]
+        L.oracle_block_aggregate.restype = None
         L.oracle_sample_gather.argtypes = [C.c_int64, _i64p, _i32p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                            _i32p, C.c_int32, _i32p, C.c_int32, C.c_uint64, _i32p, C.c_int64, _i64p,
                                            pp, pp, _i64p, C.c_void_p, C.c_int64, _u64p]
@@ -284,8 +285,9 @@ def adj_fill(indptr, indices, edge_counts, c_adj_bytes: int):
     return R[:E], cl[:N], co[:N], ac[:n]
 
 
-def mean_aggregate(bptr, bsrc, X):
-    """O-13 GraphSAGE mean over a block: H[d] = mean of X[bsrc[bptr[d]:bptr[d+1]]] (fp64)."""
+def mean_aggregate(bptr, bsrc, X, op: str = "mean"):
+    """O-13 aggregation over a block (fp64): H[d] = mean (op="mean") or sum (op="sum") of
+    X[bsrc[bptr[d]:bptr[d+1]]]."""
     bptr = np.ascontiguousarray(bptr, np.int32)
     bsrc = np.ascontiguousarray(bsrc, np.int32)
     X = np.ascontiguousarray(X, np.float32)
@@ -294,5 +296,5 @@ def mean_aggregate(bptr, bsrc, X):
     H = np.zeros((max(n, 1), D), np.float64)
     if len(bsrc) == 0:
         bsrc = np.zeros(1, np.int32)
-    lib().oracle_mean_aggregate(bptr, bsrc, n, X, D, D, H)
+    lib().oracle_block_aggregate(bptr, bsrc, n, X, D, D, {"mean": 0, "sum": 1}[op], H)
     return H[:n]

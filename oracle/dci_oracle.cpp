@@ -355,18 +355,22 @@ int64_t oracle_adj_fill(int64_t N, int64_t E, const int64_t* indptr, const int32
     return off;
 }
 
-// O-13 GraphSAGE mean aggregator over one sampled block (P:107
+// O-13 mean / sum aggregator over one sampled block (P:107
 // "aggregating" the neighbours' features; BJ north_star's optional consumer; reading C23):
 // H[d][c] = (1 / k_d) * sum_{j = bptr[d]}^{bptr[d+1]-1} X[bsrc[j]][c], accumulated in double;
 // k_d = 0 -> H[d] = 0.
-void oracle_mean_aggregate(const int32_t* bptr, const int32_t* bsrc, int64_t n_dst, const float* X,
-                           int64_t ldx, int32_t D, double* H) {
+// op = 0: mean ("avg", GCN in Table III); op = 1: sum (GraphSAGE's "sum" there).
+void oracle_block_aggregate(const int32_t* bptr, const int32_t* bsrc, int64_t n_dst, const float* X,
+                            int64_t ldx, int32_t D, int32_t op, double* H) {
     for (int64_t d = 0; d < n_dst; ++d) {
         int64_t k = bptr[d + 1] - bptr[d];
         for (int32_t c = 0; c < D; ++c) {
             double acc = 0.0;
             for (int64_t j = bptr[d]; j < bptr[d + 1]; ++j) acc += (double)X[(int64_t)bsrc[j] * ldx + c];
-            H[d * D + c] = k > 0 ? acc / (double)k : 0.0;
+            if (op == 1)
+                H[d * D + c] = acc;
+            else
+                H[d * D + c] = k > 0 ? acc / (double)k : 0.0;
         }
     }
 }

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -29,7 +30,7 @@ OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
             "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
             "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
-            "dci_workspace_stats", "dci_mean_aggregate", "dci_fill_partitioned", "dci_feature_partition_handle",
+            "dci_workspace_stats", "dci_mean_aggregate", "dci_block_aggregate", "dci_fill_partitioned", "dci_feature_partition_handle",
             "dci_attach_feature_partitions", "dci_launch_count", "dci_last_error", "dci_version"]
 IPC_HANDLE_BYTES = 64
 
@@ -92,6 +93,7 @@ def lib():
         "dci_workspace_stage_ms": [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)],
         "dci_workspace_stats": [vp, C.POINTER(dci_ws_stats), i32],
         "dci_mean_aggregate": [vp, vp, vp, vp, vp, i64, i32, vp, i64, vp],
+        "dci_block_aggregate": [vp, vp, vp, vp, vp, i64, i32, vp, i64, i32, vp],
         "dci_launch_count": [vp],
         "dci_last_error": [],
         "dci_version": [],
@@ -131,9 +133,14 @@ class Context:
 
     def __init__(self, handle, N, E, D, device):
         self.handle, self.N, self.E, self.D, self.device = handle, N, E, D, device
+        self._workspaces = weakref.WeakSet()
 
     def close(self):
+        """Destroy the context (its live workspaces first: finalizers of garbage cycles run
+        in arbitrary order, so a workspace may still exist when the context goes)."""
         if self.handle:
+            for ws in list(self._workspaces):
+                ws.close()
             lib().dci_destroy(self.handle)
             self.handle = None
 
@@ -190,6 +197,7 @@ class Workspace:
         _check(lib().dci_workspace_create(ctx.handle, max_batch, _np_ptr(fan), len(fan), C.byref(h)),
                "dci_workspace_create")
         self.handle, self.ctx, self.max_batch, self.fanouts = h, ctx, max_batch, tuple(int(f) for f in fan)
+        ctx._workspaces.add(self)
 
     def close(self):
         if self.handle:
@@ -295,9 +303,10 @@ def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: i
                                         _stream_ptr(stream)), "dci_sample_gather_host")
 
 
-def mean_aggregate(ctx: Context, out: BatchOut, hop: int | None = None, H=None, stream=None):
-    """dci_mean_aggregate (NEXT F2): GraphSAGE mean over block `hop` (default the input
-    layer L-1, whose sources are the rows of out.X).  Returns H [hop_cap, D] (device)."""
+def mean_aggregate(ctx: Context, out: BatchOut, hop: int | None = None, H=None, stream=None, op: str = "mean"):
+    """dci_block_aggregate (NEXT F2): mean ("avg", GCN) or sum (GraphSAGE "sum", Table III) over
+    block `hop` (default the input layer L-1, whose sources are the rows of out.X).  Returns
+    H [hop_cap, ldx] (device)."""
     import torch
     hop = out.L - 1 if hop is None else hop
     if hop != out.L - 1:
@@ -307,9 +316,10 @@ def mean_aggregate(ctx: Context, out: BatchOut, hop: int | None = None, H=None, 
     rows = out.bptr[hop].numel() - 1
     if H is None:
         H = torch.empty((max(rows, 1), out.ldx), dtype=torch.float32, device=out.X.device)
-    _check(lib().dci_mean_aggregate(ctx.handle, out.bptr[hop].data_ptr(), out.bsrc[hop].data_ptr(),
-                                    out.sizes.data_ptr() + 8 * hop, out.X.data_ptr(), out.ldx, out.D,
-                                    H.data_ptr(), H.shape[1], _stream_ptr(stream)), "dci_mean_aggregate")
+    _check(lib().dci_block_aggregate(ctx.handle, out.bptr[hop].data_ptr(), out.bsrc[hop].data_ptr(),
+                                     out.sizes.data_ptr() + 8 * hop, out.X.data_ptr(), out.ldx, out.D,
+                                     H.data_ptr(), H.shape[1], {"mean": 0, "sum": 1}[op], _stream_ptr(stream)),
+           "dci_block_aggregate")
     return H
 
 

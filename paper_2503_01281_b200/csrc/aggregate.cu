@@ -1,7 +1,7 @@
-// NEXT F2: GraphSAGE mean aggregator over one sampled block — the consumer
+// NEXT F2: mean / sum aggregator over one sampled block — the consumer
 // the prepared mini-batch feeds ("each vertex transforms the features from its
 // neighbours by aggregating them"; BJ north_star's optional consumer, reading C23).
-//   H[d][c] = (1 / k_d) * sum_{j in block row d} Xsrc[bsrc[j]][c],   k_d = 0 -> 0
+//   mean: H[d][c] = (1 / k_d) * sum_{j in block row d} Xsrc[bsrc[j]][c] (k_d = 0 -> 0); sum: no 1/k_d
 // One warp per dst row, float4 lanes across the row, fp32 accumulation in bsrc order (the
 // oracle accumulates in fp64; DESIGN.md §4 states the tolerance).  HBM-bound gather-reduce.
 #include <cuda_runtime.h>
@@ -21,6 +21,7 @@ struct AggArgs {
   int32_t D;
   float* H;
   int64_t ldh;
+  int32_t op;  // 0 mean, 1 sum
 };
 
 template <int VPL>
@@ -56,8 +57,10 @@ __global__ void __launch_bounds__(256) k_mean_aggregate_v4(AggArgs a) {
       for (int t = 0; t < VPL; ++t) {
         const int c = c0 + lane + 32 * t;
         if (c < D4) {
-          float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (j1 > j0) h = make_float4(acc[t].x / k, acc[t].y / k, acc[t].z / k, acc[t].w / k);
+          float4 h = acc[t];
+          if (a.op == 0)
+            h = j1 > j0 ? make_float4(acc[t].x / k, acc[t].y / k, acc[t].z / k, acc[t].w / k)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
           dst[c] = h;
         }
       }
@@ -75,16 +78,17 @@ __global__ void __launch_bounds__(256) k_mean_aggregate_scalar(AggArgs a) {
     for (int c = lane; c < a.D; c += 32) {
       float acc = 0.f;
       for (int32_t j = j0; j < j1; ++j) acc += __ldg(a.X + (int64_t)__ldg(a.bsrc + j) * a.ldx + c);
-      a.H[d * a.ldh + c] = j1 > j0 ? acc / (float)(j1 - j0) : 0.f;
+      a.H[d * a.ldh + c] = a.op == 1 ? acc : (j1 > j0 ? acc / (float)(j1 - j0) : 0.f);
     }
   }
 }
 
 }  // namespace
 
-dci_status launch_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
-                                 const float* X, int64_t ldx, int32_t D, float* H, int64_t ldh, cudaStream_t s) {
-  AggArgs a{bptr, bsrc, n_dst, X, ldx, D, H, ldh};
+dci_status launch_block_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                                  const float* X, int64_t ldx, int32_t D, float* H, int64_t ldh, int32_t op,
+                                  cudaStream_t s) {
+  AggArgs a{bptr, bsrc, n_dst, X, ldx, D, H, ldh, op};
   const int64_t D4x4 = (int64_t)((D + 3) / 4) * 4;
   const bool vec = ldx % 4 == 0 && ldh % 4 == 0 && ldx >= D4x4 && ldh >= D4x4 &&
                    reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(H) % 16 == 0;

@@ -418,6 +418,7 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   dci_workspace* w = new (std::nothrow) dci_workspace();
   if (!w) return fail(DCI_ENOMEM, "host allocation failed");
   w->ctx = ctx;
+  w->device = ctx->device;
   w->max_batch = max_batch;
   w->L = L;
   for (int i = 0; i < L; ++i) w->max_fan[i] = max_fanouts[i];
@@ -474,7 +475,7 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
 
 dci_status dci_workspace_destroy(dci_workspace* w) {
   if (!w) return DCI_OK;
-  DeviceGuard g(w->ctx->device);
+  DeviceGuard g(w->device);
   cudaDeviceSynchronize();
   cudaFree(w->pos_of);
   for (int i = 0; i < 2; ++i) {
@@ -755,7 +756,7 @@ dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on) {
 dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms) {
   if (!ws) return fail(DCI_EINVAL, "null workspace");
   if (!ws->have_times) return fail(DCI_ESTATE, "no profiled batch recorded");
-  DeviceGuard g(ws->ctx->device);
+  DeviceGuard g(ws->device);
   DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
   if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, ws->ev_t[0], ws->ev_t[1]));
   if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[2], ws->ev_t[3]));
@@ -764,7 +765,7 @@ dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* ga
 
 dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset) {
   if (!ws || !out) return fail(DCI_EINVAL, "bad arguments");
-  DeviceGuard g(ws->ctx->device);
+  DeviceGuard g(ws->device);
   DCI_CUDA(cudaDeviceSynchronize());
   if (ws->have_times) {
     float ms_s = 0.f, ms_g = 0.f;
@@ -794,12 +795,19 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   return DCI_OK;
 }
 
-dci_status dci_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
-                              const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, void* stream) {
+dci_status dci_block_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                               const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, int32_t op,
+                               void* stream) {
   if (!ctx || !bptr || !bsrc || !n_dst || !Xsrc || !H) return fail(DCI_EINVAL, "null argument");
   if (D < 1 || ldx < D || ldh < D) return fail(DCI_EINVAL, "need D >= 1, ldx >= D, ldh >= D");
+  if (op != DCI_AGG_MEAN && op != DCI_AGG_SUM) return fail(DCI_EINVAL, "op must be DCI_AGG_MEAN or DCI_AGG_SUM");
   DeviceGuard g(ctx->device);
-  return launch_mean_aggregate(ctx, bptr, bsrc, n_dst, Xsrc, ldx, D, H, ldh, static_cast<cudaStream_t>(stream));
+  return launch_block_aggregate(ctx, bptr, bsrc, n_dst, Xsrc, ldx, D, H, ldh, op, static_cast<cudaStream_t>(stream));
+}
+
+dci_status dci_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                              const float* Xsrc, int64_t ldx, int32_t D, float* H, int64_t ldh, void* stream) {
+  return dci_block_aggregate(ctx, bptr, bsrc, n_dst, Xsrc, ldx, D, H, ldh, DCI_AGG_MEAN, stream);
 }
 
 uint64_t dci_launch_count(const dci_ctx* ctx) { return ctx ? ctx->launches : 0; }

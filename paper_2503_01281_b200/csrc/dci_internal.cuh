@@ -99,6 +99,7 @@ struct dci_ctx {
 
 struct dci_workspace {
   dci_ctx* ctx = nullptr;
+  int device = 0;  // own copy: destroying a workspace never dereferences its context
   int32_t max_batch = 0;
   int32_t L = 0;
   int32_t max_fan[DCI_MAX_LAYERS] = {0};
@@ -177,8 +178,9 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
 
 // aggregate.cu
-dci_status launch_mean_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
-                                 const float* X, int64_t ldx, int32_t D, float* H, int64_t ldh, cudaStream_t s);
+dci_status launch_block_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,
+                                  const float* X, int64_t ldx, int32_t D, float* H, int64_t ldh, int32_t op,
+                                  cudaStream_t s);
 
 // fill.cu
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,

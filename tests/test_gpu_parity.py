@@ -211,6 +211,7 @@ def test_mean_aggregate_parity(D, ldx):
     out = dci.BatchOut(ctx, len(seeds), fan, ldx=ldx)
     dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(DEV), fan, 5, out)
     H = dci.mean_aggregate(ctx, out)
+    Hs = dci.mean_aggregate(ctx, out, op="sum")
     g = out.result()
     o = oracle.sample_gather(ip, ix, ft, seeds, fan, 5)
     _assert_batch_equal(g, o, 2)
@@ -219,6 +220,10 @@ def test_mean_aggregate_parity(D, ldx):
     Hg = H[: len(o.bptr[L - 1]) - 1, :D].cpu().numpy().astype(np.float64)
     assert np.all(np.abs(Hg - Hr) <= _agg_tol(o.bptr[L - 1], o.X, Hr))
     assert np.all(Hg[np.diff(o.bptr[L - 1]) == 0] == 0)
+    Hr_s = oracle.mean_aggregate(o.bptr[L - 1], o.bsrc[L - 1], o.X, op="sum")
+    Hg_s = Hs[: len(o.bptr[L - 1]) - 1, :D].cpu().numpy().astype(np.float64)
+    k = np.diff(o.bptr[L - 1]).astype(np.float64)[:, None]
+    assert np.all(np.abs(Hg_s - Hr_s) <= 1e-5 * np.abs(Hr_s) + k * k * 2.0 ** -24 * float(np.abs(o.X).max()))
 
 
 def test_abi_error_paths(small):

@@ -215,3 +215,6 @@ def test_mean_aggregate_equals_sparse_normalised_product(tiny_graph):
     Xc = np.tile(b.X[:1], (len(b.F), 1))
     Hc = oracle.mean_aggregate(bp, bs, Xc)
     assert np.allclose(Hc[k > 0], np.tile(b.X[:1].astype(np.float64), (int((k > 0).sum()), 1)), rtol=0, atol=0)
+    # sum aggregator (Table III "sum"): A_block . X
+    Hs = oracle.mean_aggregate(bp, bs, b.X, op="sum")
+    assert np.allclose(Hs, A @ b.X.astype(np.float64), rtol=1e-12, atol=1e-12)
