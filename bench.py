@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch size")
     ap.add_argument("--presample-batches", type=int, default=8, help="n pre-sampling batches (Fig. 11)")
+    ap.add_argument("--fill", default="dci", choices=["dci", "knapsack"],
+                    help="cache fill: DCI (Eq. 1 split + separate fills) or the NEXT F4 knapsack comparison")
     ap.add_argument("--partitioned", action="store_true",
                     help="NEXT F1: partition the feature cache across ranks (peer reads over NVLink)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -293,7 +295,16 @@ def run_ours(args):
     if C == 0 and world > 1:  # auto budget: the same C on every replica
         C = parallel.min_over_ranks_int(sum(dci.allocate(ctx, 0, [S], [F])), device=dev)
     c_adj, c_feat = dci.allocate(ctx, C, [S], [F], ratio=ratio)
-    if args.partitioned and world > 1:
+    if args.fill == "knapsack":
+        # DUCATI-style unified budget; per-access costs profiled by the presample itself
+        acc_adj = max(1, int(ec.sum(dtype=torch.int64).item()))
+        acc_feat = max(1, int(nv.sum(dtype=torch.int64).item()))
+        if C == 0:
+            C = c_adj + c_feat
+        dci.fill_knapsack(ctx, nv, ec, C, F / acc_feat, S / acc_adj)
+        info0 = dci.cache_info(ctx)
+        c_adj, c_feat = info0["adj_elems"] * 4, info0["feat_rows"] * 4 * info0["pitch"]
+    elif args.partitioned and world > 1:
         dci.fill_partitioned(ctx, nv, ec, c_adj, c_feat, world, rank)
         torch.cuda.synchronize()
         parallel.barrier(local)
@@ -444,7 +455,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
         "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B, "fanouts": list(fan),
                    "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
-                   "ratio": args.ratio,
+                   "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
                                                     if args.partitioned and world > 1 else "replicated caches") + ")",
                    "inflight": nws,

@@ -183,6 +183,18 @@ dci_status dci_fill(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edg
                     uint64_t c_feat, void* stream);
 
 /* --------------------------------------------------------------------------------------
+ * dci_fill_knapsack — NEXT F4: the DUCATI-style comparison strategy (
+ * simplified as in SPEC S:496-504, O-14): one budget C (bytes) over feature rows (value =
+ * visits * cost_feat, size = 4*pitch) and adjacency elements (value = count * cost_adj, 4 B),
+ * admitted greedily by value density (ties: feature first, then id), skipping items that no
+ * longer fit.  The admitted elements of each node form a prefix of its level-2 order, so the
+ * host CSC is reordered exactly as by dci_fill and the prefix hit rule holds.  cost_* are the
+ * times saved per hit (any unit, only their ratio matters).  Synchronises `stream`.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_fill_knapsack(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t C,
+                             double cost_feat, double cost_adj, void* stream);
+
+/* --------------------------------------------------------------------------------------
  * NEXT F1 — NVLink-partitioned feature cache (BJ north_star: "a partitioned cache read over
  * NVLink peer access").  All `world` ranks fill with the same (allreduced) counts; the admitted
  * set is the top min(N, world * floor(c_feat / (4*pitch))) nodes (O-11 with that capacity,

@@ -75,6 +75,9 @@ def lib():
         L.oracle_block_aggregate.argtypes = [_i32p, _i32p, C.c_int64, _f32p, C.c_int64, C.c_int32, C.c_int32,
                                              _f64p]
         L.oracle_block_aggregate.restype = None
+        L.oracle_knapsack_fill.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _i32p, C.c_uint64, C.c_int64,
+                                           C.c_double, C.c_double, _i32p, _i32p]
+        L.oracle_knapsack_fill.restype = C.c_uint64
         L.oracle_sample_gather.argtypes = [C.c_int64, _i64p, _i32p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                            _i32p, C.c_int32, _i32p, C.c_int32, C.c_uint64, _i32p, C.c_int64, _i64p,
                                            pp, pp, _i64p, C.c_void_p, C.c_int64, _u64p]
@@ -298,3 +301,19 @@ def mean_aggregate(bptr, bsrc, X, op: str = "mean"):
         bsrc = np.zeros(1, np.int32)
     lib().oracle_block_aggregate(bptr, bsrc, n, X, D, D, {"mean": 0, "sum": 1}[op], H)
     return H[:n]
+
+
+def knapsack_fill(indptr, node_visits, edge_counts, C_bytes: int, row_bytes: int, cost_feat: float,
+                  cost_adj: float):
+    """O-14 unified-budget greedy knapsack (DUCATI-style).  Returns
+    (slot_of, cached_len, bytes_used)."""
+    indptr = np.ascontiguousarray(indptr, np.int64)
+    v = np.ascontiguousarray(node_visits, np.int32)
+    c = np.ascontiguousarray(edge_counts, np.int32)
+    N, E = len(indptr) - 1, len(c)
+    slot = np.zeros(max(N, 1), np.int32)
+    cl = np.zeros(max(N, 1), np.int32)
+    if E == 0:
+        c = np.zeros(1, np.int32)
+    used = lib().oracle_knapsack_fill(N, E, indptr, v, c, C_bytes, row_bytes, cost_feat, cost_adj, slot, cl)
+    return slot[:N], cl[:N], int(used)

@@ -375,6 +375,54 @@ void oracle_block_aggregate(const int32_t* bptr, const int32_t* bsrc, int64_t n_
     }
 }
 
+// O-14 DUCATI-style unified-budget knapsack fill, as simplified by SPEC
+// (S:496-504): items are feature rows (value = visits * cost_feat, size = row_bytes) and
+// adjacency elements (value = count * cost_adj, size = 4 B); sort by value density
+// (value / size) descending, ties by kind (feature first) then id (node id / CSC position);
+// admit every item that still fits the remaining budget, in that order.  Admitted adjacency
+// elements are regrouped per node by the level-2 order (count desc, position asc): the
+// cached prefix of node v has length = #admitted elements of v ("re-sorting admitted
+// elements within each node by count so the prefix hit rule still applies").
+// Outputs: slot_of[N] (admitted rows, slots in ascending id), cached_len[N]; returns bytes used.
+uint64_t oracle_knapsack_fill(int64_t N, int64_t E, const int64_t* indptr, const int32_t* visits,
+                              const int32_t* counts, uint64_t C, int64_t row_bytes, double cost_feat,
+                              double cost_adj, int32_t* slot_of, int32_t* cached_len) {
+    struct Item {
+        double density;
+        int kind;     // 0 feature row, 1 adjacency element
+        int64_t id;   // node id or CSC position
+        int64_t size;
+    };
+    std::vector<Item> items;
+    items.reserve((size_t)(N + E));
+    for (int64_t v = 0; v < N; ++v)
+        items.push_back({(double)visits[v] * cost_feat / (double)row_bytes, 0, v, row_bytes});
+    for (int64_t e = 0; e < E; ++e) items.push_back({(double)counts[e] * cost_adj / 4.0, 1, e, 4});
+    std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+        if (a.density != b.density) return a.density > b.density;
+        if (a.kind != b.kind) return a.kind < b.kind;
+        return a.id < b.id;
+    });
+    uint64_t left = C;
+    std::vector<char> adm_node((size_t)N, 0), adm_elem((size_t)E, 0);
+    for (const Item& it : items) {
+        if ((uint64_t)it.size > left) continue;
+        left -= (uint64_t)it.size;
+        if (it.kind == 0)
+            adm_node[(size_t)it.id] = 1;
+        else
+            adm_elem[(size_t)it.id] = 1;
+    }
+    int32_t slot = 0;
+    for (int64_t v = 0; v < N; ++v) slot_of[v] = adm_node[(size_t)v] ? slot++ : -1;
+    for (int64_t v = 0; v < N; ++v) {
+        int32_t c = 0;
+        for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) c += adm_elem[(size_t)e];
+        cached_len[v] = c;
+    }
+    return C - left;
+}
+
 // One inference step on the CPU (bench.py cpu_baseline): O-6 with pass 0 over the
 // current CSC and the adjacency cache, then O-7.  Thin composition, no new arithmetic.
 int32_t oracle_sample_gather(int64_t N, const int64_t* indptr, const int32_t* indices_cur,

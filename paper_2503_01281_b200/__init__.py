@@ -30,7 +30,7 @@ OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
             "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
             "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
-            "dci_workspace_stats", "dci_mean_aggregate", "dci_block_aggregate", "dci_fill_partitioned", "dci_feature_partition_handle",
+            "dci_workspace_stats", "dci_mean_aggregate", "dci_block_aggregate", "dci_fill_partitioned", "dci_fill_knapsack", "dci_feature_partition_handle",
             "dci_attach_feature_partitions", "dci_launch_count", "dci_last_error", "dci_version"]
 IPC_HANDLE_BYTES = 64
 
@@ -85,6 +85,7 @@ def lib():
         "dci_allocate": [vp, u64, vp, vp, i32, i64, i64, C.POINTER(u64), C.POINTER(u64)],
         "dci_fill": [vp, vp, vp, u64, u64, vp],
         "dci_fill_partitioned": [vp, vp, vp, u64, u64, i32, i32, vp],
+        "dci_fill_knapsack": [vp, vp, vp, u64, C.c_double, C.c_double, vp],
         "dci_feature_partition_handle": [vp, vp],
         "dci_attach_feature_partitions": [vp, vp, i32],
         "dci_cache_info_get": [vp, C.POINTER(dci_cache_info)],
@@ -364,6 +365,14 @@ def fill_partitioned(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat:
     partition); rank -1 = all partitions on this device (emulation)."""
     _check(lib().dci_fill_partitioned(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None,
                                       c_adj, c_feat, world, rank, _stream_ptr(stream)), "dci_fill_partitioned")
+
+
+def fill_knapsack(ctx: Context, node_visits, edge_counts, C_bytes: int, cost_feat: float, cost_adj: float,
+                  stream=None):
+    """dci_fill_knapsack (NEXT F4): DUCATI-style unified-budget greedy fill (comparison)."""
+    _check(lib().dci_fill_knapsack(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None,
+                                   C_bytes, float(cost_feat), float(cost_adj), _stream_ptr(stream)),
+           "dci_fill_knapsack")
 
 
 def feature_partition_handle(ctx: Context) -> bytes:

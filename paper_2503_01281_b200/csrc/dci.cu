@@ -668,6 +668,17 @@ dci_status dci_fill_partitioned(dci_ctx* ctx, const int32_t* node_visits, const 
   return fill_impl(ctx, node_visits, edge_counts, c_adj, c_feat, world, rank, static_cast<cudaStream_t>(stream));
 }
 
+dci_status dci_fill_knapsack(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t C,
+                             double cost_feat, double cost_adj, void* stream) {
+  if (!ctx) return fail(DCI_EINVAL, "null context");
+  if (!node_visits || (ctx->E > 0 && !edge_counts)) return fail(DCI_EINVAL, "null count array");
+  if (!(cost_feat >= 0.0) || !(cost_adj >= 0.0)) return fail(DCI_EINVAL, "costs must be >= 0");
+  DeviceGuard g(ctx->device);
+  DCI_CUDA(cudaDeviceSynchronize());
+  KnapsackPlan plan{C, cost_feat, cost_adj};
+  return fill_impl(ctx, node_visits, edge_counts, 0, 0, 1, 0, static_cast<cudaStream_t>(stream), &plan);
+}
+
 dci_status dci_feature_partition_handle(dci_ctx* ctx, void* handle) {
   if (!ctx || !handle) return fail(DCI_EINVAL, "bad arguments");
   if (!ctx->d_fcache) return fail(DCI_ESTATE, "no feature partition on this device (fill first)");

@@ -183,8 +183,14 @@ dci_status launch_block_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32
                                   cudaStream_t s);
 
 // fill.cu
+struct KnapsackPlan {  // NEXT F4 unified budget (O-14)
+  uint64_t C;
+  double cost_feat;  // time saved per feature-row hit
+  double cost_adj;   // time saved per adjacency-element hit
+};
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
-                     uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s);
+                     uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s,
+                     const KnapsackPlan* knap = nullptr);
 void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t s);
 void release_feature_partitions(dci_ctx* ctx);
 

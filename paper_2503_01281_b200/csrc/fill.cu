@@ -336,6 +336,57 @@ struct AdjLenOp {
   }
 };
 
+// knapsack adjacency: value = ties of node v (exclusive scan -> ties before v)
+struct TieScanOp {
+  const int32_t* ties;
+  int64_t* ties_before;
+  __device__ __forceinline__ int64_t value(int64_t v) const { return ties[v]; }
+  __device__ __forceinline__ void write(int64_t v, int64_t excl, int64_t) const { ties_before[v] = excl; }
+};
+
+// knapsack adjacency: cached_len = #count > cv + the node's share of the first cm ties
+struct KnapAdjOp {
+  const int32_t* gt;
+  const int32_t* ties;
+  const int64_t* ties_before;
+  int64_t cm;
+  DirEntry* dir;
+  __device__ __forceinline__ int64_t value(int64_t v) const {
+    const int64_t take = cm - ties_before[v];
+    return (int64_t)gt[v] + (take <= 0 ? 0 : (take < ties[v] ? take : ties[v]));
+  }
+  __device__ __forceinline__ void write(int64_t v, int64_t excl, int64_t val) const {
+    dir[v].cached_len = (int32_t)val;
+    dir[v].cache_off = excl;
+  }
+};
+
+// knapsack features: tie rank among nodes with visits == fv
+struct FeatTieOp {
+  const int32_t* visits;
+  int32_t fv;
+  int64_t* rank;
+  __device__ __forceinline__ int64_t value(int64_t v) const { return visits[v] == fv ? 1 : 0; }
+  __device__ __forceinline__ void write(int64_t v, int64_t excl, int64_t) const { rank[v] = excl; }
+};
+
+struct KnapFeatOp {
+  const int32_t* visits;
+  int32_t fv;
+  int64_t fm;
+  const int64_t* rank;
+  DirEntry* dir;
+  int64_t* list;
+  __device__ __forceinline__ int64_t value(int64_t v) const {
+    const int32_t x = visits[v];
+    return (x > fv || (x == fv && rank[v] < fm)) ? 1 : 0;
+  }
+  __device__ __forceinline__ void write(int64_t v, int64_t excl, int64_t val) const {
+    dir[v].slot = val ? (int32_t)excl : -1;
+    if (val) list[excl] = (excl << 32) | v;
+  }
+};
+
 __global__ void k_copy_prefixes(const int64_t* __restrict__ indptr, const DirEntry* __restrict__ dir, int64_t N,
                                 const int32_t* __restrict__ idxR, int32_t* __restrict__ acache) {
   const int lane = threadIdx.x & 31;
@@ -384,6 +435,50 @@ __global__ void k_copy_rows_partitioned(const int64_t* __restrict__ list, int64_
     const int4* sp = reinterpret_cast<const int4*>(src + v * pitch);
     int4* dp = reinterpret_cast<int4*>(dst + row * pitch);
     for (int c = lane; c < row16; c += 32) dp[c] = sp[c];
+  }
+}
+
+// ---- knapsack fill (NEXT F4) helpers ----
+// histogram of small non-negative integers: block-private in shared memory when the value
+// range fits (few bins receive millions of increments), merged with one atomic per bin
+constexpr int kSmemBins = 4096;
+__global__ void k_hist_i32(const int32_t* __restrict__ a, int64_t n, int32_t nbins, unsigned long long* hist) {
+  __shared__ unsigned int sh[kSmemBins];
+  const bool priv = nbins <= kSmemBins;
+  if (priv)
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (priv)
+      atomicAdd(&sh[a[i]], 1u);
+    else
+      atomicAdd(hist + a[i], 1ull);
+  }
+  __syncthreads();
+  if (priv)
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+      if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
+}
+
+// per node: gt = #elements with count > cv, ties = #elements with count == cv
+__global__ void k_node_level_counts(const int64_t* __restrict__ indptr, const int32_t* __restrict__ cnt, int64_t N,
+                                    int32_t cv, int32_t* gt, int32_t* ties) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < N; v += nwarps) {
+    int32_t g = 0, t = 0;
+    for (int64_t e = indptr[v] + lane; e < indptr[v + 1]; e += 32) {
+      const int32_t c = cnt[e];
+      g += c > cv;
+      t += c == cv;
+    }
+    g = __reduce_add_sync(0xffffffffu, g);
+    t = __reduce_add_sync(0xffffffffu, t);
+    if (lane == 0) {
+      gt[v] = g;
+      ties[v] = t;
+    }
   }
 }
 
@@ -457,8 +552,60 @@ void release_feature_partitions(dci_ctx* ctx) {
   }
 }
 
+// Host walk of the knapsack's density levels (O-14 order: density desc, feature before
+// adjacency on ties, ids ascending inside a level), admitting whole levels while they fit.
+// Result: features {visits > fv} + the first fm (by id) with visits == fv; adjacency
+// {count > cv} + the first cm (by CSC position) with count == cv.  fv = -1 / cv = -1: all.
+void knapsack_levels(const std::vector<unsigned long long>& hf, const std::vector<unsigned long long>& ha,
+                     uint64_t C, int64_t R, double cf, double ca, int32_t* fv, int64_t* fm, int32_t* cv,
+                     int64_t* cm, uint64_t* used) {
+  int vi = (int)hf.size() - 1, ci = (int)ha.size() - 1;
+  uint64_t left = C;
+  bool fclosed = false, done = false;
+  *fv = -1;
+  *fm = 0;
+  *cv = -1;
+  *cm = 0;
+  while (!done && (vi >= 0 || ci >= 0)) {
+    const double df = vi >= 0 ? (double)vi * cf / (double)R : -1.0;
+    const double da = ci >= 0 ? (double)ci * ca / 4.0 : -1.0;
+    if (vi >= 0 && df >= da) {  // feature level (first on ties)
+      if (!fclosed) {
+        const unsigned long long need = hf[vi] * (unsigned long long)R;
+        if (need <= left) {
+          left -= need;
+        } else {
+          const int64_t m = (int64_t)(left / (uint64_t)R);
+          left -= (uint64_t)m * (uint64_t)R;
+          *fv = vi;
+          *fm = m;
+          fclosed = true;
+        }
+      }
+      --vi;
+    } else {
+      const unsigned long long need = ha[ci] * 4ull;
+      if (need <= left) {
+        left -= need;
+      } else {
+        const int64_t m = (int64_t)(left / 4);
+        left -= (uint64_t)m * 4;
+        *cv = ci;
+        *cm = m;
+        done = true;  // fewer than 4 bytes left: nothing else fits
+        if (!fclosed) {
+          *fv = vi;  // lower feature levels were never reached
+          *fm = 0;
+        }
+      }
+      --ci;
+    }
+  }
+  *used = C - left;
+}
+
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
-                     uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s) {
+                     uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s, const KnapsackPlan* knap) {
   const int64_t N = ctx->N, E = ctx->E;
   const int64_t row_bytes = 4ll * ctx->pitch;
   // c_feat is the budget of ONE partition; the admitted set spans all `world` partitions
@@ -565,6 +712,86 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
   ctx->fpart_rank = rank;
   k_dir_reset_caches<<<grid_for(ctx, 4), 256, 0, s>>>(ctx->d_dir, N);
   ++ctx->launches;
+
+  if (knap) {
+    // ---- NEXT F4: unified-budget knapsack over feature rows and adjacency elements ----
+    int32_t vmax = 0;
+    DCI_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(int32_t) * 4, s));
+    k_max_i32<<<grid_for(ctx, 4), 256, 0, s>>>(node_visits, N, d_scal);
+    ++ctx->launches;
+    DCI_CUDA(cudaMemcpyAsync(&vmax, d_scal, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    DCI_CUDA(cudaStreamSynchronize(s));
+    if (vmax > (1 << 20) || cmax > (1 << 20)) return fail(DCI_ERANGE, "knapsack fill: counts above 2^20");
+    unsigned long long *d_hf = nullptr, *d_ha = nullptr;
+    DCI_CUDA(tmp.alloc(&d_hf, sizeof(unsigned long long) * (vmax + 1)));
+    DCI_CUDA(tmp.alloc(&d_ha, sizeof(unsigned long long) * (cmax + 1)));
+    DCI_CUDA(cudaMemsetAsync(d_hf, 0, sizeof(unsigned long long) * (vmax + 1), s));
+    DCI_CUDA(cudaMemsetAsync(d_ha, 0, sizeof(unsigned long long) * (cmax + 1), s));
+    k_hist_i32<<<grid_for(ctx, 4), 256, 0, s>>>(node_visits, N, vmax + 1, d_hf);
+    if (E) k_hist_i32<<<grid_for(ctx, 4), 256, 0, s>>>(edge_counts, E, cmax + 1, d_ha);
+    ctx->launches += E ? 2 : 1;
+    std::vector<unsigned long long> hf(vmax + 1), ha(cmax + 1);
+    DCI_CUDA(cudaMemcpyAsync(hf.data(), d_hf, sizeof(unsigned long long) * (vmax + 1), cudaMemcpyDeviceToHost, s));
+    DCI_CUDA(cudaMemcpyAsync(ha.data(), d_ha, sizeof(unsigned long long) * (cmax + 1), cudaMemcpyDeviceToHost, s));
+    DCI_CUDA(cudaStreamSynchronize(s));
+    if (!E) ha.assign(1, 0ull);
+    int32_t fv, cv;
+    int64_t fm, cm;
+    uint64_t used;
+    knapsack_levels(hf, ha, knap->C, row_bytes, knap->cost_feat, knap->cost_adj, &fv, &fm, &cv, &cm, &used);
+    // adjacency: per-node counts above / at the cut level, ties before each node
+    int32_t *d_gt = nullptr, *d_ties = nullptr;
+    int64_t* d_tb = nullptr;
+    DCI_CUDA(tmp.alloc(&d_gt, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+    DCI_CUDA(tmp.alloc(&d_ties, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+    DCI_CUDA(tmp.alloc(&d_tb, sizeof(int64_t) * std::max<int64_t>(N, 1)));
+    k_node_level_counts<<<grid_for(ctx, 8), 256, 0, s>>>(d_indptr, edge_counts, N, cv, d_gt, d_ties);
+    ++ctx->launches;
+    dci_status r = scan_nodes(ctx, TieScanOp{d_ties, d_tb}, N, d_sum, s);
+    if (r != DCI_OK) return r;
+    r = scan_nodes(ctx, KnapAdjOp{d_gt, d_ties, d_tb, cv < 0 ? 0 : cm, ctx->d_dir}, N, d_sum, s);
+    if (r != DCI_OK) return r;
+    int64_t adj_elems = 0;
+    DCI_CUDA(cudaMemcpyAsync(&adj_elems, d_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DCI_CUDA(cudaStreamSynchronize(s));
+    if (adj_elems > 0) {
+      DCI_CUDA(cudaMalloc(&ctx->d_acache, sizeof(int32_t) * adj_elems));
+      k_copy_prefixes<<<grid_for(ctx, 8), 256, 0, s>>>(d_indptr, ctx->d_dir, N, d_idxR, ctx->d_acache);
+      ++ctx->launches;
+    }
+    ctx->acache_len = adj_elems;
+    // features: tie ranks at the cut level, then admission + slots in ascending id
+    int64_t* d_rank = nullptr;
+    DCI_CUDA(tmp.alloc(&d_rank, sizeof(int64_t) * std::max<int64_t>(N, 1)));
+    r = scan_nodes(ctx, FeatTieOp{node_visits, fv, d_rank}, N, d_sum, s);
+    if (r != DCI_OK) return r;
+    int64_t* d_list = nullptr;
+    DCI_CUDA(tmp.alloc(&d_list, sizeof(int64_t) * std::max<int64_t>(N, 1)));
+    r = scan_nodes(ctx, KnapFeatOp{node_visits, fv, fm, d_rank, ctx->d_dir, d_list}, N, d_sum, s);
+    if (r != DCI_OK) return r;
+    int64_t rows = 0;
+    DCI_CUDA(cudaMemcpyAsync(&rows, d_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DCI_CUDA(cudaStreamSynchronize(s));
+    DCI_CUDA(cudaMalloc(&ctx->d_fcache, (size_t)row_bytes * std::max<int64_t>(rows, 1)));
+    if (rows > 0) {
+      k_copy_rows_from_host<<<grid_for(ctx, 8), 256, 0, s>>>(d_list, rows, ctx->u_feats, ctx->pitch,
+                                                              ctx->d_fcache);
+      ++ctx->launches;
+    }
+    ctx->fcache_rows = ctx->fcache_total_rows = rows;
+    ctx->h_fbases[0] = ctx->d_fcache;
+    if (!ctx->d_fbases) DCI_CUDA(cudaMalloc(&ctx->d_fbases, sizeof(float*) * dci_ctx::kMaxParts));
+    DCI_CUDA(cudaMemcpyAsync(ctx->d_fbases, ctx->h_fbases, sizeof(float*) * dci_ctx::kMaxParts,
+                             cudaMemcpyHostToDevice, s));
+    DCI_CUDA(cudaGetLastError());
+    DCI_CUDA(cudaStreamSynchronize(s));
+    rollback.committed = true;
+    ctx->whole_fit = adj_elems == E ? 1 : 0;
+    ctx->c_adj = (uint64_t)adj_elems * 4;
+    ctx->c_feat = (uint64_t)rows * (uint64_t)row_bytes;
+    ctx->state = DCI_STATE_FILLED;
+    return DCI_OK;
+  }
 
   // ---- adjacency cache (Algorithm 1) ----
   AdjKey ak{d_total, d_indptr};

@@ -94,3 +94,47 @@ def test_random_configuration(trial):
             assert np.array_equal(g["bsrc"][h], o.bsrc[h])
         assert np.array_equal(g["counters"], o.counters)
         assert np.array_equal(g["X"], o.X)
+
+
+@pytest.mark.parametrize("trial", range(16))
+def test_knapsack_fill_parity(trial):
+    """NEXT F4: the GPU knapsack (histogram-level walk + scans) equals the oracle's full-sort
+    greedy (O-14) for random budgets / cost ratios, and batches sampled on it match."""
+    rng = np.random.default_rng(5000 + trial)
+    ip, ix = _graph(rng, ["rmat", "hub", "uniform"][trial % 3])
+    N, E = len(ip) - 1, len(ix)
+    D = int(rng.choice([4, 30, 64]))
+    ft = synth.features(N, D).numpy()
+    fan = tuple(int(x) for x in rng.integers(1, 16, int(rng.integers(1, 4))))
+    ctx = dci.load_graph(ip, ix, ft)
+    el = synth.eligible_nodes(ip)
+    if len(el) == 0:
+        pytest.skip("graph without edges")
+    B = int(rng.integers(1, min(len(el), 200) + 1))
+    pre = rng.permutation(el)[: 3 * B].astype(np.int32)
+    nv = torch.zeros(N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(max(E, 1), dtype=torch.int32, device=DEV)
+    dci.presample(ctx, torch.from_numpy(pre).to(DEV), B, fan, 5, nv, ec)
+    nv_o, ec_o = oracle.presample(ip, ix, pre, B, fan, 5)
+    R = 4 * ((D + 3) // 4 * 4)
+    Cb = int(rng.integers(0, N * R + 4 * E + 64))
+    cf, ca = float(rng.choice([0.5, 1.0, 7.3, 40.0])), float(rng.choice([0.2, 1.0, 3.0]))
+    dci.fill_knapsack(ctx, nv, ec, Cb, cf, ca)
+    slot_o, cl_o, used = oracle.knapsack_fill(ip, nv_o, ec_o, Cb, R, cf, ca)
+    st = dci.cache_state(ctx)
+    R_idx, _, _, _ = oracle.adj_fill(ip, ix, ec_o, 0)  # level-2 order (the knapsack keeps it)
+    assert np.array_equal(st["indices_cur"], R_idx)
+    assert np.array_equal(st["slot_of"], slot_o)
+    assert np.array_equal(st["cached_len"], cl_o)
+    assert st["info"]["adj_elems"] * 4 + st["info"]["feat_rows"] * R == used
+    for v in np.nonzero(cl_o)[0]:
+        a = st["cache_off"][v]
+        assert np.array_equal(st["acache"][a:a + cl_o[v]], R_idx[ip[v]:ip[v] + cl_o[v]])
+    ws = dci.workspace_create(ctx, B, fan)
+    seeds = rng.choice(N, size=min(B, N), replace=False).astype(np.int32)
+    out = dci.BatchOut(ctx, len(seeds), fan)
+    dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(DEV), fan, 17, out)
+    g = out.result()
+    o = oracle.sample_gather(ip, R_idx, ft, seeds, fan, 17, cl_o, slot_o)
+    assert np.array_equal(g["F"], o.F) and np.array_equal(g["counters"], o.counters)
+    assert np.array_equal(g["X"], o.X)

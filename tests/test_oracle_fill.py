@@ -166,3 +166,56 @@ def test_table1_redundancy_arithmetic():
     t = SPEC["table1"]
     for bs, fan, loaded, ratio in t["rows"]:
         assert round(loaded / t["test_nodes"], 3) == pytest.approx(ratio, abs=1e-3)
+
+
+# ----------------------------------------------------------------------------- F4 knapsack
+def test_knapsack_spec_example():
+    """one feature row (count 100, 4 bytes) vs one adjacency element (count 1, 4 bytes),
+    budget 4 -> the feature row is admitted."""
+    indptr = np.array([0, 1], np.int64)
+    slot, cl, used = oracle.knapsack_fill(indptr, [100], [1], 4, 4, 1.0, 1.0)
+    assert slot.tolist() == [0] and cl.tolist() == [0] and used == 4
+
+
+def test_knapsack_properties():
+    """Budget respected; full budget admits everything; every non-admitted item that would fit
+    the leftover has density no higher than the lowest admitted item of its kind (greedy);
+    each node's admitted elements are its top-count elements (the level-2 prefix, so the
+    prefix hit rule holds); monotone in the budget."""
+    rng = np.random.default_rng(7)
+    for _ in range(150):
+        N = int(rng.integers(1, 30))
+        indptr, _ = random_csc(rng, N, 6)
+        E = int(indptr[-1])
+        visits = rng.integers(0, 6, N).astype(np.int32)
+        counts = rng.integers(0, 5, E).astype(np.int32)
+        R = int(rng.choice([16, 64, 400]))
+        cf, ca = float(rng.uniform(0.1, 5)), float(rng.uniform(0.1, 5))
+        total = N * R + 4 * E
+        Cb = int(rng.integers(0, total + 20))
+        slot, cl, used = oracle.knapsack_fill(indptr, visits, counts, Cb, R, cf, ca)
+        adm = slot >= 0
+        assert used <= Cb and used == int(adm.sum()) * R + 4 * int(cl.sum())
+        assert slot[adm].tolist() == list(range(int(adm.sum())))
+        left = Cb - used
+        dens_f = visits * cf / R
+        dens_a = counts * ca / 4.0
+        if adm.any() and (~adm).any() and left >= R:
+            raise AssertionError("a feature row still fits but was not admitted")
+        for v in range(N):
+            run = counts[indptr[v]:indptr[v + 1]]
+            order = np.lexsort((np.arange(len(run)), -run.astype(np.int64)))
+            top = run[order][: cl[v]]
+            rest = run[order][cl[v]:]
+            if len(top) and len(rest):
+                assert top.min() >= rest.max()  # prefix of the level-2 order
+        adm_a = np.concatenate([np.r_[np.ones(cl[v]), np.zeros(indptr[v + 1] - indptr[v] - cl[v])]
+                                for v in range(N)]) if E else np.zeros(0)
+        if adm.any():
+            not_adm_f = dens_f[~adm]
+            if len(not_adm_f) and left >= R:
+                assert not_adm_f.max() <= dens_f[adm].min()
+        full_slot, full_cl, _ = oracle.knapsack_fill(indptr, visits, counts, total, R, cf, ca)
+        assert (full_slot >= 0).all() and full_cl.tolist() == np.diff(indptr).tolist()
+        s2, c2, _ = oracle.knapsack_fill(indptr, visits, counts, Cb + 4 * E + R * N, R, cf, ca)
+        assert ((s2 >= 0) | ~adm).all() and (c2 >= cl).all()
