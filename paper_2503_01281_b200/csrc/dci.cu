@@ -4,12 +4,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 #include <unordered_map>
 
 #include "dci_internal.cuh"
@@ -44,6 +47,25 @@ int occupancy_blocks(const void* kernel, int block, int cap) {
 }
 
 namespace {
+
+// Run body(lo, hi) over [0, n) on up to hardware_concurrency host threads (load-time copies and
+// validation of graphs with billions of edges; not on the per-batch path).
+template <class F>
+void parallel_for(int64_t n, int64_t grain, F body) {
+  const int64_t hw = std::max<int64_t>(1, std::thread::hardware_concurrency());
+  const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hw, n / std::max<int64_t>(grain, 1)));
+  if (nt <= 1) {
+    body(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t chunk = (n + nt - 1) / nt;
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t lo = t * chunk, hi = std::min<int64_t>(n, lo + chunk);
+    if (lo < hi) th.emplace_back(body, lo, hi);
+  }
+  for (auto& x : th) x.join();
+}
 
 bool gather_serial() {
   static int mode = -1;
@@ -257,7 +279,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     }
     if (part == 0) {
       ctx->launches += ws->graph_kernels[0];
-      return cudaGraphLaunch(ws->graph_exec[0], s);
+      return cudaGraphLaunch(ws->graph_exec[0], rs);
     }
     return cudaSuccess;  // single graph holds both parts
   };
@@ -325,8 +347,13 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
     if (indptr[v + 1] < indptr[v]) return fail(DCI_EINVAL, "indptr must be non-decreasing");
     if (indptr[v + 1] - indptr[v] >= (1ll << 31)) return fail(DCI_ERANGE, "a degree exceeds 2^31-1");
   }
-  for (int64_t e = 0; e < E; ++e)
-    if (indices[e] < 0 || (int64_t)indices[e] >= N) return fail(DCI_EINVAL, "indices entry out of [0, N)");
+  std::atomic<bool> bad_index{false};
+  parallel_for(E, 1 << 24, [&](int64_t lo, int64_t hi) {
+    bool bad = false;
+    for (int64_t e = lo; e < hi; ++e) bad |= indices[e] < 0 || (int64_t)indices[e] >= N;
+    if (bad) bad_index = true;
+  });
+  if (bad_index) return fail(DCI_EINVAL, "indices entry out of [0, N)");
   int ndev = 0;
   DCI_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(DCI_EINVAL, "bad device ordinal");
@@ -350,19 +377,24 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
   e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_idx_orig), sizeof(int32_t) * std::max<int64_t>(E, 1),
                     cudaHostAllocMapped | cudaHostAllocPortable);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(indices)"));
-  if (E) memcpy(c->h_idx_orig, indices, sizeof(int32_t) * E);
+  parallel_for(E, 1 << 24, [&](int64_t lo, int64_t hi) {
+    memcpy(c->h_idx_orig + lo, indices + lo, sizeof(int32_t) * (hi - lo));
+  });
   c->h_idx_cur = c->h_idx_orig;
   const size_t fbytes = sizeof(float) * (size_t)N * c->pitch;
   e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_feats), fbytes, cudaHostAllocMapped | cudaHostAllocPortable);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(feats)"));
-  if (c->pitch == D) {
-    memcpy(c->h_feats, feats, fbytes);
-  } else {
-    for (int64_t v = 0; v < N; ++v) {
-      memcpy(c->h_feats + v * c->pitch, feats + v * D, sizeof(float) * D);
-      memset(c->h_feats + v * c->pitch + D, 0, sizeof(float) * (c->pitch - D));
+  const int64_t pitch = c->pitch;
+  parallel_for(N, 1 << 16, [&](int64_t lo, int64_t hi) {
+    if (pitch == D) {
+      memcpy(c->h_feats + lo * pitch, feats + lo * D, sizeof(float) * D * (hi - lo));
+    } else {
+      for (int64_t v = lo; v < hi; ++v) {
+        memcpy(c->h_feats + v * pitch, feats + v * D, sizeof(float) * D);
+        memset(c->h_feats + v * pitch + D, 0, sizeof(float) * (pitch - D));
+      }
     }
-  }
+  });
   void* dp = nullptr;
   if ((e = cudaHostGetDevicePointer(&dp, c->h_idx_orig, 0)) != cudaSuccess)
     return bail(cuda_fail(e, "cudaHostGetDevicePointer"));
@@ -399,7 +431,8 @@ dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanou
   int64_t caps[DCI_MAX_LAYERS + 1];
   frontier_bounds(ctx->N, B, fanouts, L, caps);
   for (int h = 0; h < L; ++h)
-    if (caps[h] * fanouts[L - 1 - h] >= (1ll << 31)) return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
+    if (caps[h] * (fanouts[L - 1 - h] + 1) >= (1ll << 31))
+      return fail(DCI_ERANGE, "batch too large: |F_h| * (f + 1) must stay < 2^31");
   for (int h = 0; h <= L; ++h)
     if (frontier_caps) frontier_caps[h] = caps[h];
   for (int h = 0; h < L; ++h)
@@ -426,9 +459,9 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   int64_t max_front = 0;
   for (int h = 0; h <= L; ++h) max_front = std::max(max_front, w->hop_cap[h]);
   for (int h = 0; h < L; ++h)
-    if (w->hop_cap[h] * max_fanouts[L - 1 - h] >= (1ll << 31)) {
+    if (w->hop_cap[h] * (max_fanouts[L - 1 - h] + 1) >= (1ll << 31)) {
       delete w;
-      return fail(DCI_ERANGE, "batch too large: |F_h| * f must stay < 2^31");
+      return fail(DCI_ERANGE, "batch too large: |F_h| * (f + 1) must stay < 2^31");
     }
   w->cand_cap = 0;
   w->tiles_cap = 0;
