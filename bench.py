@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--presample-batches", type=int, default=8, help="n pre-sampling batches (Fig. 11)")
     ap.add_argument("--fill", default="dci", choices=["dci", "knapsack"],
                     help="cache fill: DCI (Eq. 1 split + separate fills) or the NEXT F4 knapsack comparison")
+    ap.add_argument("--cap-to-data", action="store_true",
+                    help="reading B4: cap each side of the split at its data (per feature partition)")
     ap.add_argument("--partitioned", action="store_true",
                     help="NEXT F1: partition the feature cache across ranks (peer reads over NVLink)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -295,6 +297,9 @@ def run_ours(args):
     if C == 0 and world > 1:  # auto budget: the same C on every replica
         C = parallel.min_over_ranks_int(sum(dci.allocate(ctx, 0, [S], [F])), device=dev)
     c_adj, c_feat = dci.allocate(ctx, C, [S], [F], ratio=ratio)
+    if args.cap_to_data:
+        parts = world if (args.partitioned and world > 1) else 1
+        c_adj, c_feat = parallel.cap_split_to_data(c_adj, c_feat, 4 * cfg.E, 4 * cfg.pitch_floats() * cfg.N, parts)
     if args.fill == "knapsack":
         # DUCATI-style unified budget; per-access costs profiled by the presample itself
         acc_adj = max(1, int(ec.sum(dtype=torch.int64).item()))

@@ -19,7 +19,7 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdci.so")
+LIB_PATH = os.environ.get("DCI_LIB", os.path.join(_HERE, "libdci.so"))  # override: build experiments
 MAX_LAYERS = 8
 MAX_FANOUT = 1024
 

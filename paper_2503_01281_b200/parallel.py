@@ -115,3 +115,18 @@ def exchange_feature_partitions(ctx, group=None):
         handles = [mine]
     dci.attach_feature_partitions(ctx, handles)
     return handles
+
+
+def cap_split_to_data(c_adj: int, c_feat: int, adj_bytes: int, feat_bytes: int, feat_partitions: int = 1):
+    """Build-level reading B4, opt-in: a cache never needs more than its data
+    (the feature cache of one of G partitions at most ceil(feat_bytes / G)), so the excess of
+    one side of Eq. 1's split goes to the other.  Total C = c_adj + c_feat is unchanged."""
+    C = c_adj + c_feat
+    feat_need = -(-feat_bytes // max(1, feat_partitions))
+    if c_feat > feat_need:
+        c_feat = feat_need
+        c_adj = C - c_feat
+    if c_adj > adj_bytes:
+        c_adj = adj_bytes
+        c_feat = min(C - c_adj, max(c_feat, C - c_adj))
+    return c_adj, C - c_adj

@@ -85,3 +85,13 @@ def test_shard_round_robin():
     assert parallel.shard(items, 0, 3) == [0, 3, 6, 9]
     assert parallel.shard(items, 2, 3) == [2, 5, 8]
     assert sorted(sum((parallel.shard(items, r, 4) for r in range(4)), [])) == items
+
+
+def test_cap_split_to_data():
+    """Reading B4: the excess of one side of the split over its data goes to the other; the
+    total is unchanged; feature need is per partition."""
+    assert parallel.cap_split_to_data(100, 900, 1000, 400) == (600, 400)
+    assert parallel.cap_split_to_data(900, 100, 300, 5000) == (300, 700)
+    assert parallel.cap_split_to_data(10, 20, 1000, 1000) == (10, 20)  # nothing to move
+    a, f = parallel.cap_split_to_data(1_159_508_631, 14_671_851_609, 4 * 1_615_685_872, 512 * 111_059_956, 8)
+    assert a == 4 * 1_615_685_872 and a + f == 1_159_508_631 + 14_671_851_609 and f * 8 >= 512 * 111_059_956
