@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle wall time for cpu_baseline")
     ap.add_argument("--no-check", action="store_true", help="skip the bit-exact spot check vs the oracle")
+    ap.add_argument("--check-light", action="store_true",
+                    help="full-size parity without a host feature copy: oracle presample/fill/sampling on the "
+                         "same graph, X rows checked against the closed-form features (papers100M-shaped)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/check)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to test several ranks on one GPU)")
@@ -166,6 +169,34 @@ def make_inputs(cfg, device):
 
 
 # ------------------------------------------------------------------------------ oracle (cpu)
+def light_check(cfg, ip, ix, c_adj, c_feat, gpu_results, npre=8, rows=4096):
+    """Bit-exact check of GPU batches against the oracle without the feature matrix: the oracle
+    presamples and fills on the same graph, samples the same seeds, and X rows are compared with
+    synth.feat_fn (the closed form the features were generated from) on a random row sample."""
+    import oracle
+    B, fan = cfg.batch, cfg.fanouts
+    pre = synth.presample_seeds(ip, npre, B)
+    nv, ec = oracle.presample(ip, ix, pre, B, fan, synth.PRESAMPLE_SEED)
+    R, cl, co, ac = oracle.adj_fill(ip, ix, ec, c_adj)
+    del co, ac, ec
+    slot, _ = oracle.feat_fill(nv, c_feat // (4 * cfg.pitch_floats()))
+    ok = True
+    rng = np.random.default_rng(0)
+    for seeds, g in gpu_results:
+        o = oracle.sample_batch(ip, R, seeds, fan, synth.SAMPLE_SEED, 0, cl)
+        fh = int((slot[o.F] >= 0).sum())
+        ok &= bool(np.array_equal(g["F"], o.F)
+                   and all(np.array_equal(g["bsrc"][h], o.bsrc[h]) and np.array_equal(g["bptr"][h], o.bptr[h])
+                           for h in range(len(fan)))
+                   and g["counters"][:2].tolist() == o.counters[:2].tolist()
+                   and g["counters"][2:].tolist() == [fh, len(o.F) - fh])
+        idx = rng.choice(len(o.F), size=min(rows, len(o.F)), replace=False)
+        ok &= bool(np.array_equal(g["X"][idx], synth.feat_fn(o.F[idx][:, None], np.arange(cfg.D)[None, :])))
+    return {"batches": len(gpu_results), "bit_exact": ok,
+            "mode": f"light: oracle presample+fill+sampling on the full graph, X on {rows} random rows per batch "
+                    "vs the closed-form features"}
+
+
 def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_results=None, npre=8):
     """Time the oracle as it stands on host cores: its own presample + fill (reported), then
     inference batches spread over `threads` threads (ctypes releases the GIL), until about
@@ -489,6 +520,13 @@ def run_ours(args):
                   "c_adj": c_adj, "c_feat": c_feat, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
                   "e2e_ms_per_step": ems / args.steps, "host_enqueue_ms_per_step": host_s * 1e3 / args.steps},
     }
+    if not args.profile_only and world == 1 and args.check_light:
+        gpu_results = []
+        for b in batches[:2]:
+            o = dci.BatchOut(ctx, B, fan)
+            dci.sample_gather(ctx, wss[0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
+            gpu_results.append((b, o.result()))
+        line["parity_check"] = light_check(cfg, ip, ix, c_adj, c_feat, gpu_results, npre=args.presample_batches)
     if not args.profile_only and world == 1 and not args.no_cpu_baseline:
         gpu_results = None
         if not args.no_check:
