@@ -1,4 +1,4 @@
-"""DCI oracle — ctypes wrapper around ``oracle/liboracle.so`` (``dci_oracle.cpp``).
+"""DCI oracle — ctypes wrapper around ``oracle/liboracle.so`` (``dci_oracle.c``, plain C11).
 
 TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 ``cpu_baseline`` / ``--impl reference`` legs may import this package.  The product package
@@ -16,7 +16,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "dci_oracle.cpp")
+_SRC = os.path.join(_HERE, "dci_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 OK, EINVAL, ESEED, EDUP, ECAP = 0, -1, -2, -3, -4
@@ -29,9 +29,9 @@ _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with g++ (plain -O2, no fast-math)."""
+    """Compile the oracle with gcc (plain C11, -O2, no fast-math)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", _LIB_PATH, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", _LIB_PATH, _SRC])
     return _LIB_PATH
 
 
