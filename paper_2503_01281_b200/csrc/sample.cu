@@ -5,6 +5,7 @@
 // from device memory, so a batch never synchronises the host.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "dci_internal.cuh"
@@ -505,13 +506,25 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cuda
     const char* e = getenv("DCI_SAMPLE_BPS");
     return e ? atoi(e) : 8;
   }();
-  // sub-warp group width: next power of two >= f
-  auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };
+  // Grid: persistent (SM count x resident blocks), but no larger than the worst-case frontier of
+  // this hop needs (small frontiers would otherwise start hundreds of idle blocks); the fused
+  // relabel of hop h-1 (|F_{h-1}| * f_{h-1} items) is covered by the grid-stride loops either way.
+  const int64_t cap = std::max<int64_t>(ws->hop_cap[p.hop], 1);
+  auto sized = [&](int persistent, int64_t nodes_per_block) {
+    const int64_t need = (cap + nodes_per_block - 1) / nodes_per_block;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(persistent, need));
+  };
+  int gsz = 1;
+  while (gsz < p.f) gsz <<= 1;
+  auto go = [&](auto kern) {
+    kern<<<sized(persistent_grid(ctx, kern, 256, bps), 256 / gsz), 256, 0, s>>>(a);
+  };
   if (p.f > 32) {
     int fp2 = 1;
     while (fp2 < p.f) fp2 <<= 1;
     const size_t smem = (size_t)kWideWarps * fp2 * sizeof(int32_t);
-    k_sample_hop_wide<<<persistent_grid(ctx, k_sample_hop_wide, 32 * kWideWarps, 16), 32 * kWideWarps, smem, s>>>(a);
+    k_sample_hop_wide<<<sized(persistent_grid(ctx, k_sample_hop_wide, 32 * kWideWarps, 16), kWideWarps),
+                        32 * kWideWarps, smem, s>>>(a);
   } else if (p.f <= 1)
     go(k_sample_hop<1>);
   else if (p.f <= 2)
