@@ -263,6 +263,18 @@ class BatchOut:
         s.counters = self.counters.data_ptr()
         s.status = self.status.data_ptr()
         self.struct = s
+        self._streams = set()
+
+    def record_stream(self, stream):
+        """Once per stream: the caching allocator then waits for all work queued on `stream`
+        before recycling these buffers, even if this BatchOut is dropped mid-flight."""
+        key = stream.cuda_stream
+        if key in self._streams:
+            return
+        for t in [self.frontier, self.sizes, self.counters, self.status, self.X] + self.bptr + self.bsrc:
+            if t is not None:
+                t.record_stream(stream)
+        self._streams.add(key)
 
     def result(self):
         """Synchronise and return host copies trimmed to the batch's actual sizes."""
@@ -285,19 +297,34 @@ class BatchOut:
         return out
 
 
+def _record(tensor, stream):
+    """The batch reads `tensor` asynchronously on `stream`: tell torch's caching allocator, so a
+    tensor the caller drops is not handed to another allocation before the batch has run."""
+    if stream is not None and tensor.is_cuda:
+        tensor.record_stream(stream)
+
+
 def sample_gather(ctx: Context, ws: Workspace, seeds, fanouts, seed: int, out: BatchOut, stream=None):
     """dci_sample_gather (S5-S8), asynchronous on `stream` (default: torch current stream).
     seeds: int32 CUDA tensor on ctx.device."""
+    import torch
     fan = np.ascontiguousarray(fanouts, np.int32)
+    st = torch.cuda.current_stream() if stream is None else stream
+    _record(seeds, st)
+    out.record_stream(st)
     _check(lib().dci_sample_gather(ctx.handle, ws.handle, seeds.data_ptr(), int(seeds.numel()), _np_ptr(fan),
-                                   len(fan), seed, C.byref(out.struct), _stream_ptr(stream)), "dci_sample_gather")
+                                   len(fan), seed, C.byref(out.struct), st.cuda_stream), "dci_sample_gather")
 
 
 def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: int, out: BatchOut, sizes_host,
                        counters_host, status_host, stream=None):
     """dci_sample_gather_host: seeds from (pinned) host memory; sizes/counters/status copied back
-    to host buffers (pinned torch tensors) on the same stream."""
+    to host buffers (pinned torch tensors) on the same stream.  The host tensors must stay alive
+    until the stream has been synchronised (the copies are asynchronous)."""
+    import torch
     fan = np.ascontiguousarray(fanouts, np.int32)
+    if stream is not None:
+        out.record_stream(stream)
     _check(lib().dci_sample_gather_host(ctx.handle, ws.handle, seeds_host.data_ptr(), int(seeds_host.numel()),
                                         _np_ptr(fan), len(fan), seed, C.byref(out.struct),
                                         sizes_host.data_ptr(), counters_host.data_ptr(), status_host.data_ptr(),

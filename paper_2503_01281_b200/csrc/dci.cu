@@ -37,13 +37,17 @@ int occupancy_blocks(const void* kernel, int block, int cap) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
   std::lock_guard<std::mutex> lk(mu);
+  // cache the raw occupancy per kernel; the cap differs between calls
   auto it = cache.find(kernel);
-  if (it != cache.end()) return it->second;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, 0) != cudaSuccess || n < 1) n = 1;
-  n = std::min(n, cap);
-  cache[kernel] = n;
-  return n;
+  int n;
+  if (it != cache.end()) {
+    n = it->second;
+  } else {
+    n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, 0) != cudaSuccess || n < 1) n = 1;
+    cache[kernel] = n;
+  }
+  return std::min(n, cap);
 }
 
 namespace {
@@ -180,6 +184,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     const void* uidx;
     const void* fbases;
     int32_t G;
+    int32_t gather_bps;
   } sig;
   memset(&sig, 0, sizeof(sig));
   sig.L = L;
@@ -195,6 +200,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   sig.uidx = ctx->u_idx_cur;
   sig.fbases = ctx->d_fbases;
   sig.G = ctx->fpart_world;
+  sig.gather_bps = gather_blocks_per_sm(ctx);
   static_assert(sizeof(Sig) <= sizeof(ws->graph_sig), "signature buffer too small");
   const bool use_graph = graph_mode();
   // serial gathers: every batch's gather kernel goes through one context-wide stream, so
@@ -441,8 +447,16 @@ dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanou
   return DCI_OK;
 }
 
+static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* max_fanouts, int32_t L,
+                                   dci_workspace** out, bool user);
+
 dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* max_fanouts, int32_t L,
                                 dci_workspace** out) {
+  return workspace_create(ctx, max_batch, max_fanouts, L, out, true);
+}
+
+static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* max_fanouts, int32_t L,
+                                   dci_workspace** out, bool user) {
   if (!ctx || !out || max_batch < 1) return fail(DCI_EINVAL, "bad arguments");
   *out = nullptr;
   dci_status st = check_fanouts(max_fanouts, L);
@@ -502,6 +516,10 @@ dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* 
   cudaMemset(w->tile_state, 0, sizeof(unsigned long long) * w->tiles_cap);
   cudaMemset(w->scal, 0, sizeof(BatchScalars));
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "workspace init");
+  if (user) {
+    w->live_ws = ctx->live_ws;
+    ++*w->live_ws;
+  }
   *out = w;
   return DCI_OK;
 }
@@ -527,6 +545,7 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
   if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
   for (int i = 0; i < 2; ++i)
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
+  if (w->live_ws) --*w->live_ws;
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   delete w;
   return DCI_OK;
@@ -585,7 +604,7 @@ dci_status dci_presample(dci_ctx* ctx, const int32_t* seeds, int64_t num_seeds, 
     ctx->pre_ws = nullptr;
     if (ctx->pre_out_mem) cudaFree(ctx->pre_out_mem);
     ctx->pre_out_mem = nullptr;
-    st = dci_workspace_create(ctx, B, fanouts, L, &ctx->pre_ws);
+    st = workspace_create(ctx, B, fanouts, L, &ctx->pre_ws, false);
     if (st != DCI_OK) return st;
     size_t bytes = 0;
     auto take = [&](size_t n) {

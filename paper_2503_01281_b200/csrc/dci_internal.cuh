@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <memory>
 #include <string>
 
 #include "../../include/dci.h"
@@ -88,6 +90,9 @@ struct dci_ctx {
   uint64_t presample_peak = 0;
   uint64_t launches = 0;
   cudaStream_t gstream = nullptr;  // shared gather stream (serial-gather mode)
+  // live user workspaces (= batches the caller keeps in flight); shared with the workspaces so
+  // either may be destroyed first
+  std::shared_ptr<std::atomic<int>> live_ws = std::make_shared<std::atomic<int>>(0);
   // lazily created presample workspace + outputs
   dci_workspace* pre_ws = nullptr;
   int32_t pre_B = 0;
@@ -99,6 +104,7 @@ struct dci_ctx {
 
 struct dci_workspace {
   dci_ctx* ctx = nullptr;
+  std::shared_ptr<std::atomic<int>> live_ws;  // set for user workspaces (not the presample one)
   int device = 0;  // own copy: destroying a workspace never dereferences its context
   int32_t max_batch = 0;
   int32_t L = 0;
@@ -176,6 +182,9 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cuda
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
 void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
+// Gather blocks per SM: the HBM-bound gather is given a small share of each SM when many
+// batches are in flight (their sampling kernels must co-reside), the whole SM when one is.
+int gather_blocks_per_sm(const dci_ctx* ctx);
 
 // aggregate.cu
 dci_status launch_block_aggregate(dci_ctx* ctx, const int32_t* bptr, const int32_t* bsrc, const int64_t* n_dst,

@@ -186,6 +186,17 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 
 }  // namespace
 
+int gather_blocks_per_sm(const dci_ctx* ctx) {
+  static const int forced = [] {
+    const char* e = getenv("DCI_GATHER_BPS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return forced;
+  // measured on M2: 1 batch in flight -> 4, 2-3 -> 2, >= 4 -> 1
+  const int w = ctx->live_ws->load();
+  return w <= 1 ? 4 : (w <= 3 ? 2 : 1);
+}
+
 void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s) {
   FusedArgs a;
@@ -214,12 +225,7 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
   a.out_sizes = out->sizes;
   a.out_counters = out->counters;
   a.out_status = out->status;
-  // Blocks per SM for the gather: a small cap leaves registers / warp slots for the
-  // sampling kernels of other in-flight batches (the gather is HBM-bound, not occupancy-bound).
-  static int bps = [] {
-    const char* e = getenv("DCI_GATHER_BPS");
-    return e ? atoi(e) : 1;
-  }();
+  const int bps = gather_blocks_per_sm(ctx);
   auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };
   const bool vec = out->X && (out->ldx % 4 == 0) && out->ldx >= ctx->pitch &&
                    (reinterpret_cast<uintptr_t>(out->X) % 16 == 0);

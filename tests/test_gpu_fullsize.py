@@ -65,13 +65,13 @@ def _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_f
     streams = [torch.cuda.Stream() for _ in range(inflight)]
     outs = [dci.BatchOut(ctx, B, fan) for _ in range(inflight)]
     batches = synth.inference_batches(ip, B)[:nbatches]
+    seeds_dev = [torch.from_numpy(b).to(DEV) for b in batches]  # alive while batches are in flight
     results = []
     for i, seeds in enumerate(batches):
         w = i % inflight
         if i >= inflight:
             results.append(outs[w].result())
-        dci.sample_gather(ctx, wss[w], torch.from_numpy(seeds).to(DEV), fan, synth.SAMPLE_SEED, outs[w],
-                          stream=streams[w])
+        dci.sample_gather(ctx, wss[w], seeds_dev[i], fan, synth.SAMPLE_SEED, outs[w], stream=streams[w])
     torch.cuda.synchronize()
     for i in range(max(0, len(batches) - inflight), len(batches)):
         results.append(outs[i % inflight].result())

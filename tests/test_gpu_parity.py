@@ -303,3 +303,21 @@ def test_wide_fanout_parity(fan):
         g = _run(ctx, ws, seeds, fan, 21)
         o = oracle.sample_gather(ip, R, ft, seeds, fan, 21, cl, slot_o)
         _assert_batch_equal(g, o, len(fan))
+
+
+def test_dropped_seed_tensors_on_several_streams(small):
+    """Seeds uploaded per call and dropped right away while batches run on other streams: the
+    binding records the stream on the tensor, so torch's allocator cannot recycle the memory
+    under an unfinished batch (this raced before)."""
+    ip, ix, ft, ctx = small
+    fan = (10, 5)
+    B = 128
+    batches = synth.inference_batches(ip, B)[:12]
+    wss = [dci.workspace_create(ctx, B, fan) for _ in range(4)]
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [dci.BatchOut(ctx, B, fan) for _ in range(12)]
+    for i, seeds in enumerate(batches):
+        dci.sample_gather(ctx, wss[i % 4], torch.from_numpy(seeds).to(DEV), fan, 13, outs[i], stream=streams[i % 4])
+    torch.cuda.synchronize()
+    for seeds, out in zip(batches, outs):
+        _assert_batch_equal(out.result(), oracle.sample_gather(ip, ix, ft, seeds, fan, 13), 2)
