@@ -344,9 +344,12 @@ def mean_aggregate(ctx: Context, out: BatchOut, hop: int | None = None, H=None, 
     rows = out.bptr[hop].numel() - 1
     if H is None:
         H = torch.empty((max(rows, 1), out.ldx), dtype=torch.float32, device=out.X.device)
+    st = torch.cuda.current_stream() if stream is None else stream
+    out.record_stream(st)
+    _record(H, st)
     _check(lib().dci_block_aggregate(ctx.handle, out.bptr[hop].data_ptr(), out.bsrc[hop].data_ptr(),
                                      out.sizes.data_ptr() + 8 * hop, out.X.data_ptr(), out.ldx, out.D,
-                                     H.data_ptr(), H.shape[1], {"mean": 0, "sum": 1}[op], _stream_ptr(stream)),
+                                     H.data_ptr(), H.shape[1], {"mean": 0, "sum": 1}[op], st.cuda_stream),
            "dci_block_aggregate")
     return H
 
