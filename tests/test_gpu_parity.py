@@ -321,3 +321,49 @@ def test_dropped_seed_tensors_on_several_streams(small):
     torch.cuda.synchronize()
     for seeds, out in zip(batches, outs):
         _assert_batch_equal(out.result(), oracle.sample_gather(ip, ix, ft, seeds, fan, 13), 2)
+
+
+@pytest.mark.parametrize("case", ["L8", "N1_E0", "selfloops", "wide_rows", "wide_rows_odd"])
+def test_edge_shapes(case):
+    """Shapes at the ABI's limits: 8 hops, a 1-node graph without edges, self-loops only, and
+    rows far wider than one warp pass (D = 1500 / 4099) through gather and aggregation."""
+    rng = np.random.default_rng(3)
+    if case == "L8":
+        ip, ix, ft = _graph(3000, 20000, 5, 6)
+        fan, seeds = (2, 2, 2, 2, 2, 2, 2, 2), synth.inference_batches(ip, 5)[0]
+    elif case == "N1_E0":
+        ip, ix, ft = np.array([0, 0], np.int64), np.zeros(0, np.int32), synth.features(1, 3).numpy()
+        fan, seeds = (4, 4), np.array([0], np.int32)
+    elif case == "selfloops":
+        N = 50
+        ip = np.arange(N + 1, dtype=np.int64) * 2
+        ix = np.repeat(np.arange(N, dtype=np.int32), 2)
+        ft, fan, seeds = synth.features(N, 7).numpy(), (3, 1), np.array([4, 9, 0], np.int32)
+    else:
+        D = 1500 if case == "wide_rows" else 4099
+        ip, ix, ft = _graph(2000, 16000, 8, D)
+        fan, seeds = (6, 3), synth.inference_batches(ip, 40)[0]
+    ctx = dci.load_graph(ip, ix, ft)
+    ws = dci.workspace_create(ctx, max(len(seeds), 1), fan)
+    out = dci.BatchOut(ctx, len(seeds), fan)
+    dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(DEV), fan, 3, out)
+    H = dci.mean_aggregate(ctx, out)
+    g = out.result()
+    o = oracle.sample_gather(ip, ix, ft, seeds, fan, 3)
+    _assert_batch_equal(g, o, len(fan))
+    L = len(fan)
+    Hr = oracle.mean_aggregate(o.bptr[L - 1], o.bsrc[L - 1], o.X)
+    Hg = H[: len(o.bptr[L - 1]) - 1, : ft.shape[1]].cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(Hg - Hr) <= _agg_tol(o.bptr[L - 1], o.X, Hr))
+    # and with a fill (C = everything) on the same context
+    nv = torch.zeros(len(ip) - 1, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(max(len(ix), 1), dtype=torch.int32, device=DEV)
+    dci.presample(ctx, torch.from_numpy(seeds).to(DEV), max(len(seeds), 1), fan, 1, nv, ec)
+    big = 4 * len(ix) + 4 * ((ft.shape[1] + 3) // 4 * 4) * (len(ip) - 1) + 64
+    dci.fill(ctx, nv, ec, big // 2, big)
+    nv_o, ec_o = oracle.presample(ip, ix, seeds, max(len(seeds), 1), fan, 1)
+    R, cl, _, _ = oracle.adj_fill(ip, ix, ec_o, big // 2)
+    slot_o, _ = oracle.feat_fill(nv_o, big // (4 * ((ft.shape[1] + 3) // 4 * 4)))
+    out2 = dci.BatchOut(ctx, len(seeds), fan)
+    dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(DEV), fan, 3, out2)
+    _assert_batch_equal(out2.result(), oracle.sample_gather(ip, R, ft, seeds, fan, 3, cl, slot_o), L)
