@@ -41,7 +41,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="M2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--inflight", type=int, default=6, help="workspaces/streams in flight")
+    ap.add_argument("--inflight", type=int, default=3,
+                    help="streams in flight (each with one batch, or one group of --group batches)")
+    ap.add_argument("--group", type=int, default=6,
+                    help="batches per dci_sample_gather_many call (one TMA gather launch per group); 0 = one "
+                         "dci_sample_gather per batch")
     ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
     ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
     ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
@@ -361,22 +365,34 @@ def run_ours(args):
     batches = [b for b in batches if len(b) == B] or batches
     seeds_dev = [torch.from_numpy(b).to(dev) for b in batches]
     nws = max(1, args.inflight)
-    wss = [dci.workspace_create(ctx, B, fan) for _ in range(nws)]
-    outs = [dci.BatchOut(ctx, B, fan) for _ in range(nws)]
+    G = max(0, args.group)
+    per = max(1, G)  # batches per call
+    wss = [[dci.workspace_create(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
+    outs = [[dci.BatchOut(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(nws)]
-    for w in wss:
-        w.set_profiling(True)
-    nsteps_total = args.warmup + args.steps
+    for wl in wss:
+        for w in wl:
+            w.set_profiling(True)
+    # whole calls: K batches -> ceil(K / per) calls (K is reported as the batches actually timed)
+    n_warm = -(-args.warmup // per)
+    n_calls = -(-args.steps // per)
+    steps_eff = n_calls * per
+    nsteps_total = n_warm + n_calls
 
     def step(i):
         w = i % nws
-        dci.sample_gather(ctx, wss[w], seeds_dev[i % len(seeds_dev)], fan, synth.SAMPLE_SEED, outs[w],
-                          stream=streams[w])
+        if G:
+            sd = [seeds_dev[(i * per + j) % len(seeds_dev)] for j in range(per)]
+            dci.sample_gather_many(ctx, wss[w], sd, fan, synth.SAMPLE_SEED, outs[w], stream=streams[w])
+        else:
+            dci.sample_gather(ctx, wss[w][0], seeds_dev[i % len(seeds_dev)], fan, synth.SAMPLE_SEED, outs[w][0],
+                              stream=streams[w])
 
-    for i in range(args.warmup):
+    for i in range(n_warm):
         step(i)
     torch.cuda.synchronize()
-    for w in wss:
+    all_ws = [w for wl in wss for w in wl]
+    for w in all_ws:
         w.stats(reset=True)
     parallel.barrier(local)
     torch.cuda.synchronize()
@@ -389,7 +405,7 @@ def run_ours(args):
     for s in streams:
         s.wait_event(ev_start)
     h0 = time.perf_counter()
-    for i in range(args.warmup, nsteps_total):
+    for i in range(n_warm, nsteps_total):
         step(i)
     host_s = time.perf_counter() - h0
     for s in streams:
@@ -403,39 +419,47 @@ def run_ours(args):
     ms_local = ev_start.elapsed_time(ev_end)
     parallel.barrier(local)
     ms = parallel.max_over_ranks(ms_local, device=dev)
-    sts = [w.stats(reset=True) for w in wss]
+    sts = [w.stats(reset=True) for w in all_ws]
     D = cfg.D
     rows = sum(st["frontier_rows"] for st in sts)
     cn = np.sum([st["counters"] for st in sts], axis=0).astype(np.float64)
     g_ms = sum(st["gather_ms"] for st in sts)
     s_ms = sum(st["sample_ms"] for st in sts)
     n_timed = sum(st["timed_batches"] for st in sts)
-    alg_bytes = rows * (8.0 * D + 4.0)  # per gather launch: read row + write row + 4 B slot lookup
+    n_glaunch = sum(st["gather_launches"] for st in sts)
+    rows_read = sum(st["rows_read"] for st in sts)
+    # the library's algorithmic gather bytes: row reads + row writes + lookups
+    alg_bytes = float(sum(st["gather_bytes"] for st in sts))
     tot = parallel.sum_over_ranks([sum(st["seeds"] for st in sts), launches, rows, alg_bytes, g_ms, s_ms, n_timed,
-                                   *cn.tolist()], device=dev)
+                                   n_glaunch, rows_read, *cn.tolist()], device=dev)
     seeds_all = tot[0]
     value = seeds_all / (ms / 1e3)
-    cn = tot[7:11]
+    cn = tot[9:13]
     hit_rates = {"adj_hit_rate": cn[0] / max(1, cn[0] + cn[1]), "feat_hit_rate": cn[2] / max(1, cn[2] + cn[3]),
                  "adj_accesses_per_seed": (cn[0] + cn[1]) / max(1, seeds_all)}
     if args.profile_only:
         clk.stop()
-        print(json.dumps({"profile_only": True, "value": value, "ms_per_step": ms / args.steps, **hit_rates}))
+        print(json.dumps({"profile_only": True, "value": value, "ms_per_step": ms / steps_eff, **hit_rates}))
         return
     # ---- e2e: the same steps through the C-ABI with host seeds + D2H results ----
     pinned_seeds = [torch.from_numpy(b).pin_memory() for b in batches]
-    e_sizes = torch.zeros((nws, L + 1), dtype=torch.int64).pin_memory()
-    e_cnt = torch.zeros((nws, 4), dtype=torch.int64).pin_memory()
-    e_st = torch.zeros((nws, 1), dtype=torch.int32).pin_memory()
-    for w in wss:
+    e_sizes = torch.zeros((nws, per, L + 1), dtype=torch.int64).pin_memory()
+    e_cnt = torch.zeros((nws, per, 4), dtype=torch.int64).pin_memory()
+    e_st = torch.zeros((nws, per), dtype=torch.int32).pin_memory()
+    for w in all_ws:
         w.set_profiling(False)
 
     def estep(i):
         w = i % nws
-        dci.sample_gather_host(ctx, wss[w], pinned_seeds[i % len(pinned_seeds)], fan, synth.SAMPLE_SEED, outs[w],
-                               e_sizes[w], e_cnt[w], e_st[w], stream=streams[w])
+        if G:
+            sd = [pinned_seeds[(i * per + j) % len(pinned_seeds)] for j in range(per)]
+            dci.sample_gather_many_host(ctx, wss[w], sd, fan, synth.SAMPLE_SEED, outs[w], e_sizes[w], e_cnt[w],
+                                        e_st[w], stream=streams[w])
+        else:
+            dci.sample_gather_host(ctx, wss[w][0], pinned_seeds[i % len(pinned_seeds)], fan, synth.SAMPLE_SEED,
+                                   outs[w][0], e_sizes[w, 0], e_cnt[w, 0], e_st[w, 0], stream=streams[w])
 
-    for i in range(args.warmup):
+    for i in range(n_warm):
         estep(i)
     torch.cuda.synchronize()
     parallel.barrier(local)
@@ -444,7 +468,7 @@ def run_ours(args):
     e0.record(main)
     for s in streams:
         s.wait_event(e0)
-    for i in range(args.warmup, nsteps_total):
+    for i in range(n_warm, nsteps_total):
         estep(i)
     for s in streams:
         e = torch.cuda.Event()
@@ -467,34 +491,41 @@ def run_ours(args):
     # slot lookup) vs the host link (miss rows read through UVA).
     host_peak, host_req_peak, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats())
     hits_rows, miss_rows = cn[2], cn[3]
-    hbm_b = hits_rows * 4.0 * D + (hits_rows + miss_rows) * (4.0 * D + 4.0)
-    host_b = miss_rows * 4.0 * D
+    # rows actually read: a node-sweep group reads each row once for all its batches; misses
+    # among them are apportioned by the batches' miss fraction
+    frac_read = tot[8] / max(1.0, tot[2])
+    host_b = miss_rows * frac_read * 4.0 * D
+    hbm_b = tot[3] - host_b
     host_bound = host_b / host_peak > hbm_b / hbm_peak
     bind_b = host_b if host_bound else hbm_b
     bind_peak = host_peak if host_bound else hbm_peak
-    achieved_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per-launch (live events)
+    n_launch = max(1.0, tot[7])
+    achieved_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per launch (live events)
+    kernel = ("k_gather_tma (group of %d: %s; route + feature gather, S7-S8)"
+              % (G, "node sweep, each row read once per group" if frac_read < 0.999 else "rows")) if G else \
+        "k_gather (fused route + relabel + feature gather, S7-S8)"
     aggregate_gbs = bind_b / (ms / 1e3) / 1e9  # all gather launches over the timed wall time
     host_link = {"feature_miss_GBps": host_b / (ms / 1e3) / 1e9, "peak_GBps": host_peak,
                  "feature_frac": host_b / (ms / 1e3) / 1e9 / host_peak,
                  "adj_miss_Mreads_per_s": cn[1] / (ms / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
                  "peak_kind": host_kind}
-    avg_fl = tot[2] / max(1, args.steps * world)
+    avg_fl = tot[2] / max(1, steps_eff * world)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gather_traffic.json")
     if os.path.exists(tfile):
-        tj = json.load(open(tfile)).get(cfg.name)
-        if tj:
-            traffic = tj.get("dram_bytes_per_row", 0) * avg_fl or None
+        tj = json.load(open(tfile)).get(f"{cfg.name}/group{G}")
+        if tj:  # ncu dram bytes per launch of this kernel and configuration
+            traffic = tj.get("dram_bytes_per_launch")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps_eff,
+        "warmup": n_warm * per, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
         "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B, "fanouts": list(fan),
                    "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
                    "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
                                                     if args.partitioned and world > 1 else "replicated caches") + ")",
-                   "inflight": nws,
+                   "inflight": nws, "group": G,
                    "l2": "inputs larger than L2 (feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
                          % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
                             avg_fl * D * 4 / 1e6)},
@@ -502,39 +533,44 @@ def run_ours(args):
                 "d2h_bytes_per_step": 8 * (L + 1) + 8 * 4 + 4},
         "gpu_launches": int(tot[1]),
         "roofline": {"bound": "host-link" if host_bound else "hbm",
-                     "kernel": "k_gather (fused route + relabel + feature gather, S7-S8)",
+                     "kernel": kernel,
                      "achieved": achieved_gbs, "peak": bind_peak,
                      "peak_kind": host_kind if host_bound else peak_kind, "unit": "GB/s",
                      "frac": (achieved_gbs / bind_peak) if achieved_gbs else None, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": bind_b / max(1, tot[6]),
-                     "avg_gather_ms": tot[4] / max(1, tot[6]), "avg_sample_ms": tot[5] / max(1, tot[6]),
-                     "concurrent_batches": (tot[4] + tot[5]) / ms if ms > 0 else None,
+                     "algorithmic_bytes_per_launch": bind_b / n_launch, "launches": int(tot[7]),
+                     "avg_gather_ms": tot[4] / n_launch, "avg_sample_ms": tot[5] / max(1, tot[6]),
+                     "rows_read_per_row": frac_read,
+                     "gather_busy_frac": tot[4] / ms if ms > 0 else None,
                      "aggregate_achieved": aggregate_gbs, "aggregate_frac": aggregate_gbs / bind_peak,
-                     "note": "achieved = algorithmic bytes per launch / mean live launch time (CUDA events on the "
-                             "launch stream); with several batches in flight launches overlap, so "
-                             "aggregate_achieved = all gather bytes / timed wall time is the device-level rate"},
+                     "note": "achieved = algorithmic bytes per gather launch / mean live launch time (CUDA events "
+                             "on the launch stream); group gathers run one at a time on the gather stream. "
+                             "aggregate_achieved = the same bytes / timed wall time"},
         "host_link": host_link,
         "clocks": clocks,
         "stats": {"avg_F_L": avg_fl, "F_L_per_seed": avg_fl / B, **hit_rates,
                   "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre, "fill": t_fill},
                   "c_adj": c_adj, "c_feat": c_feat, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
-                  "e2e_ms_per_step": ems / args.steps, "host_enqueue_ms_per_step": host_s * 1e3 / args.steps},
+                  "e2e_ms_per_step": ems / steps_eff, "host_enqueue_ms_per_step": host_s * 1e3 / steps_eff},
     }
+    def check_batches():
+        """Two full-size batches through the same call the timed region used (group or single)."""
+        bs = batches[:2]
+        os_ = [dci.BatchOut(ctx, B, fan) for _ in bs]
+        if G >= 2:
+            dci.sample_gather_many(ctx, wss[0][:2], [torch.from_numpy(b).to(dev) for b in bs], fan, synth.SAMPLE_SEED,
+                                   os_)
+        else:
+            for b, o in zip(bs, os_):
+                dci.sample_gather(ctx, wss[0][0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
+        return [(b, o.result()) for b, o in zip(bs, os_)]
+
     if not args.profile_only and world == 1 and args.check_light:
-        gpu_results = []
-        for b in batches[:2]:
-            o = dci.BatchOut(ctx, B, fan)
-            dci.sample_gather(ctx, wss[0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
-            gpu_results.append((b, o.result()))
+        gpu_results = check_batches()
         line["parity_check"] = light_check(cfg, ip, ix, c_adj, c_feat, gpu_results, npre=args.presample_batches)
     if not args.profile_only and world == 1 and not args.no_cpu_baseline:
         gpu_results = None
         if not args.no_check:
-            gpu_results = []
-            for b in batches[:2]:
-                o = dci.BatchOut(ctx, B, fan)
-                dci.sample_gather(ctx, wss[0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
-                gpu_results.append((b, o.result()))
+            gpu_results = check_batches()
         res, check = oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, args.cpu_seconds, os.cpu_count() or 1,
                                 gpu_results, npre=args.presample_batches)
         line["cpu_baseline"] = res

@@ -29,6 +29,7 @@ extern "C" {
 
 #define DCI_VERSION 100          /* 1.0.0 */
 #define DCI_MAX_LAYERS 8         /* L <= 8 hops */
+#define DCI_MAX_GROUP 16          /* batches per dci_sample_gather_many call */
 #define DCI_MAX_FANOUT 1024      /* per-hop fan-out 1..1024 (<= 32: registers, else shared memory) */
 
 typedef enum dci_status {
@@ -134,6 +135,30 @@ dci_status dci_workspace_destroy(dci_workspace* ws);
 dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B,
                              const int32_t* fanouts, int32_t L, uint64_t seed, const dci_batch_out* out,
                              void* stream);
+
+/* --------------------------------------------------------------------------------------
+ * dci_sample_gather_many — the same S5..S8 for a group of n batches (1 <= n <= DCI_MAX_GROUP),
+ * one workspace and one dci_batch_out per batch (distinct workspaces).  Batch i samples seeds[i]
+ * (device int32[B[i]]) on its workspace's own stream, all i concurrently; then ONE feature-gather
+ * launch (Blackwell bulk copies, cp.async.bulk, through a shared-memory ring) moves the rows of
+ * every batch, on the context's gather stream, so group gathers run one at a time at full
+ * bandwidth while the next group samples.  Results are identical to n dci_sample_gather calls
+ * (O-6, O-7).  Asynchronous on `stream`: work enqueued on `stream` before the call happens before
+ * the group, and work enqueued after it sees every output.  If an output cannot take bulk stores
+ * (X NULL, ldx % 4 != 0 or X not 16-byte aligned) the batches run one by one on `stream`.
+ * Errors: as dci_sample_gather per batch; DCI_EINVAL for n out of range or a repeated workspace.
+ * ------------------------------------------------------------------------------------ */
+dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const* ws, const int32_t* const* seeds,
+                                  const int32_t* B, const int32_t* fanouts, int32_t L, uint64_t seed,
+                                  const dci_batch_out* outs, void* stream);
+
+/* End-to-end group variant: seeds_host[i] HOST int32[B[i]] (pinned for overlap) copied to the
+ * workspaces' staging buffers on `stream`, then dci_sample_gather_many, then device->host copies
+ * of sizes (int64[n][L+1]), counters (uint64[n][4]) and status (int32[n]) on `stream`. */
+dci_status dci_sample_gather_many_host(dci_ctx* ctx, int32_t n, dci_workspace* const* ws,
+                                       const int32_t* const* seeds_host, const int32_t* B, const int32_t* fanouts,
+                                       int32_t L, uint64_t seed, const dci_batch_out* outs, int64_t* sizes_host,
+                                       uint64_t* counters_host, int32_t* status_host, void* stream);
 
 /* End-to-end variant: seeds_host is HOST memory (pinned for full overlap); the call
  * enqueues the host->device copy of the seeds, the batch, and device->host copies of
@@ -249,17 +274,20 @@ dci_status dci_cache_state(dci_ctx* ctx, int32_t* cached_len, int64_t* cache_off
                            int32_t* acache, float* fcache, int32_t* indices_cur);
 
 /* Stage times of the workspace's last batch, in ms (CUDA events recorded on the launch
- * stream around the sampling hops and around the gather; requires profiling on).  With
- * profiling on, dci_sample_gather first waits (host) for the previous batch of the same
- * workspace to finish so its stage times can be accumulated (see dci_workspace_stats). */
+ * streams around the sampling hops and around the gather launch; requires profiling on).
+ * Timing uses a ring of event records per workspace, so it never blocks the host. */
 dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on);
 dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms);
 
 /* Running totals of a workspace since its last reset (synchronises the device):
  * batches finished, seeds, sum of |F_L| (feature rows gathered), summed counters, and -
- * with profiling on - the number of event-timed batches and their summed stage times
- * (sampling hops S5-S6; the fused route+gather kernel S7-S8), in ms.  reset != 0 zeroes
- * the totals after reading them. */
+ * with profiling on - the number of event-timed batches and their summed sampling time
+ * (hops S5-S6), the number of timed gather launches and their summed time (S7-S8; a
+ * dci_sample_gather_many group has ONE launch, booked on its first workspace), in ms.
+ * rows_read: feature rows the gather actually read (a node-sweep group reads each row once
+ * for all its batches); gather_bytes: the gather's algorithmic bytes (row
+ * reads + row writes + lookups), also booked on a group's first workspace.
+ * reset != 0 zeroes the totals after reading them. */
 typedef struct dci_ws_stats {
   uint64_t batches;
   uint64_t seeds;
@@ -268,6 +296,9 @@ typedef struct dci_ws_stats {
   uint64_t timed_batches;
   double sample_ms;
   double gather_ms;
+  uint64_t gather_launches;
+  uint64_t rows_read;
+  uint64_t gather_bytes;
 } dci_ws_stats;
 
 dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset);

@@ -28,7 +28,8 @@ STATUS = {0: "DCI_OK", 1: "DCI_EINVAL", 2: "DCI_ESTATE", 3: "DCI_ECUDA", 4: "DCI
 OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
-            "dci_sample_gather", "dci_sample_gather_host", "dci_presample", "dci_allocate", "dci_fill",
+            "dci_sample_gather", "dci_sample_gather_host", "dci_sample_gather_many", "dci_sample_gather_many_host",
+            "dci_presample", "dci_allocate", "dci_fill",
             "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
             "dci_workspace_stats", "dci_mean_aggregate", "dci_block_aggregate", "dci_fill_partitioned", "dci_fill_knapsack", "dci_feature_partition_handle",
             "dci_attach_feature_partitions", "dci_launch_count", "dci_last_error", "dci_version"]
@@ -51,7 +52,8 @@ class dci_batch_out(C.Structure):
 class dci_ws_stats(C.Structure):
     _fields_ = [("batches", C.c_uint64), ("seeds", C.c_uint64), ("frontier_rows", C.c_uint64),
                 ("counters", C.c_uint64 * 4), ("timed_batches", C.c_uint64), ("sample_ms", C.c_double),
-                ("gather_ms", C.c_double)]
+                ("gather_ms", C.c_double), ("gather_launches", C.c_uint64), ("rows_read", C.c_uint64),
+                ("gather_bytes", C.c_uint64)]
 
 
 class dci_cache_info(C.Structure):
@@ -81,6 +83,8 @@ def lib():
         "dci_workspace_destroy": [vp],
         "dci_sample_gather": [vp, vp, vp, i32, vp, i32, u64, C.POINTER(dci_batch_out), vp],
         "dci_sample_gather_host": [vp, vp, vp, i32, vp, i32, u64, C.POINTER(dci_batch_out), vp, vp, vp, vp],
+        "dci_sample_gather_many": [vp, i32, vp, vp, vp, vp, i32, u64, vp, vp],
+        "dci_sample_gather_many_host": [vp, i32, vp, vp, vp, vp, i32, u64, vp, vp, vp, vp, vp],
         "dci_presample": [vp, vp, i64, i32, vp, i32, u64, vp, vp, vp, vp, vp],
         "dci_allocate": [vp, u64, vp, vp, i32, i64, i64, C.POINTER(u64), C.POINTER(u64)],
         "dci_fill": [vp, vp, vp, u64, u64, vp],
@@ -220,7 +224,8 @@ class Workspace:
         _check(lib().dci_workspace_stats(self.handle, C.byref(st), 1 if reset else 0), "dci_workspace_stats")
         return {"batches": st.batches, "seeds": st.seeds, "frontier_rows": st.frontier_rows,
                 "counters": [int(c) for c in st.counters], "timed_batches": st.timed_batches,
-                "sample_ms": st.sample_ms, "gather_ms": st.gather_ms}
+                "sample_ms": st.sample_ms, "gather_ms": st.gather_ms, "gather_launches": st.gather_launches,
+                "rows_read": st.rows_read, "gather_bytes": st.gather_bytes}
 
     def stage_ms(self):
         s, g = C.c_float(), C.c_float()
@@ -314,6 +319,45 @@ def sample_gather(ctx: Context, ws: Workspace, seeds, fanouts, seed: int, out: B
     out.record_stream(st)
     _check(lib().dci_sample_gather(ctx.handle, ws.handle, seeds.data_ptr(), int(seeds.numel()), _np_ptr(fan),
                                    len(fan), seed, C.byref(out.struct), st.cuda_stream), "dci_sample_gather")
+
+
+def sample_gather_many(ctx: Context, wss, seeds_list, fanouts, seed: int, outs, stream=None):
+    """dci_sample_gather_many: n <= 16 batches (one workspace and one BatchOut each) sampled
+    concurrently and gathered by ONE TMA gather launch; asynchronous on `stream`."""
+    import torch
+    n = len(wss)
+    assert n == len(seeds_list) == len(outs)
+    fan = np.ascontiguousarray(fanouts, np.int32)
+    st = torch.cuda.current_stream() if stream is None else stream
+    for sd in seeds_list:
+        _record(sd, st)
+    for o in outs:
+        o.record_stream(st)
+    ws_arr = (C.c_void_p * n)(*[w.handle for w in wss])
+    sd_arr = (C.c_void_p * n)(*[sd.data_ptr() for sd in seeds_list])
+    b_arr = (C.c_int32 * n)(*[int(sd.numel()) for sd in seeds_list])
+    out_arr = (dci_batch_out * n)(*[o.struct for o in outs])
+    _check(lib().dci_sample_gather_many(ctx.handle, n, ws_arr, sd_arr, b_arr, _np_ptr(fan), len(fan), seed, out_arr,
+                                        st.cuda_stream), "dci_sample_gather_many")
+
+
+def sample_gather_many_host(ctx: Context, wss, seeds_host_list, fanouts, seed: int, outs, sizes_host,
+                            counters_host, status_host, stream=None):
+    """dci_sample_gather_many_host: host (pinned) seeds in, sizes [n, L+1] / counters [n, 4] /
+    status [n] (pinned torch tensors) copied back on `stream`; valid after synchronising it."""
+    n = len(wss)
+    fan = np.ascontiguousarray(fanouts, np.int32)
+    if stream is not None:
+        for o in outs:
+            o.record_stream(stream)
+    ws_arr = (C.c_void_p * n)(*[w.handle for w in wss])
+    sd_arr = (C.c_void_p * n)(*[sd.data_ptr() for sd in seeds_host_list])
+    b_arr = (C.c_int32 * n)(*[int(sd.numel()) for sd in seeds_host_list])
+    out_arr = (dci_batch_out * n)(*[o.struct for o in outs])
+    _check(lib().dci_sample_gather_many_host(ctx.handle, n, ws_arr, sd_arr, b_arr, _np_ptr(fan), len(fan), seed,
+                                             out_arr, sizes_host.data_ptr(), counters_host.data_ptr(),
+                                             status_host.data_ptr(), _stream_ptr(stream)),
+           "dci_sample_gather_many_host")
 
 
 def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: int, out: BatchOut, sizes_host,

@@ -80,6 +80,16 @@ bool gather_serial() {
   return mode == 1;
 }
 
+// TMA gather: DCI_GATHER_SERIAL=0 lets gathers of concurrent batches overlap (experiments)
+bool gather_concurrent() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("DCI_GATHER_SERIAL");
+    mode = (e && e[0] == '0') ? 1 : 0;
+  }
+  return mode == 1;
+}
+
 bool graph_mode() {
   static int mode = -1;
   if (mode < 0) {
@@ -119,10 +129,37 @@ dci_status check_fanouts(const int32_t* fanouts, int32_t L) {
   return DCI_OK;
 }
 
+// Fold a timing record into the workspace totals (waits for its last event).
+dci_status trec_fold(dci_workspace* ws, dci_workspace::TimeRec& r) {
+  if (r.state & 1) {
+    float ms = 0.f;
+    DCI_CUDA(cudaEventSynchronize(r.e[1]));
+    DCI_CUDA(cudaEventElapsedTime(&ms, r.e[0], r.e[1]));
+    ws->acc_sample_ms += ms;
+    ws->acc_timed += 1;
+  }
+  if (r.state & 2) {
+    float ms = 0.f;
+    DCI_CUDA(cudaEventSynchronize(r.e[3]));
+    DCI_CUDA(cudaEventElapsedTime(&ms, r.e[2], r.e[3]));
+    ws->acc_gather_ms += ms;
+    ws->acc_gather_launches += 1;
+  }
+  r.state = 0;
+  return DCI_OK;
+}
+
+// Advance to the workspace's next timing record, folding the one it reuses (issued kTimeRing
+// batches ago on this workspace, so normally long finished: no host stall).
+dci_status trec_begin(dci_workspace* ws) {
+  ws->trec_cur = (ws->trec_cur + 1) % dci_workspace::kTimeRing;
+  return trec_fold(ws, ws->trec[ws->trec_cur]);
+}
+
 // Enqueue one batch (shared by inference pass 0 and presample pass 1).
 dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, const int32_t* fanouts,
                      int32_t L, uint64_t seed, uint32_t pass, const dci_batch_out* out, int32_t* node_visits,
-                     int32_t* edge_counts, cudaStream_t s) {
+                     int32_t* edge_counts, cudaStream_t s, bool defer_gather = false) {
   if (ws->ctx != ctx) return fail(DCI_EINVAL, "workspace belongs to another context");
   dci_status st = check_fanouts(fanouts, L);
   if (st != DCI_OK) return st;
@@ -146,16 +183,11 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
 
   DeviceGuard g(ctx->device);
   const bool prof = ws->profiling || pass == 1;
-  if (ws->have_times && pass == 0) {
-    // the previous profiled batch on this workspace: fold its stage times into the totals
-    DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
-    float ms_s = 0.f, ms_g = 0.f;
-    DCI_CUDA(cudaEventElapsedTime(&ms_s, ws->ev_t[0], ws->ev_t[1]));
-    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[2], ws->ev_t[3]));
-    ws->acc_sample_ms += ms_s;
-    ws->acc_gather_ms += ms_g;
-    ws->acc_timed += 1;
-    ws->have_times = 0;
+  dci_workspace::TimeRec* tr = nullptr;
+  if (prof) {
+    dci_status ts = trec_begin(ws);
+    if (ts != DCI_OK) return ts;
+    tr = &ws->trec[ws->trec_cur];
   }
   // ---- per-batch header: seeds pointer, B, seed, epoch (pinned ring -> device) ----
   if (++ws->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
@@ -174,7 +206,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
 
   // ---- kernels: a CUDA graph per workspace, re-captured only when the signature changes ----
   struct Sig {
-    int32_t L, pass, prof, serial;
+    int32_t L, pass, prof, serial, tma, defer;
     int32_t fan[DCI_MAX_LAYERS];
     dci_batch_out out;
     const int32_t* nv;
@@ -186,11 +218,20 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     int32_t G;
     int32_t gather_bps;
   } sig;
+  // TMA gather: the last hop's relabel runs as its own kernel; inference gathers are serialised
+  // on the context's gather stream (one at a time at full bandwidth, beside other batches'
+  // sampling).  Register-copy gather: relabel fused, gathers of concurrent batches overlap
+  // unless DCI_GATHER_SERIAL=1.
+  // defer_gather (dci_sample_gather_many): sampling + relabel only; the caller gathers the group.
+  const bool tma = defer_gather || gather_uses_tma(ctx, out);
+  const bool serial = !defer_gather && pass == 0 && (tma ? !gather_concurrent() : gather_serial());
   memset(&sig, 0, sizeof(sig));
   sig.L = L;
   sig.pass = (int32_t)pass;
   sig.prof = prof ? 1 : 0;
-  sig.serial = gather_serial() && pass == 0 ? 1 : 0;
+  sig.serial = serial ? 1 : 0;
+  sig.tma = tma ? 1 : 0;
+  sig.defer = defer_gather ? 1 : 0;
   for (int i = 0; i < L; ++i) sig.fan[i] = fanouts[i];
   sig.out = *out;
   sig.nv = node_visits;
@@ -203,12 +244,17 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   sig.gather_bps = gather_blocks_per_sm(ctx);
   static_assert(sizeof(Sig) <= sizeof(ws->graph_sig), "signature buffer too small");
   const bool use_graph = graph_mode();
-  // serial gathers: every batch's gather kernel goes through one context-wide stream, so
-  // gathers run one at a time at full bandwidth while other batches sample alongside
-  const bool serial = gather_serial() && pass == 0;
   const bool need_capture =
       use_graph && !(ws->n_graphs && ws->graph_sig_len == sizeof(Sig) && !memcmp(ws->graph_sig, &sig, sizeof(Sig)));
-  // part 0: the L sampling hops; part 1: the fused route + gather kernel
+  HopParams last{};
+  last.f = fanouts[0];
+  last.cand = ws->cand[(L - 1) & 1];
+  last.kcnt = ws->kcnt[(L - 1) & 1];
+  // part 0: the L sampling hops (+ the last hop's relabel when the gather does not fuse it and
+  // runs on the same stream); part 1: the route + gather kernel; part 2 (serial TMA gather only):
+  // the last hop's relabel, on the sampling stream while the gather runs on the gather stream
+  const bool relabel_apart = tma && serial;
+  ws->in_group = defer_gather ? 1 : 0;
   auto enqueue_part = [&](int part, cudaStream_t es) {
     if (part == 0) {
       HopParams prev{};
@@ -233,18 +279,19 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
         launch_scan_hop(ctx, ws, p, es);
         prev = p;
       }
-    } else {
-      HopParams last{};
-      last.f = fanouts[0];
-      last.cand = ws->cand[(L - 1) & 1];
-      last.kcnt = ws->kcnt[(L - 1) & 1];
+      if (tma && !relabel_apart) launch_relabel_last(ctx, ws, L, out, last, es);
+    } else if (part == 1) {
       launch_gather_fused(ctx, ws, L, out, last, node_visits, es);
+    } else {
+      launch_relabel_last(ctx, ws, L, out, last, es);
     }
   };
+  const int nparts = relabel_apart ? 3 : 2;
   if (need_capture) {
-    // one graph per part when profiling (stage events go between them), else one graph
-    const int ngraphs = (prof || serial) ? 2 : 1;
-    for (int gi = 0; gi < 2; ++gi) {
+    // one graph per part when profiling (stage events go between them) or when the gather runs
+    // on the gather stream; else one graph
+    const int ngraphs = defer_gather ? 1 : (prof || serial) ? nparts : 1;
+    for (int gi = 0; gi < 3; ++gi) {
       if (ws->graph_exec[gi]) cudaGraphExecDestroy(ws->graph_exec[gi]);
       ws->graph_exec[gi] = nullptr;
     }
@@ -252,7 +299,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     for (int gi = 0; gi < ngraphs; ++gi) {
       const uint64_t launches0 = ctx->launches;
       DCI_CUDA(cudaStreamBeginCapture(ws->cap_stream, cudaStreamCaptureModeThreadLocal));
-      if (ngraphs == 2) {
+      if (ngraphs > 1 || defer_gather) {
         enqueue_part(gi, ws->cap_stream);
       } else {
         enqueue_part(0, ws->cap_stream);
@@ -279,7 +326,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
       enqueue_part(part, rs);
       return cudaSuccess;
     }
-    if (ws->n_graphs == 2) {
+    if (ws->n_graphs > 1) {
       ctx->launches += ws->graph_kernels[part];
       return cudaGraphLaunch(ws->graph_exec[part], rs);
     }
@@ -289,24 +336,33 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     }
     return cudaSuccess;  // single graph holds both parts
   };
-  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[0], s));
+  if (prof) DCI_CUDA(cudaEventRecord(tr->e[0], s));
   DCI_CUDA(run_part(0, s));
-  if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[1], s));
+  if (prof) {
+    DCI_CUDA(cudaEventRecord(tr->e[1], s));
+    tr->state |= 1;
+  }
+  if (defer_gather) {  // the caller gathers the group (and times it on the first workspace)
+    DCI_CUDA(cudaEventRecord(ws->ev_mid, s));
+    DCI_CUDA(cudaGetLastError());
+    return DCI_OK;
+  }
   if (serial) {
     if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
     DCI_CUDA(cudaEventRecord(ws->ev_mid, s));
     DCI_CUDA(cudaStreamWaitEvent(ctx->gstream, ws->ev_mid, 0));
-    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[2], ctx->gstream));
+    if (prof) DCI_CUDA(cudaEventRecord(tr->e[2], ctx->gstream));
     DCI_CUDA(run_part(1, ctx->gstream));
-    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], ctx->gstream));
+    if (prof) DCI_CUDA(cudaEventRecord(tr->e[3], ctx->gstream));
     DCI_CUDA(cudaEventRecord(ws->ev_done, ctx->gstream));
+    if (relabel_apart) DCI_CUDA(run_part(2, s));
     DCI_CUDA(cudaStreamWaitEvent(s, ws->ev_done, 0));
   } else {
-    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[2], s));
+    if (prof) DCI_CUDA(cudaEventRecord(tr->e[2], s));
     DCI_CUDA(run_part(1, s));
-    if (prof) DCI_CUDA(cudaEventRecord(ws->ev_t[3], s));
+    if (prof) DCI_CUDA(cudaEventRecord(tr->e[3], s));
   }
-  ws->have_times = prof ? 1 : 0;
+  if (prof) tr->state |= 2;
   DCI_CUDA(cudaGetLastError());
   return DCI_OK;
 }
@@ -502,10 +558,23 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
     return bail(e, "cudaMalloc(tile_state)");
   if ((e = cudaMalloc(&w->scal, sizeof(BatchScalars))) != cudaSuccess) return bail(e, "cudaMalloc(scal)");
   if ((e = cudaMalloc(&w->seeds_stage, sizeof(int32_t) * max_batch)) != cudaSuccess) return bail(e, "cudaMalloc");
-  for (int i = 0; i < 4; ++i)
-    if ((e = cudaEventCreate(&w->ev_t[i])) != cudaSuccess) return bail(e, "event");
+  for (auto& r : w->trec)
+    for (int i = 0; i < 4; ++i)
+      if ((e = cudaEventCreate(&r.e[i])) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_mid, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  {
+    // sampling streams of dci_sample_gather_many: optionally above the gather in priority
+    static const int prio = [] {
+      const char* v = getenv("DCI_SAMPLE_PRIO");
+      return v ? atoi(v) : 0;
+    }();
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if ((e = cudaStreamCreateWithPriority(&w->stream, cudaStreamNonBlocking, prio ? hi : lo)) != cudaSuccess)
+      return bail(e, "stream");
+  }
   if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
                          cudaHostAllocPortable)) != cudaSuccess)
     return bail(e, "cudaHostAlloc(header ring)");
@@ -536,14 +605,17 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
   cudaFree(w->tile_state);
   cudaFree(w->scal);
   cudaFree(w->seeds_stage);
-  for (int i = 0; i < 4; ++i)
-    if (w->ev_t[i]) cudaEventDestroy(w->ev_t[i]);
+  for (auto& r : w->trec)
+    for (int i = 0; i < 4; ++i)
+      if (r.e[i]) cudaEventDestroy(r.e[i]);
   for (int i = 0; i < dci_workspace::kHdrRing; ++i)
     if (w->hdr_ev[i]) cudaEventDestroy(w->hdr_ev[i]);
   if (w->ev_mid) cudaEventDestroy(w->ev_mid);
   if (w->ev_done) cudaEventDestroy(w->ev_done);
+  if (w->ev_fork) cudaEventDestroy(w->ev_fork);
+  if (w->stream) cudaStreamDestroy(w->stream);
   if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 3; ++i)
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
   if (w->live_ws) --*w->live_ws;
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
@@ -557,6 +629,93 @@ dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* see
   if (!ctx || !ws) return fail(DCI_EINVAL, "null context/workspace");
   return run_batch(ctx, ws, seeds, B, fanouts, L, seed, 0, out, nullptr, nullptr,
                    static_cast<cudaStream_t>(stream));
+}
+
+dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const* ws, const int32_t* const* seeds,
+                                  const int32_t* B, const int32_t* fanouts, int32_t L, uint64_t seed,
+                                  const dci_batch_out* outs, void* stream) {
+  if (!ctx || !ws || !seeds || !B || !outs) return fail(DCI_EINVAL, "null argument");
+  if (n < 1 || n > DCI_MAX_GROUP) return fail(DCI_EINVAL, "n must be in [1, DCI_MAX_GROUP]");
+  for (int i = 0; i < n; ++i) {
+    if (!ws[i] || ws[i]->ctx != ctx) return fail(DCI_EINVAL, "workspace null or of another context");
+    for (int j = 0; j < i; ++j)
+      if (ws[j] == ws[i]) return fail(DCI_EINVAL, "a workspace appears twice in one group");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!gather_many_uses_tma(ctx, outs, n)) {
+    // outputs that cannot take bulk stores: one batch after another on `stream`
+    for (int i = 0; i < n; ++i) {
+      dci_status st = run_batch(ctx, ws[i], seeds[i], B[i], fanouts, L, seed, 0, outs + i, nullptr, nullptr, s);
+      if (st != DCI_OK) return st;
+    }
+    return DCI_OK;
+  }
+  DeviceGuard g(ctx->device);
+  // fork: every batch samples on its workspace's stream (batches of a group run concurrently)
+  DCI_CUDA(cudaEventRecord(ws[0]->ev_fork, s));
+  for (int i = 0; i < n; ++i) {
+    DCI_CUDA(cudaStreamWaitEvent(ws[i]->stream, ws[0]->ev_fork, 0));
+    dci_status st = run_batch(ctx, ws[i], seeds[i], B[i], fanouts, L, seed, 0, outs + i, nullptr, nullptr,
+                              ws[i]->stream, /*defer_gather=*/true);
+    if (st != DCI_OK) return st;
+  }
+  // join: one TMA gather over the whole group, on the context's gather stream (group gathers run
+  // one at a time; DCI_GATHER_SERIAL=0 puts it on `stream` instead)
+  cudaStream_t gs = s;
+  if (!gather_concurrent()) {
+    if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    gs = ctx->gstream;
+  }
+  for (int i = 0; i < n; ++i) DCI_CUDA(cudaStreamWaitEvent(gs, ws[i]->ev_mid, 0));
+  bool prof = false;
+  for (int i = 0; i < n; ++i) prof |= ws[i]->profiling != 0;
+  // the launch is timed once, on the first workspace's record (one gather launch per group)
+  dci_workspace::TimeRec* tr = prof && ws[0]->profiling ? &ws[0]->trec[ws[0]->trec_cur] : nullptr;
+  if (tr) DCI_CUDA(cudaEventRecord(tr->e[2], gs));
+  launch_gather_many(ctx, ws, outs, n, L, gs);
+  if (tr) {
+    DCI_CUDA(cudaEventRecord(tr->e[3], gs));
+    tr->state |= 2;
+  }
+  DCI_CUDA(cudaEventRecord(ws[0]->ev_done, gs));
+  // the caller's stream and every workspace's next batch come after the gather
+  if (gs != s) DCI_CUDA(cudaStreamWaitEvent(s, ws[0]->ev_done, 0));
+  for (int i = 0; i < n; ++i) DCI_CUDA(cudaStreamWaitEvent(ws[i]->stream, ws[0]->ev_done, 0));
+  DCI_CUDA(cudaGetLastError());
+  return DCI_OK;
+}
+
+dci_status dci_sample_gather_many_host(dci_ctx* ctx, int32_t n, dci_workspace* const* ws,
+                                       const int32_t* const* seeds_host, const int32_t* B, const int32_t* fanouts,
+                                       int32_t L, uint64_t seed, const dci_batch_out* outs, int64_t* sizes_host,
+                                       uint64_t* counters_host, int32_t* status_host, void* stream) {
+  if (!ctx || !ws || !seeds_host || !B || !outs) return fail(DCI_EINVAL, "null argument");
+  if (n < 1 || n > DCI_MAX_GROUP) return fail(DCI_EINVAL, "n must be in [1, DCI_MAX_GROUP]");
+  if (L < 1 || L > DCI_MAX_LAYERS) return fail(DCI_EINVAL, "L must be in [1, DCI_MAX_LAYERS]");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DeviceGuard g(ctx->device);
+  const int32_t* dseeds[DCI_MAX_GROUP];
+  for (int i = 0; i < n; ++i) {
+    if (!ws[i]) return fail(DCI_EINVAL, "null workspace");
+    if (B[i] < 0 || B[i] > ws[i]->max_batch) return fail(DCI_EINVAL, "B exceeds the workspace's max_batch");
+    if (B[i] > 0 && !seeds_host[i]) return fail(DCI_EINVAL, "seeds_host is null");
+    if (B[i] > 0)
+      DCI_CUDA(cudaMemcpyAsync(ws[i]->seeds_stage, seeds_host[i], sizeof(int32_t) * B[i], cudaMemcpyHostToDevice, s));
+    dseeds[i] = ws[i]->seeds_stage;
+  }
+  dci_status st = dci_sample_gather_many(ctx, n, ws, dseeds, B, fanouts, L, seed, outs, stream);
+  if (st != DCI_OK) return st;
+  for (int i = 0; i < n; ++i) {
+    if (sizes_host)
+      DCI_CUDA(cudaMemcpyAsync(sizes_host + (int64_t)i * (L + 1), outs[i].sizes, sizeof(int64_t) * (L + 1),
+                               cudaMemcpyDeviceToHost, s));
+    if (counters_host)
+      DCI_CUDA(cudaMemcpyAsync(counters_host + 4 * i, outs[i].counters, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost,
+                               s));
+    if (status_host)
+      DCI_CUDA(cudaMemcpyAsync(status_host + i, outs[i].status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  }
+  return DCI_OK;
 }
 
 dci_status dci_sample_gather_host(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds_host, int32_t B,
@@ -657,8 +816,9 @@ dci_status dci_presample(dci_ctx* ctx, const int32_t* seeds, int64_t num_seeds, 
     DCI_CUDA(cudaMemcpyAsync(&status, ctx->pre_out.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     DCI_CUDA(cudaStreamSynchronize(s));
     float ms_s = 0.f, ms_f = 0.f;
-    DCI_CUDA(cudaEventElapsedTime(&ms_s, ctx->pre_ws->ev_t[0], ctx->pre_ws->ev_t[1]));
-    DCI_CUDA(cudaEventElapsedTime(&ms_f, ctx->pre_ws->ev_t[1], ctx->pre_ws->ev_t[3]));
+    const dci_workspace::TimeRec& pr = ctx->pre_ws->trec[ctx->pre_ws->trec_cur];
+    DCI_CUDA(cudaEventElapsedTime(&ms_s, pr.e[0], pr.e[1]));
+    DCI_CUDA(cudaEventElapsedTime(&ms_f, pr.e[1], pr.e[3]));
     if (t_sample_ns) t_sample_ns[b] = (uint64_t)llround((double)ms_s * 1e6);
     if (t_feature_ns) t_feature_ns[b] = (uint64_t)llround((double)ms_f * 1e6);
     if (status != DCI_OK) return fail((dci_status)status, "dci_presample: invalid or duplicate seed in a batch");
@@ -818,11 +978,12 @@ dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on) {
 
 dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms) {
   if (!ws) return fail(DCI_EINVAL, "null workspace");
-  if (!ws->have_times) return fail(DCI_ESTATE, "no profiled batch recorded");
+  const dci_workspace::TimeRec& r = ws->trec[ws->trec_cur];
+  if (r.state != 3) return fail(DCI_ESTATE, "no profiled batch recorded");
   DeviceGuard g(ws->device);
-  DCI_CUDA(cudaEventSynchronize(ws->ev_t[3]));
-  if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, ws->ev_t[0], ws->ev_t[1]));
-  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, ws->ev_t[2], ws->ev_t[3]));
+  DCI_CUDA(cudaEventSynchronize(r.e[3]));
+  if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, r.e[0], r.e[1]));
+  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, r.e[2], r.e[3]));
   return DCI_OK;
 }
 
@@ -830,14 +991,9 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   if (!ws || !out) return fail(DCI_EINVAL, "bad arguments");
   DeviceGuard g(ws->device);
   DCI_CUDA(cudaDeviceSynchronize());
-  if (ws->have_times) {
-    float ms_s = 0.f, ms_g = 0.f;
-    DCI_CUDA(cudaEventElapsedTime(&ms_s, ws->ev_t[0], ws->ev_t[1]));
-    DCI_CUDA(cudaEventElapsedTime(&ms_g, ws->ev_t[2], ws->ev_t[3]));
-    ws->acc_sample_ms += ms_s;
-    ws->acc_gather_ms += ms_g;
-    ws->acc_timed += 1;
-    ws->have_times = 0;
+  for (auto& r : ws->trec) {
+    dci_status st = trec_fold(ws, r);
+    if (st != DCI_OK) return st;
   }
   BatchScalars h;
   DCI_CUDA(cudaMemcpy(&h, ws->scal, sizeof(h), cudaMemcpyDeviceToHost));
@@ -848,11 +1004,15 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   out->timed_batches = ws->acc_timed;
   out->sample_ms = ws->acc_sample_ms;
   out->gather_ms = ws->acc_gather_ms;
+  out->gather_launches = ws->acc_gather_launches;
+  out->rows_read = h.acc_rows_read;
+  out->gather_bytes = h.acc_gather_bytes;
   if (reset) {
     h.acc_batches = h.acc_seeds = h.acc_rows = 0;
+    h.acc_rows_read = h.acc_gather_bytes = 0;
     for (int c = 0; c < 4; ++c) h.acc_counters[c] = 0;
     DCI_CUDA(cudaMemcpy(ws->scal, &h, sizeof(h), cudaMemcpyHostToDevice));
-    ws->acc_timed = 0;
+    ws->acc_timed = ws->acc_gather_launches = 0;
     ws->acc_sample_ms = ws->acc_gather_ms = 0.0;
   }
   return DCI_OK;

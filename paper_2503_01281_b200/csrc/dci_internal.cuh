@@ -48,6 +48,10 @@ struct BatchScalars {
   // running totals since the last dci_workspace_stats(reset): batches, seeds, |F_L| rows,
   // counters (updated by the gather kernel's last block)
   unsigned long long acc_batches, acc_seeds, acc_rows, acc_counters[4];
+  // gather accounting: feature rows actually read (a group's node sweep reads a row once for all
+  // its batches) and the gather's algorithmic bytes; launch_reads is the running
+  // count of the current launch (group launches accumulate on their first batch's scalars)
+  unsigned long long acc_rows_read, acc_gather_bytes, launch_reads;
 };
 
 struct dci_ctx_impl;
@@ -132,18 +136,29 @@ struct dci_workspace {
   // with profiling on, two graphs (sampling hops | gather) so the stage events can be
   // recorded on the stream between them (events captured inside a graph cannot be timed)
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
+  cudaGraphExec_t graph_exec[3] = {nullptr, nullptr, nullptr};
   int32_t n_graphs = 0;
   unsigned char graph_sig[512] = {0};
   size_t graph_sig_len = 0;
-  uint64_t graph_kernels[2] = {0, 0};
+  uint64_t graph_kernels[3] = {0, 0, 0};
   // stage events; ev_mid / ev_done hand the gather to and from the shared gather stream
   cudaEvent_t ev_mid = nullptr, ev_done = nullptr;
-  cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
+  // stage timing (profiling on): a ring of event records, so timing never blocks the host on the
+  // batch just issued; a record is folded into the totals when it is reused (or on stats)
+  struct TimeRec {
+    cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};  // sample start/end, gather start/end
+    int32_t state = 0;  // bit 0: sampling times recorded, bit 1: gather launch times recorded
+  };
+  static constexpr int kTimeRing = 8;
+  TimeRec trec[kTimeRing];
+  int32_t trec_cur = 0;
   int32_t profiling = 0;
-  int32_t have_times = 0;
+  int32_t in_group = 0;  // the batch being enqueued belongs to a dci_sample_gather_many group
+  // dci_sample_gather_many: the workspace's own sampling stream and the fork event
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_fork = nullptr;
   // host-side running totals of the event-timed stages (profiling on)
-  uint64_t acc_timed = 0;
+  uint64_t acc_timed = 0, acc_gather_launches = 0;
   double acc_sample_ms = 0.0, acc_gather_ms = 0.0;
 };
 
@@ -180,8 +195,19 @@ struct HopParams {
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
-void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
+// Returns true when the kernel also relabelled the last hop; false (TMA gather) when the caller
+// must run launch_relabel_last on the sampling stream.
+bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
+void launch_relabel_last(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out, const HopParams& last,
+                         cudaStream_t s);
+// The TMA (bulk-copy) gather handles this output (default; env DCI_GATHER=ldg selects the
+// register-copy kernel).  It then runs serialised on the context's gather stream.
+bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out);
+// Multi-batch TMA gather (dci_sample_gather_many): every output takes bulk stores.
+bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t n);
+void launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n, int32_t L,
+                        cudaStream_t s);
 // Gather blocks per SM: the HBM-bound gather is given a small share of each SM when many
 // batches are in flight (their sampling kernels must co-reside), the whole SM when one is.
 int gather_blocks_per_sm(const dci_ctx* ctx);

@@ -9,7 +9,9 @@
 //    workspace scalars for the next batch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "dci_internal.cuh"
 
@@ -23,6 +25,12 @@ namespace {
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 
@@ -177,14 +185,591 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
     *a.out_status = __ldcg(&sc->status);
     sc->acc_batches += 1;
     sc->acc_seeds += (unsigned long long)B;
-    sc->acc_rows += (unsigned long long)__ldcg(&sc->sizes[a.L]);
+    const unsigned long long rows = (unsigned long long)__ldcg(&sc->sizes[a.L]);
+    sc->acc_rows += rows;
+    if (MODE != 0) {
+      sc->acc_rows_read += rows;
+      sc->acc_gather_bytes += rows * (8ull * (unsigned long long)a.D + 4ull);
+    }
     for (int c = 0; c < 4; ++c) sc->acc_counters[c] += a.out_counters[c];
     sc->status = 0;
     sc->done = 0;
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Relabel of the last hop (L-1) into its block CSR, run on the sampling stream beside the TMA
+// gather (which then only copies rows): bsrc[L-1][bptr[d] + s] = final local id of cand[d*f + s]
+// (tag -> id), clear of hop L-1's scan tile state and ticket.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_relabel_last(FusedArgs a) {
+  BatchScalars* sc = a.sc;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int pf = a.last_f;
+  const int64_t n_prev = (a.L == 1) ? (int64_t)sc->hdr.B : sc->sizes[a.L - 1];
+  const int64_t nq = n_prev * pf;
+  for (int64_t q = tid; q < nq; q += nthreads) {
+    const int64_t d = q / pf;
+    const int s = (int)(q - d * pf);
+    if (s < a.last_kcnt[d])
+      a.last_bsrc[a.last_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + a.last_cand[q]));
+  }
+  for (int64_t t = tid; t < a.last_ntiles; t += nthreads) a.last_tiles[t] = 0ull;
+  if (tid == 0) sc->tickets[a.L - 1] = 0;
+}
+
+// ------------------------------------------------------------------------------------
+// k_gather_tma: S7 + S8 with the Blackwell bulk-copy (TMA) engine instead of register copies.
+// Each warp runs a K-slot shared-memory ring; a slot holds a chunk of R consecutive rows of F_L.
+//  issue   lane 0 arms the slot's mbarrier with the chunk's bytes (expect_tx), then lane j of
+//          the chunk issues cp.async.bulk global -> shared for its row (HBM cache row on a hit,
+//          pinned host row through UVA on a miss), completing on the mbarrier
+//  drain   wait on the mbarrier, then cp.async.bulk shared -> global into X (one bulk store of
+//          R rows when X rows are contiguous, else one per row), committed as a bulk group;
+//          a slot is refilled once its store has finished reading shared memory
+// Row lookups (F[r] -> dir[F[r]].slot -> source address) are done 32 rows (one group) at a time
+// by the 32 lanes and prefetched one group ahead, so the issuing lanes never wait on them.
+// A handful of warps per SM keep ~150 KB of rows in flight, leaving the SM's registers and warps to
+// the latency-bound sampling kernels of other batches.
+// ------------------------------------------------------------------------------------
+constexpr int kTmaMaxSlots = 16;
+constexpr int kTmaMaxWarps = 16;
+constexpr int kTmaMaxBatches = DCI_MAX_GROUP;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TMA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TMA_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst), "r"(src),
+               "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct TmaArgs {
+  int32_t hint;       // 1: evict-first L2 hint on rows and X, 0: evict-normal
+  int32_t sweep;      // node-sweep mode allowed (group launches, see gather_sweep)
+  int32_t Rs;         // rows per chunk in sweep mode (<= R)
+  int32_t meta_off;   // byte offset of the sweep metadata area in dynamic shared memory
+  int32_t K;          // ring slots per warp
+  int32_t R;          // rows per chunk (slot)
+  int32_t row_bytes;  // 4 * pitch
+  int32_t slot_bytes; // R * row_bytes
+};
+
+// One batch of a (multi-batch) TMA gather launch.
+struct TmaBatch {
+  const int32_t* F;       // F_L (global ids)
+  const unsigned long long* pos_of;  // the workspace's node -> (epoch, local id) table
+  BatchScalars* sc;       // the batch's workspace scalars (sizes[L], counters, status)
+  float* X;
+  int64_t ldx;            // floats
+  int32_t* node_visits;   // presample only
+  int64_t* out_sizes;
+  uint64_t* out_counters;
+  int32_t* out_status;
+};
+
+struct TmaBatches {
+  int32_t n;  // batches in this launch (<= kTmaMaxBatches)
+  int32_t L;
+  int64_t N;
+  const DirEntry* dir;
+  const float* fcache;
+  const float* const* fbases;
+  int32_t G;
+  int32_t pitch;
+  int32_t D;
+  const float* hfeats;
+  TmaBatch b[kTmaMaxBatches];
+};
+
+
+// ------------------------------------------------------------------------------------
+// Node-sweep mode of a group launch (2..kSweepMax batches whose frontiers together hold at least N
+// rows, e.g. Reddit-shaped graphs where one batch touches 61 % of all nodes).  Instead of reading
+// a feature row once per (batch, row), the warps sweep node ids v = 0..N-1 and look v up in every
+// batch's node -> local-id table (the epoch-tagged position table the sampler leaves behind: v is
+// in batch b's F_L iff its tag carries b's epoch, and the tag's low word is then v's row).  A
+// node present in any batch is read ONCE (cp.async.bulk into the shared-memory ring) and written
+// to every batch that holds it (one bulk store per (batch, row)).  Reads drop from sum_b |F_L(b)|
+// rows to |union_b F_L(b)| rows and are in ascending cache-slot order; X is bit-identical.
+// ------------------------------------------------------------------------------------
+constexpr int kSweepMax = 8;
+
+__device__ __forceinline__ void gather_sweep(const TmaBatches& a, const TmaArgs& t, uint32_t ring, int* meta,
+                                             unsigned long long* bars, int* s_nr, unsigned (*s_cnt)[2],
+                                             unsigned* s_reads, int lane, int64_t gw, int64_t nw, uint64_t pol) {
+  const int K = t.K, R = t.Rs, nb = a.n;
+  const int MS = R * (1 + kSweepMax);  // ints of metadata per slot: R masks, R x kSweepMax rows
+  const int64_t lo = a.N * gw / nw, hi = a.N * (gw + 1) / nw;
+  uint32_t ep[kSweepMax];
+  const unsigned long long* pt[kSweepMax];
+#pragma unroll
+  for (int b = 0; b < kSweepMax; ++b) {
+    ep[b] = b < nb ? __ldcg(&a.b[b].sc->hdr.epoch) : 0u;
+    pt[b] = b < nb ? a.b[b].pos_of : nullptr;
+  }
+  // one group of 32 consecutive node ids: lane j holds v = g + j.  The next group's table tags and
+  // directory slot are loaded while the current group issues.
+  unsigned long long nt[kSweepMax];
+  int32_t ns = -1;
+  auto probe = [&](int64_t g) {
+    const int64_t v = g + lane;
+    const bool in = v < hi;
+#pragma unroll
+    for (int b = 0; b < kSweepMax; ++b) nt[b] = (in && b < nb) ? __ldcg(pt[b] + v) : 0ull;
+    ns = in ? __ldg(&a.dir[v].slot) : -1;
+  };
+  int64_t g_cur = lo;
+  unsigned cmask = 0;
+  int crow[kSweepMax];
+  const char* csrc = nullptr;
+  probe(g_cur);
+  auto start = [&]() {
+    cmask = 0;
+#pragma unroll
+    for (int b = 0; b < kSweepMax; ++b) {
+      crow[b] = -1;
+      if (b < nb && (uint32_t)(nt[b] >> 32) == ep[b]) {
+        crow[b] = (int)(0xFFFFFFFFu - (uint32_t)nt[b]);
+        cmask |= 1u << b;
+      }
+    }
+    const int64_t v = g_cur + lane;
+    const int32_t sl = ns;
+    csrc = nullptr;
+    if (cmask) {
+      if (sl < 0)
+        csrc = reinterpret_cast<const char*>(a.hfeats + v * a.pitch);
+      else if (a.G == 1)
+        csrc = reinterpret_cast<const char*>(a.fcache + (int64_t)sl * a.pitch);
+      else
+        csrc = reinterpret_cast<const char*>(
+            reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(a.fbases) + sl % a.G)) +
+            (int64_t)(sl / a.G) * a.pitch);
+#pragma unroll
+      for (int b = 0; b < kSweepMax; ++b)
+        if ((cmask >> b) & 1u) atomicAdd(&s_cnt[b][sl >= 0 ? 0 : 1], 1u);
+    }
+    probe(g_cur + 32);
+  };
+  start();
+  int off = 0;
+  int64_t issued = 0, consumed = 0;
+  auto issue = [&]() -> bool {
+    unsigned pres;
+    for (;;) {
+      if (g_cur >= hi) return false;
+      pres = __ballot_sync(0xffffffffu, cmask != 0) & (off >= 32 ? 0u : (0xffffffffu << off));
+      if (pres) break;
+      g_cur += 32;
+      off = 0;
+      start();
+    }
+    unsigned chunk = 0, rest = pres;
+    for (int q = 0; q < R && rest; ++q) {
+      chunk |= rest & (0u - rest);
+      rest &= rest - 1;
+    }
+    const int cnt = __popc(chunk);
+    const int s = (int)(issued % K);
+    const uint32_t bar = smem_addr(bars + s);
+    const bool mine = (chunk >> lane) & 1u;
+    const int q = __popc(chunk & ((1u << lane) - 1u));
+    if (mine) {
+      int* m = meta + s * MS;
+      m[q] = (int)cmask;
+#pragma unroll
+      for (int b = 0; b < kSweepMax; ++b) m[R + q * kSweepMax + b] = crow[b];
+    }
+    if (lane == 0) {
+      s_nr[s] = cnt;
+      mbar_expect_tx(bar, (uint32_t)cnt * (uint32_t)t.row_bytes);
+      atomicAdd(s_reads, (unsigned)cnt);
+    }
+    __syncwarp();
+    if (mine) bulk_g2s(ring + (uint32_t)(s * t.slot_bytes + q * t.row_bytes), csrc, (uint32_t)t.row_bytes, bar, pol);
+    ++issued;
+    off = 32 - __clz(chunk);
+    if (!rest) {  // the group's present nodes are all issued: next group
+      g_cur += 32;
+      off = 0;
+      start();
+    }
+    return true;
+  };
+  for (int k = 0; k < K; ++k)
+    if (!issue()) break;
+  while (consumed < issued) {
+    const int s = (int)(consumed % K);
+    mbar_wait(smem_addr(bars + s), (uint32_t)((consumed / K) & 1));
+    const int nr = s_nr[s];
+    if (lane < nr) {
+      const int* m = meta + s * MS;
+      const unsigned mask = (unsigned)m[lane];
+      const uint32_t src = ring + (uint32_t)(s * t.slot_bytes + lane * t.row_bytes);
+#pragma unroll
+      for (int b = 0; b < kSweepMax; ++b)
+        if ((mask >> b) & 1u) {
+          const TmaBatch& tb = a.b[b];
+          bulk_s2g(tb.X + (int64_t)m[R + lane * kSweepMax + b] * tb.ldx, src, (uint32_t)t.row_bytes, pol);
+        }
+    }
+    bulk_commit();
+    ++consumed;
+    bulk_wait_read1();
+    __syncwarp();
+    if (issued < consumed - 1 + K) issue();
+  }
+}
+
+__global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_constant__ TmaBatches a, TmaArgs t) {
+  extern __shared__ __align__(128) unsigned char s_ring[];
+  __shared__ __align__(8) unsigned long long s_bar[kTmaMaxWarps][kTmaMaxSlots];
+  __shared__ char* s_dst[kTmaMaxWarps][kTmaMaxSlots];   // X address of the chunk's first row
+  __shared__ int s_nr[kTmaMaxWarps][kTmaMaxSlots];      // rows in the chunk
+  __shared__ int s_ldb[kTmaMaxWarps][kTmaMaxSlots];     // X row stride in bytes; 0 = contiguous
+  __shared__ long long s_pre[kTmaMaxBatches + 1];       // row prefix over the launch's batches
+  __shared__ unsigned s_cnt[kTmaMaxBatches][2];         // feature hits / misses per batch
+  __shared__ unsigned s_reads;                          // feature rows this block read
+  __shared__ bool s_sweep;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int K = t.K, R = t.R, nb = a.n;
+  const uint32_t ring = smem_addr(s_ring) + (uint32_t)(wib * K * t.slot_bytes);
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int i = 0; i < nb; ++i) {
+      s_pre[i] = acc;
+      acc += __ldcg(&a.b[i].sc->sizes[a.L]);
+    }
+    s_pre[nb] = acc;
+  }
+  if (threadIdx.x < 2 * kTmaMaxBatches) (&s_cnt[0][0])[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) s_reads = 0u;
+  if (lane == 0) {
+    for (int s = 0; s < K; ++s) mbar_init(smem_addr(&s_bar[wib][s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntot = s_pre[nb];
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint64_t pol = t.hint ? policy_evict_first() : policy_evict_normal();
+  const bool sweep = t.sweep && nb >= 2 && nb <= kSweepMax && ntot >= a.N;
+  if (threadIdx.x == 0) s_sweep = sweep;
+  if (sweep) {
+    gather_sweep(a, t, ring, reinterpret_cast<int*>(s_ring + t.meta_off) + wib * K * t.Rs * (1 + kSweepMax),
+                 &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
+  } else {
+  // balanced contiguous row ranges per warp over the concatenated batches
+  const int64_t lo = ntot * gw / nw, hi = ntot * (gw + 1) / nw;
+
+  // Row lookups, 32 rows (a group) at a time: lane j holds row grp + j.  Two-stage prefetch: the
+  // frontier id of group +2 and the cache slot of group +1 are in flight while group 0 issues.
+  struct Look {
+    int32_t b;  // batch of the lane's row (-1: past the range)
+    int64_t r;  // row within the batch
+    int32_t v;
+  };
+  auto look_v = [&](int64_t grp) -> Look {
+    Look l{-1, 0, -1};
+    const int64_t gr = grp + lane;
+    if (gr < hi) {
+      int b = 0;
+      while (b + 1 < nb && gr >= s_pre[b + 1]) ++b;
+      l.b = b;
+      l.r = gr - s_pre[b];
+      l.v = __ldg(a.b[b].F + l.r);
+    }
+    return l;
+  };
+  auto look_slot = [&](const Look& l) -> int32_t {
+    return (l.v >= 0 && (int64_t)l.v < a.N) ? __ldg(&a.dir[l.v].slot) : -1;
+  };
+  int64_t g_cur = lo;
+  Look l_cur = look_v(g_cur);
+  int32_t s_cur = look_slot(l_cur);
+  Look l_nxt = look_v(g_cur + 32);
+  int32_t s_nxt = look_slot(l_nxt);
+  Look l_nn = look_v(g_cur + 64);
+  const char* src_cur = nullptr;
+  int rows_cur = 0;
+  auto start_group = [&]() {
+    rows_cur = g_cur < hi ? (int)(hi - g_cur < 32 ? hi - g_cur : 32) : 0;
+    src_cur = nullptr;
+    if (lane < rows_cur && l_cur.v >= 0 && (int64_t)l_cur.v < a.N) {
+      if (s_cur < 0)
+        src_cur = reinterpret_cast<const char*>(a.hfeats + (int64_t)l_cur.v * a.pitch);
+      else if (a.G == 1)
+        src_cur = reinterpret_cast<const char*>(a.fcache + (int64_t)s_cur * a.pitch);
+      else  // partitioned cache: local or peer (NVLink) rows
+        src_cur = reinterpret_cast<const char*>(
+            reinterpret_cast<const float*>(
+                __ldg(reinterpret_cast<const unsigned long long*>(a.fbases) + s_cur % a.G)) +
+            (int64_t)(s_cur / a.G) * a.pitch);
+      atomicAdd(&s_cnt[l_cur.b][s_cur >= 0 ? 0 : 1], 1u);
+      if (a.b[l_cur.b].node_visits) atomicAdd(a.b[l_cur.b].node_visits + l_cur.v, 1);
+    }
+  };
+  start_group();
+  int off = 0;
+  int64_t issued = 0, consumed = 0;
+  // issue the next chunk (<= R rows of one batch) of this warp's range into slot issued % K
+  auto issue = [&]() -> bool {
+    if (g_cur >= hi) return false;
+    const int b0 = __shfl_sync(0xffffffffu, l_cur.b, off);
+    const unsigned same = __ballot_sync(0xffffffffu, lane >= off && lane < rows_cur && l_cur.b == b0);
+    const int cnt = min(R, __popc(same));  // rows of one batch are consecutive
+    const int s = (int)(issued % K);
+    const uint32_t bar = smem_addr(&s_bar[wib][s]);
+    // rows whose id is invalid (a bad seed; the batch status reports DCI_ESEED) are not loaded
+    const unsigned valid = __ballot_sync(0xffffffffu, src_cur != nullptr && lane >= off && lane < off + cnt);
+    const int64_t r0 = __shfl_sync(0xffffffffu, l_cur.r, off);
+    if (lane == 0) {
+      const TmaBatch& tb = a.b[b0];
+      s_dst[wib][s] = reinterpret_cast<char*>(tb.X + r0 * tb.ldx);
+      s_nr[wib][s] = cnt;
+      s_ldb[wib][s] = tb.ldx == a.pitch ? 0 : (int)(tb.ldx * 4);
+      mbar_expect_tx(bar, (uint32_t)__popc(valid) * (uint32_t)t.row_bytes);
+      atomicAdd(&s_reads, (unsigned)__popc(valid));
+    }
+    __syncwarp();
+    if ((valid >> lane) & 1u)
+      bulk_g2s(ring + (uint32_t)(s * t.slot_bytes + (lane - off) * t.row_bytes), src_cur, (uint32_t)t.row_bytes, bar,
+               pol);
+    ++issued;
+    off += cnt;
+    if (off >= rows_cur) {  // next group of this warp's range
+      off = 0;
+      g_cur += 32;
+      l_cur = l_nxt;
+      s_cur = s_nxt;
+      l_nxt = l_nn;
+      s_nxt = look_slot(l_nxt);
+      l_nn = look_v(g_cur + 64);
+      start_group();
+    }
+    return true;
+  };
+  for (int k = 0; k < K; ++k)
+    if (!issue()) break;
+  while (consumed < issued) {
+    const int s = (int)(consumed % K);
+    mbar_wait(smem_addr(&s_bar[wib][s]), (uint32_t)((consumed / K) & 1));
+    char* dst = s_dst[wib][s];
+    const int nr = s_nr[wib][s];
+    const int ldb = s_ldb[wib][s];
+    const uint32_t slot_sm = ring + (uint32_t)(s * t.slot_bytes);
+    if (ldb == 0) {
+      if (lane == 0) bulk_s2g(dst, slot_sm, (uint32_t)(nr * t.row_bytes), pol);
+    } else if (lane < nr) {
+      bulk_s2g(dst + (int64_t)lane * ldb, slot_sm + (uint32_t)(lane * t.row_bytes), (uint32_t)t.row_bytes, pol);
+    }
+    bulk_commit();
+    ++consumed;
+    bulk_wait_read1();  // stores of chunks < consumed - 1 have finished reading their slots
+    __syncwarp();
+    if (issued < consumed - 1 + K) issue();
+  }
+  }  // row mode
+  bulk_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 0 && s_reads) atomicAdd(&a.b[0].sc->launch_reads, (unsigned long long)s_reads);
+  if (threadIdx.x < nb) {
+    const int i = threadIdx.x;
+    if (s_cnt[i][0]) atomicAdd(&a.b[i].sc->counters[2], (unsigned long long)s_cnt[i][0]);
+    if (s_cnt[i][1]) atomicAdd(&a.b[i].sc->counters[3], (unsigned long long)s_cnt[i][1]);
+  }
+  // the last block publishes every batch's scalars and resets them for its next batch (done
+  // counter of the first batch's scalars)
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.b[0].sc->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    // algorithmic gather bytes of this launch, booked on the first batch:
+    //  rows:  sum_b |F_L(b)| x (row read 4D + row write 4D + 4 B slot lookup)
+    //  sweep: N x (8 B tag probe per batch + 4 B slot lookup) + |union| x 4D + sum_b |F_L(b)| x 4D
+    __threadfence();
+    BatchScalars* sc0 = a.b[0].sc;
+    const unsigned long long reads = __ldcg(&sc0->launch_reads);
+    const unsigned long long tot = (unsigned long long)s_pre[nb];
+    const unsigned long long rowb = 4ull * (unsigned long long)a.D;
+    sc0->acc_rows_read += reads;
+    sc0->acc_gather_bytes += s_sweep ? (unsigned long long)a.N * (8ull * nb + 4ull) + reads * rowb + tot * rowb
+                                     : tot * (2ull * rowb + 4ull);
+    sc0->launch_reads = 0;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < nb) {
+    __threadfence();
+    const TmaBatch& tb = a.b[threadIdx.x];
+    BatchScalars* sc = tb.sc;
+    const int32_t B = sc->hdr.B;
+    tb.out_sizes[0] = B;
+    for (int h = 1; h <= a.L; ++h) tb.out_sizes[h] = __ldcg(&sc->sizes[h]);
+    for (int c = 0; c < 4; ++c) {
+      tb.out_counters[c] = __ldcg(&sc->counters[c]);
+      sc->counters[c] = 0;
+    }
+    *tb.out_status = __ldcg(&sc->status);
+    sc->acc_batches += 1;
+    sc->acc_seeds += (unsigned long long)B;
+    sc->acc_rows += (unsigned long long)__ldcg(&sc->sizes[a.L]);
+    for (int c = 0; c < 4; ++c) sc->acc_counters[c] += tb.out_counters[c];
+    sc->status = 0;
+    if (threadIdx.x == 0) sc->done = 0;
+  }
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 }  // namespace
+
+bool gather_tma_mode() {
+  static const int mode = [] {
+    const char* e = getenv("DCI_GATHER");
+    return (e && (e[0] == 't' || e[0] == 'T')) ? 1 : 0;  // "tma": single-batch calls use the TMA gather too
+  }();
+  return mode == 1;
+}
+
+// TMA gather configuration for rows of this context: W warps per block (1 block per SM), a ring of
+// K slots of R rows per warp in dynamic shared memory; false when an output cannot take bulk
+// stores (X null or not 16-byte aligned rows) or a row does not fit (register-copy kernel then).
+static bool tma_config(const dci_ctx* ctx, const dci_batch_out* out, TmaArgs* t, int* warps, size_t* smem) {
+  if (!out->X) return false;
+  if ((out->ldx % 4) != 0 || out->ldx < ctx->pitch || (reinterpret_cast<uintptr_t>(out->X) % 16) != 0) return false;
+  static const int W = std::max(1, std::min(kTmaMaxWarps, env_int("DCI_TMA_WARPS", 8)));
+  static const int smem_kb = std::max(16, std::min(220, env_int("DCI_TMA_SMEM_KB", 200)));
+  static const int chunk_target = env_int("DCI_TMA_CHUNK", 8192);
+  static const int hint = env_int("DCI_TMA_HINT", 1);
+  static const int sweep = env_int("DCI_SWEEP", 1);
+  const int row_bytes = ctx->pitch * 4;
+  int R = std::max(1, std::min(32, (chunk_target + row_bytes / 2) / row_bytes));
+  const int ring = smem_kb * 1024 / W;
+  auto per_slot = [&](int r) { return r * row_bytes + std::min(r, 4) * (1 + kSweepMax) * 4; };
+  int K = ring / per_slot(R);
+  while (K < 4 && R > 1) {
+    R = (R + 1) / 2;
+    K = ring / per_slot(R);
+  }
+  K = std::min(K, kTmaMaxSlots);
+  if (K < 3) return false;
+  t->hint = hint;
+  t->sweep = sweep;
+  t->Rs = std::min(R, 4);
+  t->K = K;
+  t->R = R;
+  t->row_bytes = row_bytes;
+  t->slot_bytes = R * row_bytes;
+  t->meta_off = W * K * t->slot_bytes;
+  *warps = W;
+  *smem = (size_t)t->meta_off + (size_t)W * K * t->Rs * (1 + kSweepMax) * 4;
+  return true;
+}
+
+bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out) {
+  TmaArgs t;
+  int w;
+  size_t sm;
+  return gather_tma_mode() && tma_config(ctx, out, &t, &w, &sm);
+}
+
+bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t n) {
+  TmaArgs t;
+  int w;
+  size_t sm;
+  for (int i = 0; i < n; ++i)
+    if (!tma_config(ctx, outs + i, &t, &w, &sm)) return false;
+  return true;
+}
+
+static TmaBatches tma_batches(const dci_ctx* ctx, int32_t L) {
+  TmaBatches tb;
+  memset(&tb, 0, sizeof(tb));
+  tb.L = L;
+  tb.N = ctx->N;
+  tb.dir = ctx->d_dir;
+  tb.fcache = ctx->d_fcache;
+  tb.fbases = ctx->d_fbases;
+  tb.G = ctx->fpart_world;
+  tb.pitch = ctx->pitch;
+  tb.D = ctx->D;
+  tb.hfeats = ctx->u_feats;
+  return tb;
+}
+
+static void tma_add(TmaBatches* tb, dci_workspace* ws, const dci_batch_out* out, int32_t* node_visits) {
+  TmaBatch& b = tb->b[tb->n++];
+  b.F = out->frontier;
+  b.pos_of = ws->pos_of;
+  b.sc = ws->scal;
+  b.X = out->X;
+  b.ldx = out->ldx;
+  b.node_visits = node_visits;
+  b.out_sizes = out->sizes;
+  b.out_counters = out->counters;
+  b.out_status = out->status;
+}
+
+static void tma_launch(dci_ctx* ctx, const TmaBatches& tb, const dci_batch_out* out0, cudaStream_t s) {
+  TmaArgs t;
+  int warps = 0;
+  size_t smem = 0;
+  tma_config(ctx, out0, &t, &warps, &smem);
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
+  static const int bps = std::max(1, std::min(4, env_int("DCI_TMA_BPS", 1)));
+  k_gather_tma<<<ctx->num_sms * bps, 32 * warps, smem, s>>>(tb, t);
+  ++ctx->launches;
+}
+
+void launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n, int32_t L,
+                        cudaStream_t s) {
+  TmaBatches tb = tma_batches(ctx, L);
+  for (int i = 0; i < n; ++i) tma_add(&tb, ws[i], outs + i, nullptr);
+  tma_launch(ctx, tb, outs, s);
+}
 
 int gather_blocks_per_sm(const dci_ctx* ctx) {
   static const int forced = [] {
@@ -197,8 +782,8 @@ int gather_blocks_per_sm(const dci_ctx* ctx) {
   return w <= 1 ? 4 : (w <= 3 ? 2 : 1);
 }
 
-void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
-                         const HopParams& last, int32_t* node_visits, cudaStream_t s) {
+static FusedArgs fused_args(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
+                            const HopParams& last, int32_t* node_visits) {
   FusedArgs a;
   a.dir = ctx->d_dir;
   a.pos_of = ws->pos_of;
@@ -225,6 +810,27 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
   a.out_sizes = out->sizes;
   a.out_counters = out->counters;
   a.out_status = out->status;
+  return a;
+}
+
+void launch_relabel_last(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out, const HopParams& last,
+                         cudaStream_t s) {
+  const FusedArgs a = fused_args(ctx, ws, L, out, last, nullptr);
+  const int64_t need = std::max<int64_t>(1, (ws->hop_cap[L - 1] * last.f + 255) / 256);
+  const int grid = (int)std::min<int64_t>(persistent_grid(ctx, k_relabel_last, 256, 8), need);
+  k_relabel_last<<<grid, 256, 0, s>>>(a);
+  ++ctx->launches;
+}
+
+bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
+                         const HopParams& last, int32_t* node_visits, cudaStream_t s) {
+  const FusedArgs a = fused_args(ctx, ws, L, out, last, node_visits);
+  if (gather_uses_tma(ctx, out)) {
+    TmaBatches tb = tma_batches(ctx, L);
+    tma_add(&tb, ws, out, node_visits);
+    tma_launch(ctx, tb, out, s);
+    return false;  // relabel of the last hop not fused: launch_relabel_last
+  }
   const int bps = gather_blocks_per_sm(ctx);
   auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };
   const bool vec = out->X && (out->ldx % 4 == 0) && out->ldx >= ctx->pitch &&
@@ -238,6 +844,7 @@ void launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
   else
     go(k_gather<2, 5>);
   ++ctx->launches;
+  return true;
 }
 
 }  // namespace dci

@@ -502,10 +502,13 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cuda
     a.prev_tiles = ws->tile_state + ws->tile_off[p.hop - 1];
     a.prev_ntiles = ws->tile_off[p.hop] - ws->tile_off[p.hop - 1];
   }
-  static int bps = [] {
+  // resident blocks per SM of the sampling grids: 8 for one batch per call; 2 inside a
+  // dci_sample_gather_many group, whose batches sample concurrently (measured)
+  static const int forced = [] {
     const char* e = getenv("DCI_SAMPLE_BPS");
-    return e ? atoi(e) : 8;
+    return e ? atoi(e) : 0;
   }();
+  const int bps = forced > 0 ? forced : (ws->in_group ? 2 : 8);
   // Grid: persistent (SM count x resident blocks), but no larger than the worst-case frontier of
   // this hop needs (small frontiers would otherwise start hundreds of idle blocks); the fused
   // relabel of hop h-1 (|F_{h-1}| * f_{h-1} items) is covered by the grid-stride loops either way.

@@ -3,11 +3,11 @@
 # Only kernels inside bench.py's NVTX range "timed" are profiled.
 tag=${1:-run}; shift
 out=gpurun_out/prof_$tag; mkdir -p $out
-args="--profile-only --steps 12 --warmup 3 --no-cpu-baseline $@"
+args="--profile-only --steps 24 --warmup 6 --no-cpu-baseline $@"
 nv="--nvtx --nvtx-include timed/"
 ncu $nv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $out/launches.csv python bench.py $args > $out/launches.stdout 2>&1
-ncu $nv --set full --clock-control none --import-source on -k regex:k_gather -s 3 -c 2 -o $out/gather \
+ncu $nv --set full --clock-control none --import-source on -k regex:k_gather -s 1 -c 2 -o $out/gather \
     python bench.py $args > $out/gather.stdout 2>&1
 ncu $nv --set full --clock-control none --import-source on -k regex:k_sample_hop -s 3 -c 3 -o $out/sample \
     python bench.py $args > $out/sample.stdout 2>&1
