@@ -41,11 +41,15 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="M2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--inflight", type=int, default=3,
-                    help="streams in flight (each with one batch, or one group of --group batches)")
-    ap.add_argument("--group", type=int, default=6,
+    ap.add_argument("--inflight", type=int, default=None,
+                    help="streams in flight (each with one batch, or one group of --group batches); default 3 "
+                         "groups, or 6 single batches")
+    ap.add_argument("--group", type=int, default=None,
                     help="batches per dci_sample_gather_many call (one TMA gather launch per group); 0 = one "
-                         "dci_sample_gather per batch")
+                         "dci_sample_gather per batch.  Default (measured, DESIGN.md §9): 6 when the data is "
+                         "HBM-resident (M1, M2), 0 for host-link-bound configs (M3, M4, M5)")
+    ap.add_argument("--ldx", default="pitch", choices=["pitch", "line"],
+                    help="X row stride: the 16-byte feature pitch, or rounded up to whole 128-byte lines")
     ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
     ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
     ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
@@ -364,11 +368,12 @@ def run_ours(args):
     batches = parallel.shard(synth.inference_batches(ip, B), rank, world)
     batches = [b for b in batches if len(b) == B] or batches
     seeds_dev = [torch.from_numpy(b).to(dev) for b in batches]
-    nws = max(1, args.inflight)
-    G = max(0, args.group)
+    G = max(0, args.group) if args.group is not None else (6 if cfg.name.split("-")[0] in ("M1", "M2") else 0)
+    nws = max(1, args.inflight) if args.inflight is not None else (3 if G else 6)
     per = max(1, G)  # batches per call
     wss = [[dci.workspace_create(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
-    outs = [[dci.BatchOut(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
+    ldx = None if args.ldx == "pitch" else -(-cfg.D // 32) * 32
+    outs = [[dci.BatchOut(ctx, B, fan, ldx=ldx) for _ in range(per)] for _ in range(nws)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(nws)]
     for wl in wss:
         for w in wl:
@@ -525,7 +530,7 @@ def run_ours(args):
                    "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
                                                     if args.partitioned and world > 1 else "replicated caches") + ")",
-                   "inflight": nws, "group": G,
+                   "inflight": nws, "group": G, "ldx": outs[0][0].ldx,
                    "l2": "inputs larger than L2 (feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
                          % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
                             avg_fl * D * 4 / 1e6)},
