@@ -62,8 +62,20 @@ struct SampleArgs {
   BatchScalars* sc;
   unsigned long long* prev_tiles;  // previous hop's scan tile state (cleared here)
   int64_t prev_ntiles;
+  int32_t elem_policy;  // L2 policy of adjacency-cache element loads: 0 evict-last, 1 normal, 2 evict-first
   HopParams p;
 };
+
+__device__ __forceinline__ uint64_t policy_by(int k) {
+  uint64_t p;
+  if (k == 0)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (k == 1)
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
 // (position = seed index); hop h >= 1 relabels hop h-1's candidates into its block CSR
@@ -142,6 +154,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
   const int64_t nwarps = nthreads >> 5;
   uint32_t hits = 0, misses = 0;
   const uint64_t keep = policy_evict_last();
+  const uint64_t epol = policy_by(a.elem_policy);
   for (int64_t dbase = warp_id * GPW; dbase < n_h; dbase += nwarps * GPW) {
     const int64_t d = dbase + lane / G;
     const bool active = d < n_h;
@@ -193,7 +206,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
     int32_t x = -1;
     if (valid) {
       if (rank < cached_len) {
-        x = ld_keep_i32(a.acache + cache_off + rank, keep);
+        x = ld_keep_i32(a.acache + cache_off + rank, epol);
         ++hits;
       } else {
         x = ld_host_i32(a.uidx + host_off + rank);
@@ -245,6 +258,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(SampleArgs 
   const int64_t n_h = (h == 0) ? B : sc->sizes[h];
   hop_prologue(a, tid, nthreads, B, ehi, F_in);
   const uint64_t keep = policy_evict_last();
+  const uint64_t epol = policy_by(a.elem_policy);
   uint32_t hits = 0, misses = 0;
   for (int64_t d = tid >> 5; d < n_h; d += nthreads >> 5) {
     const int32_t v = F_in[d];
@@ -306,7 +320,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(SampleArgs 
       if (pos < k) {
         const int32_t rank = deg > f ? chosen[pos] : pos;
         if (rank < cached_len) {
-          x = ld_keep_i32(a.acache + cache_off + rank, keep);
+          x = ld_keep_i32(a.acache + cache_off + rank, epol);
           ++hits;
         } else {
           x = ld_host_i32(a.uidx + host_off + rank);
@@ -497,7 +511,11 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
 }  // namespace
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
-  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->scal, nullptr, 0, p};
+  static const int elem_policy = [] {
+    const char* e = getenv("DCI_ELEM_POLICY");
+    return e ? atoi(e) : 0;
+  }();
+  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->scal, nullptr, 0, elem_policy, p};
   if (p.hop > 0) {
     a.prev_tiles = ws->tile_state + ws->tile_off[p.hop - 1];
     a.prev_ntiles = ws->tile_off[p.hop] - ws->tile_off[p.hop - 1];

@@ -43,7 +43,8 @@ def _setup(cfg, ratio=None):
     return ip, ix, ft, ctx, nv, ec, nv_o, ec_o, ts, tf
 
 
-def _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_feat, nbatches=3, inflight=3):
+def _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_feat, nbatches=3, inflight=3,
+                            group=0):
     dci.fill(ctx, nv, ec, c_adj, c_feat)
     st = dci.cache_state(ctx)
     R, cl, co, ac = oracle.adj_fill(ip, ix, ec_o, c_adj)
@@ -78,6 +79,21 @@ def _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_f
     for seeds, g in zip(batches, results):
         o = oracle.sample_gather(ip, R, ft, seeds, fan, synth.SAMPLE_SEED, cl, slot_o)
         assert _same(g, o, len(fan))
+    if group:
+        # the bench's default call on HBM-resident data: groups of `group` batches, 2 groups in
+        # flight on 2 streams, one TMA gather launch per group (node sweep when sum |F_L| >= N)
+        batches = synth.inference_batches(ip, B)[nbatches:nbatches + 2 * group]
+        gw = [[dci.workspace_create(ctx, B, fan) for _ in range(group)] for _ in range(2)]
+        go = [[dci.BatchOut(ctx, B, fan) for _ in range(group)] for _ in range(2)]
+        gs = [torch.cuda.Stream() for _ in range(2)]
+        sd = [torch.from_numpy(b).to(DEV) for b in batches]
+        for k in range(2):
+            dci.sample_gather_many(ctx, gw[k], sd[k * group:(k + 1) * group], fan, synth.SAMPLE_SEED, go[k],
+                                   stream=gs[k])
+        torch.cuda.synchronize()
+        for i, seeds in enumerate(batches):
+            o = oracle.sample_gather(ip, R, ft, seeds, fan, synth.SAMPLE_SEED, cl, slot_o)
+            assert _same(go[i // group][i % group].result(), o, len(fan)), i
 
 
 def test_m2_reddit_fullsize_auto_budget():
@@ -86,7 +102,7 @@ def test_m2_reddit_fullsize_auto_budget():
     ip, ix, ft, ctx, nv, ec, nv_o, ec_o, ts, tf = _setup(cfg)
     c_adj, c_feat = dci.allocate(ctx, 0, ts, tf)
     assert c_adj + c_feat > 0
-    _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_feat, nbatches=4)
+    _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_feat, nbatches=4, group=6)
 
 
 @pytest.mark.parametrize("r", [None, 0.0, 0.5])
@@ -99,7 +115,8 @@ def test_m3_products_fullsize_quarter_budget(r):
     ratio = None if r is None else (int(r * 100), 100)
     c_adj, c_feat = dci.allocate(ctx, C, ts, tf, ratio=ratio)
     assert (c_adj, c_feat) == oracle.allocate(C, ts, tf, ratio=ratio)
-    _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_feat, nbatches=4)
+    _check_fill_and_batches(cfg, ip, ix, ft, ctx, nv, ec, nv_o, ec_o, c_adj, c_feat, nbatches=4,
+                            group=3 if r == 0.5 else 0)
 
 
 def test_workspace_stats_and_graph_recapture():
@@ -129,6 +146,17 @@ def test_workspace_stats_and_graph_recapture():
     assert st["counters"] == tot_cnt.tolist()
     assert st["timed_batches"] == 2 and st["gather_ms"] > 0 and st["sample_ms"] > 0
     assert ws.stats()["batches"] == 0
+
+
+@pytest.mark.parametrize("env", [{"DCI_GATHER": "tma"}, {"DCI_SWEEP": "0"}, {"DCI_GATHER_SERIAL": "0"},
+                                 {"DCI_TMA_WARPS": "2", "DCI_TMA_CHUNK": "2048"}])
+def test_gather_variants_subprocess(env):
+    """Process-wide gather switches (read once per process): the TMA gather for single-batch calls,
+    row mode for groups, group gathers on the caller's stream, a small TMA ring."""
+    r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=ROOT,
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "smoke ok" in r.stdout
 
 
 def test_no_graph_path_subprocess():

@@ -27,18 +27,30 @@ def _inputs():
     return ip.numpy(), ix.numpy(), synth.features(N, D).numpy()
 
 
+def _check(g, o):
+    assert g["status"] == 0 and np.array_equal(g["F"], o.F)
+    assert np.array_equal(g["counters"], o.counters)
+    assert np.array_equal(g["X"], o.X)
+    for h in range(len(FAN)):
+        assert np.array_equal(g["bsrc"][h], o.bsrc[h])
+
+
 def _check_batches(ctx, ip, R, ft, cl, slot_o, dev, nb=4):
     ws = dci.workspace_create(ctx, B, FAN)
-    for seeds in synth.inference_batches(ip, B)[:nb]:
+    batches = synth.inference_batches(ip, B)
+    for seeds in batches[:nb]:
         out = dci.BatchOut(ctx, B, FAN)
         dci.sample_gather(ctx, ws, torch.from_numpy(seeds).to(dev), FAN, 9, out)
-        g = out.result()
-        o = oracle.sample_gather(ip, R, ft, seeds, FAN, 9, cl, slot_o)
-        assert g["status"] == 0 and np.array_equal(g["F"], o.F)
-        assert np.array_equal(g["counters"], o.counters)
-        assert np.array_equal(g["X"], o.X)
-        for h in range(len(FAN)):
-            assert np.array_equal(g["bsrc"][h], o.bsrc[h])
+        _check(out.result(), oracle.sample_gather(ip, R, ft, seeds, FAN, 9, cl, slot_o))
+    # groups (one TMA gather launch reading local and peer partitions): 3 batches (row mode) and
+    # 8 batches (node sweep: together they hold more rows than N)
+    for n in (3, 8):
+        grp = [batches[i % len(batches)] for i in range(n)]
+        wss = [dci.workspace_create(ctx, B, FAN) for _ in grp]
+        outs = [dci.BatchOut(ctx, B, FAN) for _ in grp]
+        dci.sample_gather_many(ctx, wss, [torch.from_numpy(s).to(dev) for s in grp], FAN, 9, outs)
+        for s, og in zip(grp, outs):
+            _check(og.result(), oracle.sample_gather(ip, R, ft, s, FAN, 9, cl, slot_o))
 
 
 @pytest.mark.parametrize("world", [2, 3, 5])
