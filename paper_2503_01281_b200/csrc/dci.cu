@@ -136,7 +136,7 @@ dci_status trec_fold(dci_workspace* ws, dci_workspace::TimeRec& r) {
     DCI_CUDA(cudaEventSynchronize(r.e[1]));
     DCI_CUDA(cudaEventElapsedTime(&ms, r.e[0], r.e[1]));
     ws->acc_sample_ms += ms;
-    ws->acc_timed += 1;
+    ws->acc_timed += r.nb;
   }
   if (r.state & 2) {
     float ms = 0.f;
@@ -156,10 +156,23 @@ dci_status trec_begin(dci_workspace* ws) {
   return trec_fold(ws, ws->trec[ws->trec_cur]);
 }
 
-// Enqueue one batch (shared by inference pass 0 and presample pass 1).
-dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, const int32_t* fanouts,
-                     int32_t L, uint64_t seed, uint32_t pass, const dci_batch_out* out, int32_t* node_visits,
-                     int32_t* edge_counts, cudaStream_t s, bool defer_gather = false) {
+// Parameters of the last hop's relabel (a virtual hop L whose "previous hop" is hop L-1).
+HopParams epilogue_params(dci_workspace* ws, int32_t L, const int32_t* fanouts, const dci_batch_out* out) {
+  HopParams e{};
+  e.F = out->frontier;
+  e.hop = L;
+  e.f = 1;
+  e.prev_cand = ws->cand[(L - 1) & 1];
+  e.prev_kcnt = ws->kcnt[(L - 1) & 1];
+  e.prev_bptr = out->bptr[L - 1];
+  e.prev_bsrc = out->bsrc[L - 1];
+  e.prev_f = fanouts[0];
+  return e;
+}
+
+// Argument checks of one batch (dci_sample_gather, _many, presample).
+dci_status validate_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, const int32_t* fanouts,
+                          int32_t L, const dci_batch_out* out) {
   if (ws->ctx != ctx) return fail(DCI_EINVAL, "workspace belongs to another context");
   dci_status st = check_fanouts(fanouts, L);
   if (st != DCI_OK) return st;
@@ -180,16 +193,13 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
       return fail(DCI_ECAP, "hop_cap/bsrc_cap < dci_output_bounds");
   }
   if (out->X && out->ldx < ctx->D) return fail(DCI_EINVAL, "ldx < D");
+  return DCI_OK;
+}
 
-  DeviceGuard g(ctx->device);
-  const bool prof = ws->profiling || pass == 1;
-  dci_workspace::TimeRec* tr = nullptr;
-  if (prof) {
-    dci_status ts = trec_begin(ws);
-    if (ts != DCI_OK) return ts;
-    tr = &ws->trec[ws->trec_cur];
-  }
-  // ---- per-batch header: seeds pointer, B, seed, epoch (pinned ring -> device) ----
+// Per-batch header (seeds pointer, B, seed, table epoch): pinned ring -> the workspace's device
+// scalars, on stream s, ahead of the batch's kernels (which are a fixed CUDA graph).
+dci_status stage_header(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, uint64_t seed,
+                        cudaStream_t s) {
   if (++ws->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
     DCI_CUDA(cudaMemsetAsync(ws->pos_of, 0, sizeof(unsigned long long) * ctx->N, s));
     ws->epoch = 1;
@@ -203,10 +213,30 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   hh->epoch = ws->epoch;
   DCI_CUDA(cudaMemcpyAsync(&ws->scal->hdr, hh, sizeof(BatchHeader), cudaMemcpyHostToDevice, s));
   DCI_CUDA(cudaEventRecord(ws->hdr_ev[slot], s));
+  return DCI_OK;
+}
+
+// Enqueue one batch (shared by inference pass 0 and presample pass 1).
+dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, const int32_t* fanouts,
+                     int32_t L, uint64_t seed, uint32_t pass, const dci_batch_out* out, int32_t* node_visits,
+                     int32_t* edge_counts, cudaStream_t s) {
+  dci_status st = validate_batch(ctx, ws, seeds, B, fanouts, L, out);
+  if (st != DCI_OK) return st;
+  DeviceGuard g(ctx->device);
+  const bool prof = ws->profiling || pass == 1;
+  dci_workspace::TimeRec* tr = nullptr;
+  if (prof) {
+    dci_status ts = trec_begin(ws);
+    if (ts != DCI_OK) return ts;
+    tr = &ws->trec[ws->trec_cur];
+    tr->nb = 1;
+  }
+  st = stage_header(ctx, ws, seeds, B, seed, s);
+  if (st != DCI_OK) return st;
 
   // ---- kernels: a CUDA graph per workspace, re-captured only when the signature changes ----
   struct Sig {
-    int32_t L, pass, prof, serial, tma, defer;
+    int32_t L, pass, prof, serial, tma;
     int32_t fan[DCI_MAX_LAYERS];
     dci_batch_out out;
     const int32_t* nv;
@@ -222,16 +252,14 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   // on the context's gather stream (one at a time at full bandwidth, beside other batches'
   // sampling).  Register-copy gather: relabel fused, gathers of concurrent batches overlap
   // unless DCI_GATHER_SERIAL=1.
-  // defer_gather (dci_sample_gather_many): sampling + relabel only; the caller gathers the group.
-  const bool tma = defer_gather || gather_uses_tma(ctx, out);
-  const bool serial = !defer_gather && pass == 0 && (tma ? !gather_concurrent() : gather_serial());
+  const bool tma = gather_uses_tma(ctx, out);
+  const bool serial = pass == 0 && (tma ? !gather_concurrent() : gather_serial());
   memset(&sig, 0, sizeof(sig));
   sig.L = L;
   sig.pass = (int32_t)pass;
   sig.prof = prof ? 1 : 0;
   sig.serial = serial ? 1 : 0;
   sig.tma = tma ? 1 : 0;
-  sig.defer = defer_gather ? 1 : 0;
   for (int i = 0; i < L; ++i) sig.fan[i] = fanouts[i];
   sig.out = *out;
   sig.nv = node_visits;
@@ -250,11 +278,12 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   last.f = fanouts[0];
   last.cand = ws->cand[(L - 1) & 1];
   last.kcnt = ws->kcnt[(L - 1) & 1];
+  const HopParams epi = epilogue_params(ws, L, fanouts, out);
   // part 0: the L sampling hops (+ the last hop's relabel when the gather does not fuse it and
   // runs on the same stream); part 1: the route + gather kernel; part 2 (serial TMA gather only):
   // the last hop's relabel, on the sampling stream while the gather runs on the gather stream
   const bool relabel_apart = tma && serial;
-  ws->in_group = defer_gather ? 1 : 0;
+  ws->in_group = 0;
   auto enqueue_part = [&](int part, cudaStream_t es) {
     if (part == 0) {
       HopParams prev{};
@@ -275,22 +304,22 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
         }
         p.bptr = out->bptr[h];
         p.edge_counts = edge_counts;
-        launch_sample_hop(ctx, ws, p, es);
-        launch_scan_hop(ctx, ws, p, es);
+        launch_sample_hop(ctx, &ws, &p, 1, es);
+        launch_scan_hop(ctx, &ws, &p, 1, es);
         prev = p;
       }
-      if (tma && !relabel_apart) launch_relabel_last(ctx, ws, L, out, last, es);
+      if (tma && !relabel_apart) launch_hop_epilogue(ctx, &ws, &epi, 1, es);
     } else if (part == 1) {
       launch_gather_fused(ctx, ws, L, out, last, node_visits, es);
     } else {
-      launch_relabel_last(ctx, ws, L, out, last, es);
+      launch_hop_epilogue(ctx, &ws, &epi, 1, es);
     }
   };
   const int nparts = relabel_apart ? 3 : 2;
   if (need_capture) {
     // one graph per part when profiling (stage events go between them) or when the gather runs
     // on the gather stream; else one graph
-    const int ngraphs = defer_gather ? 1 : (prof || serial) ? nparts : 1;
+    const int ngraphs = (prof || serial) ? nparts : 1;
     for (int gi = 0; gi < 3; ++gi) {
       if (ws->graph_exec[gi]) cudaGraphExecDestroy(ws->graph_exec[gi]);
       ws->graph_exec[gi] = nullptr;
@@ -299,7 +328,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     for (int gi = 0; gi < ngraphs; ++gi) {
       const uint64_t launches0 = ctx->launches;
       DCI_CUDA(cudaStreamBeginCapture(ws->cap_stream, cudaStreamCaptureModeThreadLocal));
-      if (ngraphs > 1 || defer_gather) {
+      if (ngraphs > 1) {
         enqueue_part(gi, ws->cap_stream);
       } else {
         enqueue_part(0, ws->cap_stream);
@@ -341,11 +370,6 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
   if (prof) {
     DCI_CUDA(cudaEventRecord(tr->e[1], s));
     tr->state |= 1;
-  }
-  if (defer_gather) {  // the caller gathers the group (and times it on the first workspace)
-    DCI_CUDA(cudaEventRecord(ws->ev_mid, s));
-    DCI_CUDA(cudaGetLastError());
-    return DCI_OK;
   }
   if (serial) {
     if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
@@ -520,7 +544,9 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
   DeviceGuard g(ctx->device);
   dci_workspace* w = new (std::nothrow) dci_workspace();
   if (!w) return fail(DCI_ENOMEM, "host allocation failed");
+  static std::atomic<uint64_t> next_uid{1};
   w->ctx = ctx;
+  w->uid = next_uid++;
   w->device = ctx->device;
   w->max_batch = max_batch;
   w->L = L;
@@ -563,18 +589,6 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
       if ((e = cudaEventCreate(&r.e[i])) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_mid, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
-  if ((e = cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
-  {
-    // sampling streams of dci_sample_gather_many: optionally above the gather in priority
-    static const int prio = [] {
-      const char* v = getenv("DCI_SAMPLE_PRIO");
-      return v ? atoi(v) : 0;
-    }();
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if ((e = cudaStreamCreateWithPriority(&w->stream, cudaStreamNonBlocking, prio ? hi : lo)) != cudaSuccess)
-      return bail(e, "stream");
-  }
   if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
                          cudaHostAllocPortable)) != cudaSuccess)
     return bail(e, "cudaHostAlloc(header ring)");
@@ -612,11 +626,12 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     if (w->hdr_ev[i]) cudaEventDestroy(w->hdr_ev[i]);
   if (w->ev_mid) cudaEventDestroy(w->ev_mid);
   if (w->ev_done) cudaEventDestroy(w->ev_done);
-  if (w->ev_fork) cudaEventDestroy(w->ev_fork);
-  if (w->stream) cudaStreamDestroy(w->stream);
+
   if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
   for (int i = 0; i < 3; ++i)
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
+  if (w->gg_exec) cudaGraphExecDestroy(w->gg_exec);
+  free(w->gg_sig);
   if (w->live_ws) --*w->live_ws;
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   delete w;
@@ -650,37 +665,131 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     }
     return DCI_OK;
   }
-  DeviceGuard g(ctx->device);
-  // fork: every batch samples on its workspace's stream (batches of a group run concurrently)
-  DCI_CUDA(cudaEventRecord(ws[0]->ev_fork, s));
   for (int i = 0; i < n; ++i) {
-    DCI_CUDA(cudaStreamWaitEvent(ws[i]->stream, ws[0]->ev_fork, 0));
-    dci_status st = run_batch(ctx, ws[i], seeds[i], B[i], fanouts, L, seed, 0, outs + i, nullptr, nullptr,
-                              ws[i]->stream, /*defer_gather=*/true);
+    dci_status st = validate_batch(ctx, ws[i], seeds[i], B[i], fanouts, L, outs + i);
     if (st != DCI_OK) return st;
   }
-  // join: one TMA gather over the whole group, on the context's gather stream (group gathers run
-  // one at a time; DCI_GATHER_SERIAL=0 puts it on `stream` instead)
+  DeviceGuard g(ctx->device);
+  dci_workspace* w0 = ws[0];
+  const bool prof = w0->profiling != 0;
+  dci_workspace::TimeRec* tr = nullptr;
+  if (prof) {
+    dci_status ts = trec_begin(w0);
+    if (ts != DCI_OK) return ts;
+    tr = &w0->trec[w0->trec_cur];
+    tr->nb = n;
+  }
+  for (int i = 0; i < n; ++i) {
+    dci_status st = stage_header(ctx, ws[i], seeds[i], B[i], seed, s);
+    if (st != DCI_OK) return st;
+  }
+  // ---- the group's sampling: every hop of all n batches is ONE launch (hop, scan), then one
+  // relabel of the last hop; captured as a CUDA graph on the first workspace, re-captured when
+  // the group (workspaces, outputs, fan-outs, caches) changes ----
+  struct GroupSig {
+    int32_t n, L;
+    int32_t fan[DCI_MAX_LAYERS];
+    uint64_t ws[DCI_MAX_GROUP];  // workspace uids (a freed workspace's address may be reused)
+    dci_batch_out out[DCI_MAX_GROUP];
+    const void* acache;
+    const void* uidx;
+  };
+  GroupSig* sig = new (std::nothrow) GroupSig;
+  if (!sig) return fail(DCI_ENOMEM, "host allocation failed");
+  std::unique_ptr<GroupSig> sig_guard(sig);
+  memset(sig, 0, sizeof(GroupSig));
+  sig->n = n;
+  sig->L = L;
+  for (int i = 0; i < L; ++i) sig->fan[i] = fanouts[i];
+  for (int i = 0; i < n; ++i) {
+    sig->ws[i] = ws[i]->uid;
+    sig->out[i] = outs[i];
+  }
+  sig->acache = ctx->d_acache;
+  sig->uidx = ctx->u_idx_cur;
+  auto enqueue = [&](cudaStream_t es) {
+    HopParams p[DCI_MAX_GROUP], prev[DCI_MAX_GROUP];
+    for (int h = 0; h < L; ++h) {
+      for (int i = 0; i < n; ++i) {
+        HopParams& q = p[i];
+        q = HopParams{};
+        q.F = outs[i].frontier;
+        q.hop = h;
+        q.f = fanouts[L - 1 - h];
+        q.pass = 0;
+        q.cand = ws[i]->cand[h & 1];
+        q.kcnt = ws[i]->kcnt[h & 1];
+        if (h > 0) {
+          q.prev_cand = prev[i].cand;
+          q.prev_kcnt = prev[i].kcnt;
+          q.prev_bptr = outs[i].bptr[h - 1];
+          q.prev_bsrc = outs[i].bsrc[h - 1];
+          q.prev_f = prev[i].f;
+        }
+        q.bptr = outs[i].bptr[h];
+      }
+      launch_sample_hop(ctx, ws, p, n, es);
+      launch_scan_hop(ctx, ws, p, n, es);
+      for (int i = 0; i < n; ++i) prev[i] = p[i];
+    }
+    for (int i = 0; i < n; ++i) p[i] = epilogue_params(ws[i], L, fanouts, outs + i);
+    launch_hop_epilogue(ctx, ws, p, n, es);
+  };
+  w0->in_group = 1;
+  const bool use_graph = graph_mode();
+  if (use_graph) {
+    const bool need = !(w0->gg_exec && w0->gg_sig_len == sizeof(GroupSig) && w0->gg_sig &&
+                        !memcmp(w0->gg_sig, sig, sizeof(GroupSig)));
+    if (need) {
+      if (w0->gg_exec) cudaGraphExecDestroy(w0->gg_exec);
+      w0->gg_exec = nullptr;
+      const uint64_t launches0 = ctx->launches;
+      DCI_CUDA(cudaStreamBeginCapture(w0->cap_stream, cudaStreamCaptureModeThreadLocal));
+      enqueue(w0->cap_stream);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(w0->cap_stream, &graph);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      w0->gg_kernels = ctx->launches - launches0;
+      ctx->launches = launches0;
+      e = cudaGraphInstantiate(&w0->gg_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      if (!w0->gg_sig) w0->gg_sig = malloc(sizeof(GroupSig));
+      if (!w0->gg_sig) return fail(DCI_ENOMEM, "host allocation failed");
+      memcpy(w0->gg_sig, sig, sizeof(GroupSig));
+      w0->gg_sig_len = sizeof(GroupSig);
+    }
+  }
+  if (tr) DCI_CUDA(cudaEventRecord(tr->e[0], s));
+  if (use_graph) {
+    ctx->launches += w0->gg_kernels;
+    DCI_CUDA(cudaGraphLaunch(w0->gg_exec, s));
+  } else {
+    enqueue(s);
+  }
+  if (tr) {
+    DCI_CUDA(cudaEventRecord(tr->e[1], s));
+    tr->state |= 1;
+  }
+  // ---- one TMA gather over the whole group, on the context's gather stream (group gathers run
+  // one at a time; DCI_GATHER_SERIAL=0 puts it on `stream` instead) ----
   cudaStream_t gs = s;
   if (!gather_concurrent()) {
     if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
     gs = ctx->gstream;
+    DCI_CUDA(cudaEventRecord(w0->ev_mid, s));
+    DCI_CUDA(cudaStreamWaitEvent(gs, w0->ev_mid, 0));
   }
-  for (int i = 0; i < n; ++i) DCI_CUDA(cudaStreamWaitEvent(gs, ws[i]->ev_mid, 0));
-  bool prof = false;
-  for (int i = 0; i < n; ++i) prof |= ws[i]->profiling != 0;
-  // the launch is timed once, on the first workspace's record (one gather launch per group)
-  dci_workspace::TimeRec* tr = prof && ws[0]->profiling ? &ws[0]->trec[ws[0]->trec_cur] : nullptr;
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[2], gs));
   launch_gather_many(ctx, ws, outs, n, L, gs);
   if (tr) {
     DCI_CUDA(cudaEventRecord(tr->e[3], gs));
     tr->state |= 2;
   }
-  DCI_CUDA(cudaEventRecord(ws[0]->ev_done, gs));
-  // the caller's stream and every workspace's next batch come after the gather
-  if (gs != s) DCI_CUDA(cudaStreamWaitEvent(s, ws[0]->ev_done, 0));
-  for (int i = 0; i < n; ++i) DCI_CUDA(cudaStreamWaitEvent(ws[i]->stream, ws[0]->ev_done, 0));
+  if (gs != s) {
+    DCI_CUDA(cudaEventRecord(w0->ev_done, gs));
+    DCI_CUDA(cudaStreamWaitEvent(s, w0->ev_done, 0));
+  }
   DCI_CUDA(cudaGetLastError());
   return DCI_OK;
 }

@@ -108,6 +108,7 @@ struct dci_ctx {
 
 struct dci_workspace {
   dci_ctx* ctx = nullptr;
+  uint64_t uid = 0;  // unique per workspace ever created (graph signatures)
   std::shared_ptr<std::atomic<int>> live_ws;  // set for user workspaces (not the presample one)
   int device = 0;  // own copy: destroying a workspace never dereferences its context
   int32_t max_batch = 0;
@@ -148,15 +149,18 @@ struct dci_workspace {
   struct TimeRec {
     cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};  // sample start/end, gather start/end
     int32_t state = 0;  // bit 0: sampling times recorded, bit 1: gather launch times recorded
+    int32_t nb = 1;     // batches whose sampling the record covers (a group's sampling is one graph)
   };
   static constexpr int kTimeRing = 8;
   TimeRec trec[kTimeRing];
   int32_t trec_cur = 0;
   int32_t profiling = 0;
   int32_t in_group = 0;  // the batch being enqueued belongs to a dci_sample_gather_many group
-  // dci_sample_gather_many: the workspace's own sampling stream and the fork event
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev_fork = nullptr;
+  // dci_sample_gather_many: the group's sampling graph, cached on the group's first workspace
+  cudaGraphExec_t gg_exec = nullptr;
+  void* gg_sig = nullptr;
+  size_t gg_sig_len = 0;
+  uint64_t gg_kernels = 0;
   // host-side running totals of the event-timed stages (profiling on)
   uint64_t acc_timed = 0, acc_gather_launches = 0;
   double acc_sample_ms = 0.0, acc_gather_ms = 0.0;
@@ -193,14 +197,17 @@ struct HopParams {
   int32_t* edge_counts;     // presample only (nullable)
 };
 
-void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
-void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s);
+// Hop launches over n >= 1 batches (p[i] / ws[i] per batch; hop, f, pass, prev_f and edge_counts
+// are taken from p[0]).  A dci_sample_gather_many group samples all its batches with one launch
+// per kernel; a single call is n = 1.
+void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
+void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
+// Relabel of the last hop (p[i].hop = L, prev_* = hop L-1) when the gather does not fuse it.
+void launch_hop_epilogue(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
 // Returns true when the kernel also relabelled the last hop; false (TMA gather) when the caller
-// must run launch_relabel_last on the sampling stream.
+// must run launch_hop_epilogue on the sampling stream.
 bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
-void launch_relabel_last(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out, const HopParams& last,
-                         cudaStream_t s);
 // The TMA (bulk-copy) gather handles this output (default; env DCI_GATHER=ldg selects the
 // register-copy kernel).  It then runs serialised on the context's gather stream.
 bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out);

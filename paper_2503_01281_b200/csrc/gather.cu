@@ -198,28 +198,6 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
-// Relabel of the last hop (L-1) into its block CSR, run on the sampling stream beside the TMA
-// gather (which then only copies rows): bsrc[L-1][bptr[d] + s] = final local id of cand[d*f + s]
-// (tag -> id), clear of hop L-1's scan tile state and ticket.
-// ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_relabel_last(FusedArgs a) {
-  BatchScalars* sc = a.sc;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int pf = a.last_f;
-  const int64_t n_prev = (a.L == 1) ? (int64_t)sc->hdr.B : sc->sizes[a.L - 1];
-  const int64_t nq = n_prev * pf;
-  for (int64_t q = tid; q < nq; q += nthreads) {
-    const int64_t d = q / pf;
-    const int s = (int)(q - d * pf);
-    if (s < a.last_kcnt[d])
-      a.last_bsrc[a.last_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + a.last_cand[q]));
-  }
-  for (int64_t t = tid; t < a.last_ntiles; t += nthreads) a.last_tiles[t] = 0ull;
-  if (tid == 0) sc->tickets[a.L - 1] = 0;
-}
-
-// ------------------------------------------------------------------------------------
 // k_gather_tma: S7 + S8 with the Blackwell bulk-copy (TMA) engine instead of register copies.
 // Each warp runs a K-slot shared-memory ring; a slot holds a chunk of R consecutive rows of F_L.
 //  issue   lane 0 arms the slot's mbarrier with the chunk's bytes (expect_tx), then lane j of
@@ -324,41 +302,43 @@ struct TmaBatches {
 // to every batch that holds it (one bulk store per (batch, row)).  Reads drop from sum_b |F_L(b)|
 // rows to |union_b F_L(b)| rows and are in ascending cache-slot order; X is bit-identical.
 // ------------------------------------------------------------------------------------
-constexpr int kSweepMax = 8;
+constexpr int kSweepMax = 16;  // batches per sweep launch (masks are 16-bit)
+
+template <int SMAX>
 
 __device__ __forceinline__ void gather_sweep(const TmaBatches& a, const TmaArgs& t, uint32_t ring, int* meta,
                                              unsigned long long* bars, int* s_nr, unsigned (*s_cnt)[2],
                                              unsigned* s_reads, int lane, int64_t gw, int64_t nw, uint64_t pol) {
   const int K = t.K, R = t.Rs, nb = a.n;
-  const int MS = R * (1 + kSweepMax);  // ints of metadata per slot: R masks, R x kSweepMax rows
+  const int MS = R * (1 + SMAX);  // ints of metadata per slot: R masks, R x SMAX rows
   const int64_t lo = a.N * gw / nw, hi = a.N * (gw + 1) / nw;
-  uint32_t ep[kSweepMax];
-  const unsigned long long* pt[kSweepMax];
+  uint32_t ep[SMAX];
+  const unsigned long long* pt[SMAX];
 #pragma unroll
-  for (int b = 0; b < kSweepMax; ++b) {
+  for (int b = 0; b < SMAX; ++b) {
     ep[b] = b < nb ? __ldcg(&a.b[b].sc->hdr.epoch) : 0u;
     pt[b] = b < nb ? a.b[b].pos_of : nullptr;
   }
   // one group of 32 consecutive node ids: lane j holds v = g + j.  The next group's table tags and
   // directory slot are loaded while the current group issues.
-  unsigned long long nt[kSweepMax];
+  unsigned long long nt[SMAX];
   int32_t ns = -1;
   auto probe = [&](int64_t g) {
     const int64_t v = g + lane;
     const bool in = v < hi;
 #pragma unroll
-    for (int b = 0; b < kSweepMax; ++b) nt[b] = (in && b < nb) ? __ldcg(pt[b] + v) : 0ull;
+    for (int b = 0; b < SMAX; ++b) nt[b] = (in && b < nb) ? __ldcg(pt[b] + v) : 0ull;
     ns = in ? __ldg(&a.dir[v].slot) : -1;
   };
   int64_t g_cur = lo;
   unsigned cmask = 0;
-  int crow[kSweepMax];
+  int crow[SMAX];
   const char* csrc = nullptr;
   probe(g_cur);
   auto start = [&]() {
     cmask = 0;
 #pragma unroll
-    for (int b = 0; b < kSweepMax; ++b) {
+    for (int b = 0; b < SMAX; ++b) {
       crow[b] = -1;
       if (b < nb && (uint32_t)(nt[b] >> 32) == ep[b]) {
         crow[b] = (int)(0xFFFFFFFFu - (uint32_t)nt[b]);
@@ -378,7 +358,7 @@ __device__ __forceinline__ void gather_sweep(const TmaBatches& a, const TmaArgs&
             reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(a.fbases) + sl % a.G)) +
             (int64_t)(sl / a.G) * a.pitch);
 #pragma unroll
-      for (int b = 0; b < kSweepMax; ++b)
+      for (int b = 0; b < SMAX; ++b)
         if ((cmask >> b) & 1u) atomicAdd(&s_cnt[b][sl >= 0 ? 0 : 1], 1u);
     }
     probe(g_cur + 32);
@@ -410,7 +390,7 @@ __device__ __forceinline__ void gather_sweep(const TmaBatches& a, const TmaArgs&
       int* m = meta + s * MS;
       m[q] = (int)cmask;
 #pragma unroll
-      for (int b = 0; b < kSweepMax; ++b) m[R + q * kSweepMax + b] = crow[b];
+      for (int b = 0; b < SMAX; ++b) m[R + q * SMAX + b] = crow[b];
     }
     if (lane == 0) {
       s_nr[s] = cnt;
@@ -439,10 +419,10 @@ __device__ __forceinline__ void gather_sweep(const TmaBatches& a, const TmaArgs&
       const unsigned mask = (unsigned)m[lane];
       const uint32_t src = ring + (uint32_t)(s * t.slot_bytes + lane * t.row_bytes);
 #pragma unroll
-      for (int b = 0; b < kSweepMax; ++b)
+      for (int b = 0; b < SMAX; ++b)
         if ((mask >> b) & 1u) {
           const TmaBatch& tb = a.b[b];
-          bulk_s2g(tb.X + (int64_t)m[R + lane * kSweepMax + b] * tb.ldx, src, (uint32_t)t.row_bytes, pol);
+          bulk_s2g(tb.X + (int64_t)m[R + lane * SMAX + b] * tb.ldx, src, (uint32_t)t.row_bytes, pol);
         }
     }
     bulk_commit();
@@ -488,8 +468,11 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
   const bool sweep = t.sweep && nb >= 2 && nb <= kSweepMax && ntot >= a.N;
   if (threadIdx.x == 0) s_sweep = sweep;
   if (sweep) {
-    gather_sweep(a, t, ring, reinterpret_cast<int*>(s_ring + t.meta_off) + wib * K * t.Rs * (1 + kSweepMax),
-                 &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
+    int* meta = reinterpret_cast<int*>(s_ring + t.meta_off) + wib * K * t.Rs * (1 + kSweepMax);
+    if (nb <= 8)
+      gather_sweep<8>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
+    else
+      gather_sweep<16>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
   } else {
   // balanced contiguous row ranges per warp over the concatenated batches
   const int64_t lo = ntot * gw / nw, hi = ntot * (gw + 1) / nw;
@@ -813,15 +796,6 @@ static FusedArgs fused_args(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dc
   return a;
 }
 
-void launch_relabel_last(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out, const HopParams& last,
-                         cudaStream_t s) {
-  const FusedArgs a = fused_args(ctx, ws, L, out, last, nullptr);
-  const int64_t need = std::max<int64_t>(1, (ws->hop_cap[L - 1] * last.f + 255) / 256);
-  const int grid = (int)std::min<int64_t>(persistent_grid(ctx, k_relabel_last, 256, 8), need);
-  k_relabel_last<<<grid, 256, 0, s>>>(a);
-  ++ctx->launches;
-}
-
 bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s) {
   const FusedArgs a = fused_args(ctx, ws, L, out, last, node_visits);
@@ -829,7 +803,7 @@ bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
     TmaBatches tb = tma_batches(ctx, L);
     tma_add(&tb, ws, out, node_visits);
     tma_launch(ctx, tb, out, s);
-    return false;  // relabel of the last hop not fused: launch_relabel_last
+    return false;  // relabel of the last hop not fused: launch_hop_epilogue
   }
   const int bps = gather_blocks_per_sm(ctx);
   auto go = [&](auto kern) { kern<<<persistent_grid(ctx, kern, 256, bps), 256, 0, s>>>(a); };

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "dci_internal.cuh"
 #include "philox.cuh"
@@ -53,17 +54,34 @@ __device__ __forceinline__ int4 ld_keep_v4(const int4* p, uint64_t pol) {
   return r;
 }
 
-struct SampleArgs {
+// One batch of a (multi-batch) hop launch.  A dci_sample_gather_many group runs every hop of all
+// its batches as ONE launch over the concatenation of their frontiers; a single call is n = 1.
+struct HopBatch {
+  int32_t* F;                      // frontier (global ids); hop 0 reads the seeds from the header
+  int32_t* cand;                   // [n_h * f]
+  int32_t* kcnt;                   // [n_h]
+  const int32_t* prev_cand;        // hop h-1 (relabelled by this hop's kernel)
+  const int32_t* prev_kcnt;
+  const int32_t* prev_bptr;
+  int32_t* prev_bsrc;
+  int32_t* bptr;                   // this hop's block row pointers (written by the scan)
+  unsigned long long* pos_of;      // the workspace's node -> position tag table
+  BatchScalars* sc;
+  unsigned long long* tiles;       // this hop's scan tile state
+  unsigned long long* prev_tiles;  // previous hop's scan tile state (cleared here)
+  int64_t prev_ntiles;
+};
+
+struct HopLaunch {
   const DirEntry* dir;
   const int32_t* acache;
   const int32_t* uidx;  // device alias of the pinned host CSC (current order)
   int64_t N;
-  unsigned long long* pos_of;
-  BatchScalars* sc;
-  unsigned long long* prev_tiles;  // previous hop's scan tile state (cleared here)
-  int64_t prev_ntiles;
+  int32_t hop, f, prev_f, n;
+  uint32_t pass;
   int32_t elem_policy;  // L2 policy of adjacency-cache element loads: 0 evict-last, 1 normal, 2 evict-first
-  HopParams p;
+  int32_t* edge_counts; // presample only (nullable, n = 1)
+  HopBatch b[DCI_MAX_GROUP];
 };
 
 __device__ __forceinline__ uint64_t policy_by(int k) {
@@ -77,41 +95,103 @@ __device__ __forceinline__ uint64_t policy_by(int k) {
   return p;
 }
 
-// Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
-// (position = seed index); hop h >= 1 relabels hop h-1's candidates into its block CSR
-// (tag -> final local id) and clears hop h-1's scan tile state.
-__device__ __forceinline__ void hop_prologue(const SampleArgs& a, int64_t tid, int64_t nthreads, int64_t B,
-                                             unsigned long long ehi, const int32_t* F_in) {
-  const HopParams& p = a.p;
-  BatchScalars* sc = a.sc;
-  const int h = p.hop;
-  if (h == 0) {
-    for (int64_t d = tid; d < B; d += nthreads) {
-      const int32_t s = F_in[d];
-      p.F[d] = s;
-      if (s < 0 || (int64_t)s >= a.N)
-        atomicCAS(&sc->status, 0, (int32_t)DCI_ESEED);
-      else
-        atomicMax(a.pos_of + s, ehi | (0xFFFFFFFFu - (uint32_t)d));
+// Per-launch batch table in shared memory: frontier prefix over the batches, epoch tags, seeds.
+struct HopShared {
+  long long pre[DCI_MAX_GROUP + 1];   // prefix of n_h(b)
+  long long ppre[DCI_MAX_GROUP + 1];  // prefix of n_{h-1}(b) * f_{h-1} (relabel items)
+  long long tpre[DCI_MAX_GROUP + 1];  // prefix of prev_ntiles(b)
+  unsigned long long ehi[DCI_MAX_GROUP];
+  unsigned long long seed[DCI_MAX_GROUP];
+  const int32_t* Fin[DCI_MAX_GROUP];
+  unsigned cnt[DCI_MAX_GROUP][2];     // adjacency hits / misses of this block, per batch
+};
+
+__device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S) {
+  if (threadIdx.x == 0) {
+    long long acc = 0, pacc = 0, tacc = 0;
+    for (int b = 0; b < a.n; ++b) {
+      const BatchScalars* sc = a.b[b].sc;
+      const long long B = sc->hdr.B;
+      const long long nh = a.hop == 0 ? B : sc->sizes[a.hop];
+      const long long np = a.hop == 0 ? 0 : (a.hop == 1 ? B : sc->sizes[a.hop - 1]);
+      S.pre[b] = acc;
+      S.ppre[b] = pacc;
+      S.tpre[b] = tacc;
+      acc += nh;
+      pacc += np * a.prev_f;
+      tacc += a.b[b].prev_ntiles;
+      S.ehi[b] = (unsigned long long)sc->hdr.epoch << 32;
+      S.seed[b] = sc->hdr.seed;
+      S.Fin[b] = a.hop == 0 ? sc->hdr.seeds : a.b[b].F;
     }
-  } else {
-    // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
-    const int pf = p.prev_f;
-    const int64_t n_prev = (h == 1) ? B : sc->sizes[h - 1];
-    const int64_t nq = n_prev * pf;
-    for (int64_t q = tid; q < nq; q += nthreads) {
-      const int64_t d = q / pf;
-      const int s = (int)(q - d * pf);
-      if (s < p.prev_kcnt[d])
-        p.prev_bsrc[p.prev_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + p.prev_cand[q]));
-    }
-    for (int64_t t = tid; t < a.prev_ntiles; t += nthreads) a.prev_tiles[t] = 0ull;
-    if (tid == 0) sc->tickets[h - 1] = 0;
+    S.pre[a.n] = acc;
+    S.ppre[a.n] = pacc;
+    S.tpre[a.n] = tacc;
+  }
+  if (threadIdx.x < 2 * DCI_MAX_GROUP) (&S.cnt[0][0])[threadIdx.x] = 0u;
+  __syncthreads();
+}
+
+// batch of item q in a prefix table (n <= 16: a short linear scan over shared memory)
+__device__ __forceinline__ int batch_of(const long long* pre, int n, long long q) {
+  int b = 0;
+  while (b + 1 < n && q >= pre[b + 1]) ++b;
+  return b;
+}
+
+__device__ __forceinline__ void hop_shared_flush(const HopLaunch& a, HopShared& S) {
+  __syncthreads();
+  if (threadIdx.x < a.n) {
+    BatchScalars* sc = a.b[threadIdx.x].sc;
+    if (S.cnt[threadIdx.x][0]) atomicAdd(&sc->counters[0], (unsigned long long)S.cnt[threadIdx.x][0]);
+    if (S.cnt[threadIdx.x][1]) atomicAdd(&sc->counters[1], (unsigned long long)S.cnt[threadIdx.x][1]);
   }
 }
 
+// Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
+// (position = seed index); hop h >= 1 relabels hop h-1's candidates into its block CSR
+// (tag -> final local id) and clears hop h-1's scan tile state and ticket.  With hop = L (no
+// sampling: k_hop_epilogue) it relabels the last hop.
+__device__ __forceinline__ void hop_prologue(const HopLaunch& a, const HopShared& S, int64_t tid, int64_t nthreads) {
+  const int h = a.hop, n = a.n;
+  if (h == 0) {
+    const long long tot = S.pre[n];
+    for (long long q = tid; q < tot; q += nthreads) {
+      const int b = batch_of(S.pre, n, q);
+      const int64_t d = q - S.pre[b];
+      const HopBatch& hb = a.b[b];
+      const int32_t s = S.Fin[b][d];
+      hb.F[d] = s;
+      if (s < 0 || (int64_t)s >= a.N)
+        atomicCAS(&hb.sc->status, 0, (int32_t)DCI_ESEED);
+      else
+        atomicMax(hb.pos_of + s, S.ehi[b] | (0xFFFFFFFFu - (uint32_t)d));
+    }
+    return;
+  }
+  // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
+  const int pf = a.prev_f;
+  const long long ptot = S.ppre[n];
+  for (long long q = tid; q < ptot; q += nthreads) {
+    const int b = batch_of(S.ppre, n, q);
+    const HopBatch& hb = a.b[b];
+    const int64_t ql = q - S.ppre[b];
+    const int64_t d = ql / pf;
+    const int s = (int)(ql - d * pf);
+    if (s < hb.prev_kcnt[d])
+      hb.prev_bsrc[hb.prev_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(hb.pos_of + hb.prev_cand[ql]));
+  }
+  const long long ttot = S.tpre[n];
+  for (long long t = tid; t < ttot; t += nthreads) {
+    const int b = batch_of(S.tpre, n, t);
+    a.b[b].prev_tiles[t - S.tpre[b]] = 0ull;
+  }
+  if (tid < n) a.b[tid].sc->tickets[h - 1] = 0;
+}
+
 // ------------------------------------------------------------------------------------
-// k_sample_hop<G>: one group of G lanes (G = next pow2 >= f) per dst node of F_h.
+// k_sample_hop<G>: one group of G lanes (G = next pow2 >= f) per dst node of F_h (of any batch of
+// the launch: dst index q over the concatenated frontiers -> batch b, local dst d).
 //  1. one broadcast 32 B directory load (host_off, cache_off, deg, cached_len)
 //  2. k = min(deg, f); deg <= f -> ranks 0..deg-1; else Floyd's selection with lane i
 //     drawing t_i = floor(u_i * (j_i + 1) / 2^64), j_i = deg - k + i, u_i =
@@ -120,48 +200,43 @@ __device__ __forceinline__ void hop_prologue(const SampleArgs& a, int64_t tid, i
 //  3. ranks sorted in registers (position = #smaller ranks in the group)
 //  4. element read: HBM cache iff rank < cached_len, else UVA host read
 //  5. cand[d*f + pos] = neighbour, pads -1; kcnt[d] = k
-//  6. insert into the node->position table: atomicMax(tag(n_h + d*f + pos)), tag(p) =
+//  6. insert into the batch's node->position table: atomicMax(tag(n_h + d*f + pos)), tag(p) =
 //     epoch << 32 | ~p, so the table keeps each node's first (dst-major, rank-ascending)
 //     occurrence and entries of earlier batches read as absent
 //  7. presample: edge_counts[host_off + rank] += 1 (C8)
-// Fused extra work: hop 0 writes the seeds into F and the table (position = seed index);
-// hop h >= 1 relabels hop h-1's candidates into its block CSR (bsrc[h-1]) and clears hop
-// h-1's scan tile state.
+// Fused extra work: hop_prologue.
 // ------------------------------------------------------------------------------------
 template <int G>
-__global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
-  const HopParams& p = a.p;
-  BatchScalars* sc = a.sc;
-  const int h = p.hop;
-  const int f = p.f;
+__global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopLaunch a) {
+  __shared__ HopShared S;
+  hop_shared_init(a, S);
+  const int h = a.hop;
+  const int f = a.f;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int gbase = lane & ~(G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t B = sc->hdr.B;
-  const unsigned long long seed = sc->hdr.seed;
-  const unsigned long long ehi = (unsigned long long)sc->hdr.epoch << 32;
-  const int32_t* F_in = (h == 0) ? sc->hdr.seeds : p.F;
-
-  const int64_t n_h = (h == 0) ? B : sc->sizes[h];
-
-  hop_prologue(a, tid, nthreads, B, ehi, F_in);
+  hop_prologue(a, S, tid, nthreads);
+  const long long total = S.pre[a.n];
 
   const int GPW = 32 / G;
   const int64_t warp_id = tid >> 5;
   const int64_t nwarps = nthreads >> 5;
-  uint32_t hits = 0, misses = 0;
   const uint64_t keep = policy_evict_last();
   const uint64_t epol = policy_by(a.elem_policy);
-  for (int64_t dbase = warp_id * GPW; dbase < n_h; dbase += nwarps * GPW) {
-    const int64_t d = dbase + lane / G;
-    const bool active = d < n_h;
+  for (int64_t dbase = warp_id * GPW; dbase < total; dbase += nwarps * GPW) {
+    const int64_t q = dbase + lane / G;
+    const bool active = q < total;
+    const int b = active ? batch_of(S.pre, a.n, q) : 0;
+    const HopBatch& hb = a.b[b];
+    const int64_t d = q - S.pre[b];
+    const int64_t n_h = S.pre[b + 1] - S.pre[b];
     int32_t v = -1;
     int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
     if (active) {
-      v = F_in[d];
+      v = S.Fin[b][d];
       if (v >= 0 && (int64_t)v < a.N) {
         const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
         e0 = ld_keep_v4(ep, keep);
@@ -181,7 +256,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
       int32_t chosen = 0, j = 0;
       if (floyd && gl < f) {
         j = deg - f + gl;
-        const uint64_t u = philox_u64(seed, p.pass, (uint32_t)h, (uint32_t)v, (uint32_t)gl);
+        const uint64_t u = philox_u64(S.seed[b], a.pass, (uint32_t)h, (uint32_t)v, (uint32_t)gl);
         chosen = (int32_t)__umul64hi(u, (uint64_t)(j + 1));
       }
       // Floyd: slot i keeps t_i unless an earlier slot already chose it, then takes j_i.
@@ -205,28 +280,22 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
     const bool valid = active && gl < k;
     int32_t x = -1;
     if (valid) {
-      if (rank < cached_len) {
+      const bool hit = rank < cached_len;
+      if (hit)
         x = ld_keep_i32(a.acache + cache_off + rank, epol);
-        ++hits;
-      } else {
+      else
         x = ld_host_i32(a.uidx + host_off + rank);
-        ++misses;
-      }
+      atomicAdd(&S.cnt[b][hit ? 0 : 1], 1u);
     }
-    if (active && gl < f) p.cand[d * f + (valid ? pos : gl)] = x;
-    if (active && gl == 0) p.kcnt[d] = k;
+    if (active && gl < f) hb.cand[d * f + (valid ? pos : gl)] = x;
+    if (active && gl == 0) hb.kcnt[d] = k;
     if (valid) {
-      const unsigned long long tag = ehi | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
-      if (__ldcg(a.pos_of + x) < tag) atomicMax(a.pos_of + x, tag);
-      if (p.edge_counts) atomicAdd(p.edge_counts + host_off + rank, 1);
+      const unsigned long long tag = S.ehi[b] | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
+      if (__ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
+      if (a.edge_counts) atomicAdd(a.edge_counts + host_off + rank, 1);
     }
   }
-  hits = __reduce_add_sync(0xffffffffu, hits);
-  misses = __reduce_add_sync(0xffffffffu, misses);
-  if (lane == 0 && (hits | misses)) {
-    atomicAdd(&sc->counters[0], (unsigned long long)hits);
-    atomicAdd(&sc->counters[1], (unsigned long long)misses);
-  }
+  hop_shared_flush(a, S);
 }
 
 
@@ -239,29 +308,28 @@ __global__ void __launch_bounds__(256) k_sample_hop(SampleArgs a) {
 // ------------------------------------------------------------------------------------
 constexpr int kWideWarps = 4;
 
-__global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(SampleArgs a) {
+__global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __grid_constant__ HopLaunch a) {
   extern __shared__ int32_t s_wide[];
-  const HopParams& p = a.p;
-  BatchScalars* sc = a.sc;
-  const int h = p.hop;
-  const int f = p.f;
+  __shared__ HopShared S;
+  hop_shared_init(a, S);
+  const int h = a.hop;
+  const int f = a.f;
   int fp2 = 1;
   while (fp2 < f) fp2 <<= 1;
   int32_t* chosen = s_wide + (threadIdx.x >> 5) * fp2;
   const int lane = threadIdx.x & 31;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t B = sc->hdr.B;
-  const unsigned long long seed = sc->hdr.seed;
-  const unsigned long long ehi = (unsigned long long)sc->hdr.epoch << 32;
-  const int32_t* F_in = (h == 0) ? sc->hdr.seeds : p.F;
-  const int64_t n_h = (h == 0) ? B : sc->sizes[h];
-  hop_prologue(a, tid, nthreads, B, ehi, F_in);
+  hop_prologue(a, S, tid, nthreads);
+  const long long total = S.pre[a.n];
   const uint64_t keep = policy_evict_last();
   const uint64_t epol = policy_by(a.elem_policy);
-  uint32_t hits = 0, misses = 0;
-  for (int64_t d = tid >> 5; d < n_h; d += nthreads >> 5) {
-    const int32_t v = F_in[d];
+  for (int64_t q = tid >> 5; q < total; q += nthreads >> 5) {
+    const int b = batch_of(S.pre, a.n, q);
+    const HopBatch& hb = a.b[b];
+    const int64_t d = q - S.pre[b];
+    const int64_t n_h = S.pre[b + 1] - S.pre[b];
+    const int32_t v = S.Fin[b][d];
     int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
     if (v >= 0 && (int64_t)v < a.N) {
       const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
@@ -281,7 +349,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(SampleArgs 
         bool coll_prev = false;
         if (in) {
           j = deg - f + i;
-          const uint64_t u = philox_u64(seed, p.pass, (uint32_t)h, (uint32_t)v, (uint32_t)i);
+          const uint64_t u = philox_u64(S.seed[b], a.pass, (uint32_t)h, (uint32_t)v, (uint32_t)i);
           t = (int32_t)__umul64hi(u, (uint64_t)(j + 1));
           for (int m = 0; m < c0; ++m) coll_prev |= chosen[m] == t;
         }
@@ -319,35 +387,40 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(SampleArgs 
       int32_t x = -1;
       if (pos < k) {
         const int32_t rank = deg > f ? chosen[pos] : pos;
-        if (rank < cached_len) {
+        const bool hit = rank < cached_len;
+        if (hit)
           x = ld_keep_i32(a.acache + cache_off + rank, epol);
-          ++hits;
-        } else {
+        else
           x = ld_host_i32(a.uidx + host_off + rank);
-          ++misses;
-        }
-        const unsigned long long tag = ehi | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
-        if (__ldcg(a.pos_of + x) < tag) atomicMax(a.pos_of + x, tag);
-        if (p.edge_counts) atomicAdd(p.edge_counts + host_off + rank, 1);
+        atomicAdd(&S.cnt[b][hit ? 0 : 1], 1u);
+        const unsigned long long tag = S.ehi[b] | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
+        if (__ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
+        if (a.edge_counts) atomicAdd(a.edge_counts + host_off + rank, 1);
       }
-      p.cand[d * f + pos] = x;
+      hb.cand[d * f + pos] = x;
     }
-    if (lane == 0) p.kcnt[d] = k;
+    if (lane == 0) hb.kcnt[d] = k;
     __syncwarp();
   }
-  hits = __reduce_add_sync(0xffffffffu, hits);
-  misses = __reduce_add_sync(0xffffffffu, misses);
-  if (lane == 0 && (hits | misses)) {
-    atomicAdd(&sc->counters[0], (unsigned long long)hits);
-    atomicAdd(&sc->counters[1], (unsigned long long)misses);
-  }
+  hop_shared_flush(a, S);
+}
+
+// k_hop_epilogue: the hop_prologue of a virtual hop L, i.e. the relabel of the last hop into its
+// block CSR and the clear of its scan state (launched after the last scan; the gather of a
+// group / TMA gather does not fuse it).
+__global__ void __launch_bounds__(256) k_hop_epilogue(const __grid_constant__ HopLaunch a) {
+  __shared__ HopShared S;
+  hop_shared_init(a, S);
+  hop_prologue(a, S, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 // ------------------------------------------------------------------------------------
 // k_scan_hop: one thread per dst of F_h, kScanTile dsts per tile, tiles taken by dynamic
-// tickets (in-order => deadlock-free look-back).  Per dst: k (samples) and the bitmask of
-// candidates that are the first occurrence of a node not yet in F (table tag == tag(n_h +
-// q)).  One block scan + warp-parallel decoupled look-back over packed (k << 31 | nn):
+// tickets (in-order => deadlock-free look-back); a multi-batch launch numbers the tiles of all its
+// batches consecutively (one ticket counter) and each batch's tiles look back only within it.
+// Per dst: k (samples) and the bitmask of candidates that are the first occurrence of a node not
+// yet in F (table tag == tag(n_h + q)).  One block scan + warp-parallel decoupled look-back over
+// packed (k << 31 | nn):
 //   bptr_h[d]            = sum of k over earlier dsts                 (block CSR)
 //   new id of candidate  = n_h + (#new candidates before it)          (F_{h+1} append)
 // and the owner of each new node rewrites its table tag to the final local id, which the
@@ -357,44 +430,55 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-struct ScanArgs {
-  unsigned long long* pos_of;
-  BatchScalars* sc;
-  unsigned long long* tile_state;  // this hop's region
-  int64_t N;
-  HopParams p;
-};
-
-__global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
-  const HopParams& p = a.p;
-  BatchScalars* sc = a.sc;
-  const int h = p.hop;
-  const int f = p.f;
-  const int64_t n_h = (h == 0) ? (int64_t)sc->hdr.B : sc->sizes[h];
-  const int64_t ntiles = (n_h + kScanTile - 1) / kScanTile;
-  const unsigned long long ehi = (unsigned long long)sc->hdr.epoch << 32;
+__global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ HopLaunch a) {
+  const int h = a.hop;
+  const int f = a.f;
+  const int n = a.n;
+  __shared__ long long s_pre[DCI_MAX_GROUP + 1];   // n_h(b) prefix
+  __shared__ long long s_tpre[DCI_MAX_GROUP + 1];  // tile prefix
+  __shared__ unsigned long long s_ehi[DCI_MAX_GROUP];
   __shared__ uint32_t s_ticket;
   __shared__ unsigned long long s_warp[kScanTile / 32];
   __shared__ unsigned long long s_prefix;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-
-  if (n_h == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      p.bptr[0] = 0;
-      sc->sizes[h + 1] = 0;
+  if (threadIdx.x == 0) {
+    long long acc = 0, tacc = 0;
+    for (int b = 0; b < n; ++b) {
+      const BatchScalars* sc = a.b[b].sc;
+      const long long nh = h == 0 ? (long long)sc->hdr.B : sc->sizes[h];
+      s_pre[b] = acc;
+      s_tpre[b] = tacc;
+      s_ehi[b] = (unsigned long long)sc->hdr.epoch << 32;
+      acc += nh;
+      tacc += (nh + kScanTile - 1) / kScanTile;
     }
-    return;
+    s_pre[n] = acc;
+    s_tpre[n] = tacc;
   }
+  __syncthreads();
+  // empty batches: no tiles; their block CSR and size are written here
+  if (blockIdx.x == 0 && threadIdx.x < n && s_pre[threadIdx.x + 1] == s_pre[threadIdx.x]) {
+    a.b[threadIdx.x].bptr[0] = 0;
+    a.b[threadIdx.x].sc->sizes[h + 1] = 0;
+  }
+  const long long ntiles_all = s_tpre[n];
+  unsigned int* ticket = &a.b[0].sc->tickets[h];
   for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&sc->tickets[h], 1u);
+    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);
     __syncthreads();
-    const int64_t tile = s_ticket;
-    if (tile >= ntiles) break;
+    const long long gt = s_ticket;
+    if (gt >= ntiles_all) break;
+    const int b = batch_of(s_tpre, n, gt);
+    const HopBatch& hb = a.b[b];
+    const int64_t tile = gt - s_tpre[b];
+    const int64_t n_h = s_pre[b + 1] - s_pre[b];
+    const int64_t ntiles = (n_h + kScanTile - 1) / kScanTile;
+    const unsigned long long ehi = s_ehi[b];
     const int64_t d = tile * kScanTile + threadIdx.x;
     uint32_t k = 0, newmask = 0, nwide = 0;
     if (d < n_h) {
-      k = (uint32_t)p.kcnt[d];
-      const int32_t* c = p.cand + d * f;
+      k = (uint32_t)hb.kcnt[d];
+      const int32_t* c = hb.cand + d * f;
       const uint32_t base = (uint32_t)(n_h + d * f);
       // which of my candidates own their node's first occurrence (8 loads in flight); a
       // 32-bit mask for f <= 32, else counted here and re-checked when appending
@@ -404,7 +488,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
         for (int u = 0; u < 8; ++u) x[u] = (s0 + u < k) ? c[s0 + u] : -1;
         unsigned long long t[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? __ldcg(a.pos_of + x[u]) : 0ull;
+        for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? __ldcg(hb.pos_of + x[u]) : 0ull;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) {
@@ -415,9 +499,9 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
           }
       }
       if (h == 0) {
-        const int32_t sd = p.F[d];
-        if (sd >= 0 && (int64_t)sd < a.N && __ldcg(a.pos_of + sd) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
-          atomicCAS(&sc->status, 0, (int32_t)DCI_EDUP);
+        const int32_t sd = hb.F[d];
+        if (sd >= 0 && (int64_t)sd < a.N && __ldcg(hb.pos_of + sd) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
+          atomicCAS(&hb.sc->status, 0, (int32_t)DCI_EDUP);
       }
     }
     const uint32_t nn = f <= 32 ? __popc(newmask) : nwide;
@@ -443,19 +527,19 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
     __syncthreads();
     const unsigned long long tile_total = s_warp[kScanTile / 32 - 1];
     const unsigned long long excl = incl - mine + (wid > 0 ? s_warp[wid - 1] : 0ull);
-    // decoupled look-back, warp-parallel: 32 predecessors per round
+    // decoupled look-back within the batch, warp-parallel: 32 predecessors per round
     if (wid == 0) {
       unsigned long long prefix = 0;
       if (tile == 0) {
-        if (lane == 0) st_volatile_u64(a.tile_state, kFlagIncl | tile_total);
+        if (lane == 0) st_volatile_u64(hb.tiles, kFlagIncl | tile_total);
       } else {
-        if (lane == 0) st_volatile_u64(a.tile_state + tile, kFlagAgg | tile_total);
+        if (lane == 0) st_volatile_u64(hb.tiles + tile, kFlagAgg | tile_total);
         int64_t base = tile - 1;
         for (;;) {
           const int64_t t = base - lane;
-          unsigned long long st = t >= 0 ? ld_volatile_u64(a.tile_state + t) : kFlagIncl;
+          unsigned long long st = t >= 0 ? ld_volatile_u64(hb.tiles + t) : kFlagIncl;
           while (__any_sync(0xffffffffu, (st & ~kValMask) == 0)) {
-            if ((st & ~kValMask) == 0) st = ld_volatile_u64(a.tile_state + t);
+            if ((st & ~kValMask) == 0) st = ld_volatile_u64(hb.tiles + t);
           }
           const unsigned incl_mask = __ballot_sync(0xffffffffu, (st & ~kValMask) == kFlagIncl);
           const int stop = incl_mask ? (__ffs(incl_mask) - 1) : 31;
@@ -466,29 +550,29 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
           if (incl_mask) break;
           base -= 32;
         }
-        if (lane == 0) st_volatile_u64(a.tile_state + tile, kFlagIncl | (prefix + tile_total));
+        if (lane == 0) st_volatile_u64(hb.tiles + tile, kFlagIncl | (prefix + tile_total));
       }
       if (lane == 0) {
         s_prefix = prefix;
         if (tile == ntiles - 1) {
           const unsigned long long tot = prefix + tile_total;
-          p.bptr[n_h] = (int32_t)(tot >> 31);
-          sc->sizes[h + 1] = n_h + (int64_t)(tot & ((1ull << 31) - 1));
+          hb.bptr[n_h] = (int32_t)(tot >> 31);
+          hb.sc->sizes[h + 1] = n_h + (int64_t)(tot & ((1ull << 31) - 1));
         }
       }
     }
     __syncthreads();
     if (d < n_h) {
       const unsigned long long pre = s_prefix + excl;
-      p.bptr[d] = (int32_t)(pre >> 31);
+      hb.bptr[d] = (int32_t)(pre >> 31);
       uint32_t nid = (uint32_t)(n_h + (int64_t)(pre & ((1ull << 31) - 1)));
-      const int32_t* c = p.cand + d * f;
+      const int32_t* c = hb.cand + d * f;
       if (f <= 32) {
         for (uint32_t m = newmask; m; m &= m - 1) {
           const int s = __ffs(m) - 1;
           const int32_t x = c[s];
-          p.F[nid] = x;
-          a.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+          hb.F[nid] = x;
+          hb.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
           ++nid;
         }
       } else if (nwide) {
@@ -496,9 +580,9 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
         const uint32_t base = (uint32_t)(n_h + d * f);
         for (uint32_t s = 0; s < k; ++s) {
           const int32_t x = c[s];
-          if (x >= 0 && __ldcg(a.pos_of + x) == (ehi | (0xFFFFFFFFu - (base + s)))) {
-            p.F[nid] = x;
-            a.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+          if (x >= 0 && __ldcg(hb.pos_of + x) == (ehi | (0xFFFFFFFFu - (base + s)))) {
+            hb.F[nid] = x;
+            hb.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
             ++nid;
           }
         }
@@ -508,65 +592,111 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(ScanArgs a) {
   }
 }
 
-}  // namespace
-
-void launch_sample_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
+static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n) {
   static const int elem_policy = [] {
     const char* e = getenv("DCI_ELEM_POLICY");
     return e ? atoi(e) : 0;
   }();
-  SampleArgs a{ctx->d_dir, ctx->d_acache, ctx->u_idx_cur, ctx->N, ws->pos_of, ws->scal, nullptr, 0, elem_policy, p};
-  if (p.hop > 0) {
-    a.prev_tiles = ws->tile_state + ws->tile_off[p.hop - 1];
-    a.prev_ntiles = ws->tile_off[p.hop] - ws->tile_off[p.hop - 1];
+  HopLaunch a;
+  memset(&a, 0, sizeof(a));
+  a.dir = ctx->d_dir;
+  a.acache = ctx->d_acache;
+  a.uidx = ctx->u_idx_cur;
+  a.N = ctx->N;
+  a.hop = p[0].hop;
+  a.f = p[0].f;
+  a.prev_f = p[0].prev_f;
+  a.n = n;
+  a.pass = p[0].pass;
+  a.elem_policy = elem_policy;
+  a.edge_counts = p[0].edge_counts;
+  for (int i = 0; i < n; ++i) {
+    HopBatch& b = a.b[i];
+    const int h = p[i].hop;
+    b.F = p[i].F;
+    b.cand = p[i].cand;
+    b.kcnt = p[i].kcnt;
+    b.prev_cand = p[i].prev_cand;
+    b.prev_kcnt = p[i].prev_kcnt;
+    b.prev_bptr = p[i].prev_bptr;
+    b.prev_bsrc = p[i].prev_bsrc;
+    b.bptr = p[i].bptr;
+    b.pos_of = ws[i]->pos_of;
+    b.sc = ws[i]->scal;
+    b.tiles = h < ws[i]->L ? ws[i]->tile_state + ws[i]->tile_off[h] : nullptr;
+    if (h > 0) {
+      b.prev_tiles = ws[i]->tile_state + ws[i]->tile_off[h - 1];
+      b.prev_ntiles = ws[i]->tile_off[h] - ws[i]->tile_off[h - 1];
+    }
   }
+  return a;
+}
+
+}  // namespace
+
+void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
+  const HopLaunch a = hop_launch(ctx, ws, p, n);
   // resident blocks per SM of the sampling grids: 8 for one batch per call; 2 inside a
-  // dci_sample_gather_many group, whose batches sample concurrently (measured)
+  // dci_sample_gather_many group (measured)
   static const int forced = [] {
     const char* e = getenv("DCI_SAMPLE_BPS");
     return e ? atoi(e) : 0;
   }();
-  const int bps = forced > 0 ? forced : (ws->in_group ? 2 : 8);
+  const int bps = forced > 0 ? forced : (ws[0]->in_group ? 2 : 8);
   // Grid: persistent (SM count x resident blocks), but no larger than the worst-case frontier of
   // this hop needs (small frontiers would otherwise start hundreds of idle blocks); the fused
   // relabel of hop h-1 (|F_{h-1}| * f_{h-1} items) is covered by the grid-stride loops either way.
-  const int64_t cap = std::max<int64_t>(ws->hop_cap[p.hop], 1);
+  int64_t cap = 0;
+  for (int i = 0; i < n; ++i) cap += ws[i]->hop_cap[p[0].hop];
+  cap = std::max<int64_t>(cap, 1);
   auto sized = [&](int persistent, int64_t nodes_per_block) {
     const int64_t need = (cap + nodes_per_block - 1) / nodes_per_block;
     return (int)std::max<int64_t>(1, std::min<int64_t>(persistent, need));
   };
+  const int f = p[0].f;
   int gsz = 1;
-  while (gsz < p.f) gsz <<= 1;
+  while (gsz < f) gsz <<= 1;
   auto go = [&](auto kern) {
     kern<<<sized(persistent_grid(ctx, kern, 256, bps), 256 / gsz), 256, 0, s>>>(a);
   };
-  if (p.f > 32) {
+  if (f > 32) {
     int fp2 = 1;
-    while (fp2 < p.f) fp2 <<= 1;
+    while (fp2 < f) fp2 <<= 1;
     const size_t smem = (size_t)kWideWarps * fp2 * sizeof(int32_t);
     k_sample_hop_wide<<<sized(persistent_grid(ctx, k_sample_hop_wide, 32 * kWideWarps, 16), kWideWarps),
                         32 * kWideWarps, smem, s>>>(a);
-  } else if (p.f <= 1)
+  } else if (f <= 1)
     go(k_sample_hop<1>);
-  else if (p.f <= 2)
+  else if (f <= 2)
     go(k_sample_hop<2>);
-  else if (p.f <= 4)
+  else if (f <= 4)
     go(k_sample_hop<4>);
-  else if (p.f <= 8)
+  else if (f <= 8)
     go(k_sample_hop<8>);
-  else if (p.f <= 16)
+  else if (f <= 16)
     go(k_sample_hop<16>);
   else
     go(k_sample_hop<32>);
   ++ctx->launches;
 }
 
-void launch_scan_hop(dci_ctx* ctx, dci_workspace* ws, const HopParams& p, cudaStream_t s) {
-  ScanArgs a{ws->pos_of, ws->scal, ws->tile_state + ws->tile_off[p.hop], ctx->N, p};
-  const int64_t tiles = (ws->hop_cap[p.hop] + kScanTile - 1) / kScanTile;
+void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
+  const HopLaunch a = hop_launch(ctx, ws, p, n);
+  int64_t tiles = 0;
+  for (int i = 0; i < n; ++i) tiles += (ws[i]->hop_cap[p[0].hop] + kScanTile - 1) / kScanTile;
   int64_t grid = persistent_grid(ctx, k_scan_hop, kScanTile, 8);
   if (tiles < grid) grid = tiles > 0 ? tiles : 1;
   k_scan_hop<<<(unsigned)grid, kScanTile, 0, s>>>(a);
+  ++ctx->launches;
+}
+
+void launch_hop_epilogue(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
+  const HopLaunch a = hop_launch(ctx, ws, p, n);
+  int64_t items = 0;
+  for (int i = 0; i < n; ++i) items += ws[i]->hop_cap[p[0].hop - 1] * p[0].prev_f;
+  const int64_t need = std::max<int64_t>(1, (items + 255) / 256);
+  const int grid = (int)std::min<int64_t>(persistent_grid(ctx, k_hop_epilogue, 256, 8), need);
+  k_hop_epilogue<<<grid, 256, 0, s>>>(a);
   ++ctx->launches;
 }
 
