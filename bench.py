@@ -451,6 +451,7 @@ def run_ours(args):
     e_sizes = torch.zeros((nws, per, L + 1), dtype=torch.int64).pin_memory()
     e_cnt = torch.zeros((nws, per, 4), dtype=torch.int64).pin_memory()
     e_st = torch.zeros((nws, per), dtype=torch.int32).pin_memory()
+    e_res = [dci.result_buffer(per) for _ in range(nws)]
     for w in all_ws:
         w.set_profiling(False)
 
@@ -458,8 +459,8 @@ def run_ours(args):
         w = i % nws
         if G:
             sd = [pinned_seeds[(i * per + j) % len(pinned_seeds)] for j in range(per)]
-            dci.sample_gather_many_host(ctx, wss[w], sd, fan, synth.SAMPLE_SEED, outs[w], e_sizes[w], e_cnt[w],
-                                        e_st[w], stream=streams[w])
+            dci.sample_gather_many_host(ctx, wss[w], sd, fan, synth.SAMPLE_SEED, outs[w], e_res[w],
+                                        stream=streams[w])
         else:
             dci.sample_gather_host(ctx, wss[w][0], pinned_seeds[i % len(pinned_seeds)], fan, synth.SAMPLE_SEED,
                                    outs[w][0], e_sizes[w, 0], e_cnt[w, 0], e_st[w, 0], stream=streams[w])
@@ -535,7 +536,7 @@ def run_ours(args):
                          % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
                             avg_fl * D * 4 / 1e6)},
         "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
-                "d2h_bytes_per_step": 8 * (L + 1) + 8 * 4 + 4},
+                "d2h_bytes_per_step": (8 * dci.RESULT_WORDS) if G else (8 * (L + 1) + 8 * 4 + 4)},
         "gpu_launches": int(tot[1]),
         "roofline": {"bound": "host-link" if host_bound else "hbm",
                      "kernel": kernel,

@@ -152,13 +152,22 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
                                   const int32_t* B, const int32_t* fanouts, int32_t L, uint64_t seed,
                                   const dci_batch_out* outs, void* stream);
 
+/* Per-batch results copied back to the host by dci_sample_gather_many_host. */
+typedef struct dci_batch_result {
+  int64_t sizes[DCI_MAX_LAYERS + 1]; /* |F_0| .. |F_L| (entries past L unspecified) */
+  uint64_t counters[4];              /* adj_hit, adj_miss, feat_hit, feat_miss */
+  int32_t status;                    /* DCI_OK, DCI_ESEED or DCI_EDUP */
+  int32_t pad_;
+} dci_batch_result;
+
 /* End-to-end group variant: seeds_host[i] HOST int32[B[i]] (pinned for overlap) copied to the
- * workspaces' staging buffers on `stream`, then dci_sample_gather_many, then device->host copies
- * of sizes (int64[n][L+1]), counters (uint64[n][4]) and status (int32[n]) on `stream`. */
+ * workspaces' staging buffers on `stream`, then dci_sample_gather_many, then ONE device->host
+ * copy of all n results into results_host (HOST dci_batch_result[n], pinned for overlap), on
+ * `stream`; valid once the stream has been synchronised. */
 dci_status dci_sample_gather_many_host(dci_ctx* ctx, int32_t n, dci_workspace* const* ws,
                                        const int32_t* const* seeds_host, const int32_t* B, const int32_t* fanouts,
-                                       int32_t L, uint64_t seed, const dci_batch_out* outs, int64_t* sizes_host,
-                                       uint64_t* counters_host, int32_t* status_host, void* stream);
+                                       int32_t L, uint64_t seed, const dci_batch_out* outs,
+                                       dci_batch_result* results_host, void* stream);
 
 /* End-to-end variant: seeds_host is HOST memory (pinned for full overlap); the call
  * enqueues the host->device copy of the seeds, the batch, and device->host copies of

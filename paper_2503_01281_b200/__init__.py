@@ -84,7 +84,7 @@ def lib():
         "dci_sample_gather": [vp, vp, vp, i32, vp, i32, u64, C.POINTER(dci_batch_out), vp],
         "dci_sample_gather_host": [vp, vp, vp, i32, vp, i32, u64, C.POINTER(dci_batch_out), vp, vp, vp, vp],
         "dci_sample_gather_many": [vp, i32, vp, vp, vp, vp, i32, u64, vp, vp],
-        "dci_sample_gather_many_host": [vp, i32, vp, vp, vp, vp, i32, u64, vp, vp, vp, vp, vp],
+        "dci_sample_gather_many_host": [vp, i32, vp, vp, vp, vp, i32, u64, vp, vp, vp],
         "dci_presample": [vp, vp, i64, i32, vp, i32, u64, vp, vp, vp, vp, vp],
         "dci_allocate": [vp, u64, vp, vp, i32, i64, i64, C.POINTER(u64), C.POINTER(u64)],
         "dci_fill": [vp, vp, vp, u64, u64, vp],
@@ -341,10 +341,32 @@ def sample_gather_many(ctx: Context, wss, seeds_list, fanouts, seed: int, outs, 
                                         st.cuda_stream), "dci_sample_gather_many")
 
 
-def sample_gather_many_host(ctx: Context, wss, seeds_host_list, fanouts, seed: int, outs, sizes_host,
-                            counters_host, status_host, stream=None):
-    """dci_sample_gather_many_host: host (pinned) seeds in, sizes [n, L+1] / counters [n, 4] /
-    status [n] (pinned torch tensors) copied back on `stream`; valid after synchronising it."""
+MAX_LAYERS = 8
+RESULT_WORDS = MAX_LAYERS + 1 + 4 + 1  # dci_batch_result as int64 words: sizes[9], counters[4], status|pad
+
+
+def result_buffer(n: int):
+    """Pinned host buffer for n dci_batch_result records (int64 [n, RESULT_WORDS])."""
+    import torch
+    return torch.zeros((n, RESULT_WORDS), dtype=torch.int64).pin_memory()
+
+
+def parse_results(results_host, L: int):
+    """dci_batch_result records -> [{"sizes", "counters", "status"}] (after a stream sync)."""
+    r = results_host.numpy()
+    out = []
+    for row in r:
+        st = int(row[MAX_LAYERS + 5] & 0xFFFFFFFF)
+        out.append({"sizes": row[: L + 1].copy(), "counters": row[MAX_LAYERS + 1: MAX_LAYERS + 5].astype(np.uint64),
+                    "status": st - (1 << 32) if st >= 1 << 31 else st})
+    return out
+
+
+def sample_gather_many_host(ctx: Context, wss, seeds_host_list, fanouts, seed: int, outs, results_host=None,
+                            stream=None):
+    """dci_sample_gather_many_host: host (pinned) seeds in; every batch's sizes / counters /
+    status come back in ONE copy into results_host (see result_buffer / parse_results), valid
+    after synchronising `stream`."""
     n = len(wss)
     fan = np.ascontiguousarray(fanouts, np.int32)
     if stream is not None:
@@ -354,10 +376,10 @@ def sample_gather_many_host(ctx: Context, wss, seeds_host_list, fanouts, seed: i
     sd_arr = (C.c_void_p * n)(*[sd.data_ptr() for sd in seeds_host_list])
     b_arr = (C.c_int32 * n)(*[int(sd.numel()) for sd in seeds_host_list])
     out_arr = (dci_batch_out * n)(*[o.struct for o in outs])
+    assert results_host is None or (results_host.shape[0] >= n and results_host.shape[-1] == RESULT_WORDS)
     _check(lib().dci_sample_gather_many_host(ctx.handle, n, ws_arr, sd_arr, b_arr, _np_ptr(fan), len(fan), seed,
-                                             out_arr, sizes_host.data_ptr(), counters_host.data_ptr(),
-                                             status_host.data_ptr(), _stream_ptr(stream)),
-           "dci_sample_gather_many_host")
+                                             out_arr, results_host.data_ptr() if results_host is not None else None,
+                                             _stream_ptr(stream)), "dci_sample_gather_many_host")
 
 
 def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: int, out: BatchOut, sizes_host,

@@ -631,6 +631,7 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
   for (int i = 0; i < 3; ++i)
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
   if (w->gg_exec) cudaGraphExecDestroy(w->gg_exec);
+  if (w->stage) cudaFree(w->stage);
   free(w->gg_sig);
   if (w->live_ws) --*w->live_ws;
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
@@ -657,6 +658,7 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
       if (ws[j] == ws[i]) return fail(DCI_EINVAL, "a workspace appears twice in one group");
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ws[0]->staged = false;
   if (!gather_many_uses_tma(ctx, outs, n)) {
     // outputs that cannot take bulk stores: one batch after another on `stream`
     for (int i = 0; i < n; ++i) {
@@ -781,7 +783,13 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     DCI_CUDA(cudaStreamWaitEvent(gs, w0->ev_mid, 0));
   }
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[2], gs));
-  launch_gather_many(ctx, ws, outs, n, L, gs);
+  dci_batch_result* stage = nullptr;
+  if (w0->want_stage) {
+    if (!w0->stage) DCI_CUDA(cudaMalloc(&w0->stage, sizeof(dci_batch_result) * DCI_MAX_GROUP));
+    stage = w0->stage;
+    w0->staged = true;
+  }
+  launch_gather_many(ctx, ws, outs, n, L, stage, gs);
   if (tr) {
     DCI_CUDA(cudaEventRecord(tr->e[3], gs));
     tr->state |= 2;
@@ -796,8 +804,8 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
 
 dci_status dci_sample_gather_many_host(dci_ctx* ctx, int32_t n, dci_workspace* const* ws,
                                        const int32_t* const* seeds_host, const int32_t* B, const int32_t* fanouts,
-                                       int32_t L, uint64_t seed, const dci_batch_out* outs, int64_t* sizes_host,
-                                       uint64_t* counters_host, int32_t* status_host, void* stream) {
+                                       int32_t L, uint64_t seed, const dci_batch_out* outs,
+                                       dci_batch_result* results_host, void* stream) {
   if (!ctx || !ws || !seeds_host || !B || !outs) return fail(DCI_EINVAL, "null argument");
   if (n < 1 || n > DCI_MAX_GROUP) return fail(DCI_EINVAL, "n must be in [1, DCI_MAX_GROUP]");
   if (L < 1 || L > DCI_MAX_LAYERS) return fail(DCI_EINVAL, "L must be in [1, DCI_MAX_LAYERS]");
@@ -812,17 +820,23 @@ dci_status dci_sample_gather_many_host(dci_ctx* ctx, int32_t n, dci_workspace* c
       DCI_CUDA(cudaMemcpyAsync(ws[i]->seeds_stage, seeds_host[i], sizeof(int32_t) * B[i], cudaMemcpyHostToDevice, s));
     dseeds[i] = ws[i]->seeds_stage;
   }
+  // the group gather's last block also writes every batch's results into the first workspace's
+  // device staging block, so one copy brings them all back
+  ws[0]->want_stage = results_host != nullptr;
   dci_status st = dci_sample_gather_many(ctx, n, ws, dseeds, B, fanouts, L, seed, outs, stream);
-  if (st != DCI_OK) return st;
-  for (int i = 0; i < n; ++i) {
-    if (sizes_host)
-      DCI_CUDA(cudaMemcpyAsync(sizes_host + (int64_t)i * (L + 1), outs[i].sizes, sizeof(int64_t) * (L + 1),
+  const bool staged = ws[0]->want_stage && ws[0]->staged;
+  ws[0]->want_stage = false;
+  if (st != DCI_OK || !results_host) return st;
+  if (staged) {
+    DCI_CUDA(cudaMemcpyAsync(results_host, ws[0]->stage, sizeof(dci_batch_result) * n, cudaMemcpyDeviceToHost, s));
+  } else {  // batch-by-batch fallback path: per-batch copies
+    for (int i = 0; i < n; ++i) {
+      DCI_CUDA(cudaMemcpyAsync(results_host[i].sizes, outs[i].sizes, sizeof(int64_t) * (L + 1),
                                cudaMemcpyDeviceToHost, s));
-    if (counters_host)
-      DCI_CUDA(cudaMemcpyAsync(counters_host + 4 * i, outs[i].counters, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost,
-                               s));
-    if (status_host)
-      DCI_CUDA(cudaMemcpyAsync(status_host + i, outs[i].status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      DCI_CUDA(cudaMemcpyAsync(results_host[i].counters, outs[i].counters, sizeof(uint64_t) * 4,
+                               cudaMemcpyDeviceToHost, s));
+      DCI_CUDA(cudaMemcpyAsync(&results_host[i].status, outs[i].status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
   }
   return DCI_OK;
 }

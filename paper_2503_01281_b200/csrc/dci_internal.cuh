@@ -161,6 +161,9 @@ struct dci_workspace {
   void* gg_sig = nullptr;
   size_t gg_sig_len = 0;
   uint64_t gg_kernels = 0;
+  // dci_sample_gather_many_host: device block the group gather publishes all results into
+  dci_batch_result* stage = nullptr;
+  bool want_stage = false, staged = false;
   // host-side running totals of the event-timed stages (profiling on)
   uint64_t acc_timed = 0, acc_gather_launches = 0;
   double acc_sample_ms = 0.0, acc_gather_ms = 0.0;
@@ -214,7 +217,7 @@ bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out);
 // Multi-batch TMA gather (dci_sample_gather_many): every output takes bulk stores.
 bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t n);
 void launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n, int32_t L,
-                        cudaStream_t s);
+                        dci_batch_result* stage, cudaStream_t s);
 // Gather blocks per SM: the HBM-bound gather is given a small share of each SM when many
 // batches are in flight (their sampling kernels must co-reside), the whole SM when one is.
 int gather_blocks_per_sm(const dci_ctx* ctx);

@@ -288,6 +288,7 @@ struct TmaBatches {
   int32_t pitch;
   int32_t D;
   const float* hfeats;
+  dci_batch_result* stage;  // nullable: results of every batch, for one device->host copy
   TmaBatch b[kTmaMaxBatches];
 };
 
@@ -629,6 +630,12 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
       sc->counters[c] = 0;
     }
     *tb.out_status = __ldcg(&sc->status);
+    if (a.stage) {
+      dci_batch_result& r = a.stage[threadIdx.x];
+      for (int h = 0; h <= a.L; ++h) r.sizes[h] = tb.out_sizes[h];
+      for (int c = 0; c < 4; ++c) r.counters[c] = tb.out_counters[c];
+      r.status = *tb.out_status;
+    }
     sc->acc_batches += 1;
     sc->acc_seeds += (unsigned long long)B;
     sc->acc_rows += (unsigned long long)__ldcg(&sc->sizes[a.L]);
@@ -748,8 +755,9 @@ static void tma_launch(dci_ctx* ctx, const TmaBatches& tb, const dci_batch_out* 
 }
 
 void launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n, int32_t L,
-                        cudaStream_t s) {
+                        dci_batch_result* stage, cudaStream_t s) {
   TmaBatches tb = tma_batches(ctx, L);
+  tb.stage = stage;
   for (int i = 0; i < n; ++i) tma_add(&tb, ws[i], outs + i, nullptr);
   tma_launch(ctx, tb, outs, s);
 }

@@ -203,3 +203,25 @@ def test_many_stats_and_profiling(filled):
     else:
         assert read == 3 * rows
         assert sts[0]["gather_bytes"] == 3 * rows * (8 * D + 4)
+
+
+@pytest.mark.parametrize("ldx_pad", [0, 1])
+def test_many_host_results_in_one_copy(filled, ldx_pad):
+    """dci_sample_gather_many_host: host seeds in, all results back in one copy (or, on the
+    batch-by-batch fallback for unaligned X, per-batch copies into the same records)."""
+    ip, R, ft, ctx, cl, slot, fan, B = filled
+    batches = synth.inference_batches(ip, B)[:4]
+    batches[2] = batches[2][:5]
+    wss = [dci.workspace_create(ctx, B, fan) for _ in batches]
+    ldx = None if not ldx_pad else (ctx.D + 1 if (ctx.D + 1) % 4 else ctx.D + 2)
+    outs = [dci.BatchOut(ctx, B, fan, ldx=ldx) for _ in batches]
+    res = dci.result_buffer(len(batches))
+    st = torch.cuda.Stream()
+    dci.sample_gather_many_host(ctx, wss, [torch.from_numpy(b).pin_memory() for b in batches], fan,
+                                synth.SAMPLE_SEED, outs, res, stream=st)
+    st.synchronize()
+    for b, og, r in zip(batches, outs, dci.parse_results(res, len(fan))):
+        o = oracle.sample_gather(ip, R, ft, b, fan, synth.SAMPLE_SEED, cl, slot)
+        _assert_batch_equal(og.result(), o, len(fan))
+        assert np.array_equal(r["sizes"], o.sizes) and np.array_equal(r["counters"], o.counters)
+        assert r["status"] == 0
