@@ -372,7 +372,6 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
     tr->state |= 1;
   }
   if (serial) {
-    if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
     DCI_CUDA(cudaEventRecord(ws->ev_mid, s));
     DCI_CUDA(cudaStreamWaitEvent(ctx->gstream, ws->ev_mid, 0));
     if (prof) DCI_CUDA(cudaEventRecord(tr->e[2], ctx->gstream));
@@ -458,6 +457,10 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
   };
   c->h_indptr = static_cast<int64_t*>(malloc(sizeof(int64_t) * (N + 1)));
   if (!c->h_indptr) return bail(fail(DCI_ENOMEM, "host allocation failed"));
+  // the context's gather stream (group gathers and serial gathers run one at a time on it);
+  // created here so concurrent callers with distinct workspaces never race on it
+  if (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(DCI_ECUDA, "cudaStreamCreate(gather stream)"));
   memcpy(c->h_indptr, indptr, sizeof(int64_t) * (N + 1));
   cudaError_t e;
   e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_idx_orig), sizeof(int32_t) * std::max<int64_t>(E, 1),
@@ -777,7 +780,6 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   // one at a time; DCI_GATHER_SERIAL=0 puts it on `stream` instead) ----
   cudaStream_t gs = s;
   if (!gather_concurrent()) {
-    if (!ctx->gstream) DCI_CUDA(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
     gs = ctx->gstream;
     DCI_CUDA(cudaEventRecord(w0->ev_mid, s));
     DCI_CUDA(cudaStreamWaitEvent(gs, w0->ev_mid, 0));
