@@ -138,14 +138,20 @@ dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* see
 
 /* --------------------------------------------------------------------------------------
  * dci_sample_gather_many — the same S5..S8 for a group of n batches (1 <= n <= DCI_MAX_GROUP),
- * one workspace and one dci_batch_out per batch (distinct workspaces).  Batch i samples seeds[i]
- * (device int32[B[i]]) on its workspace's own stream, all i concurrently; then ONE feature-gather
- * launch (Blackwell bulk copies, cp.async.bulk, through a shared-memory ring) moves the rows of
- * every batch, on the context's gather stream, so group gathers run one at a time at full
- * bandwidth while the next group samples.  Results are identical to n dci_sample_gather calls
- * (O-6, O-7).  Asynchronous on `stream`: work enqueued on `stream` before the call happens before
- * the group, and work enqueued after it sees every output.  If an output cannot take bulk stores
- * (X NULL, ldx % 4 != 0 or X not 16-byte aligned) the batches run one by one on `stream`.
+ * one workspace and one dci_batch_out per batch (distinct workspaces, all with the call's L).
+ * Batch i samples seeds[i] (device int32[B[i]]).  Every sampling kernel covers all n batches
+ * (one hop / scan launch per hop for the whole group, captured once as a CUDA graph on ws[0]);
+ * then ONE feature-gather launch (Blackwell bulk copies, cp.async.bulk, through a shared-memory
+ * ring) moves the rows of every batch on the context's gather stream, so group gathers run one at
+ * a time while the next group samples.  When 2..16 batches together hold at least N rows, the
+ * gather sweeps node ids and reads each feature row ONCE for all batches holding it (P:170's
+ * hit/miss sources unchanged).  Results are identical to n dci_sample_gather calls (O-6, O-7;
+ * the draws do not depend on the batch, C4).  Asynchronous on `stream`: work enqueued on `stream`
+ * before the call happens before the group, and work enqueued after it sees every output; issue
+ * a workspace's groups in order on one stream.  If an output cannot take bulk stores (X NULL,
+ * ldx % 4 != 0 or X not 16-byte aligned) the batches run one by one on `stream`.  Timing
+ * (profiling on ws[0]): the group's sampling and its gather launch are each timed once and
+ * booked on ws[0] (dci_workspace_stats).
  * Errors: as dci_sample_gather per batch; DCI_EINVAL for n out of range or a repeated workspace.
  * ------------------------------------------------------------------------------------ */
 dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const* ws, const int32_t* const* seeds,
