@@ -42,11 +42,11 @@ def parse():
     ap.add_argument("--config", default="M2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--inflight", type=int, default=None,
-                    help="streams in flight (each with one batch, or one group of --group batches); default 3 "
+                    help="streams in flight (each with one batch, or one group of --group batches); default 2 "
                          "groups, or 6 single batches")
     ap.add_argument("--group", type=int, default=None,
                     help="batches per dci_sample_gather_many call (one TMA gather launch per group); 0 = one "
-                         "dci_sample_gather per batch.  Default (measured, DESIGN.md §9): 6 when the data is "
+                         "dci_sample_gather per batch.  Default (measured, DESIGN.md §9): 16 when the data is "
                          "HBM-resident (M1, M2), 0 for host-link-bound configs (M3, M4, M5)")
     ap.add_argument("--ldx", default="pitch", choices=["pitch", "line"],
                     help="X row stride: the 16-byte feature pitch, or rounded up to whole 128-byte lines")
@@ -368,8 +368,8 @@ def run_ours(args):
     batches = parallel.shard(synth.inference_batches(ip, B), rank, world)
     batches = [b for b in batches if len(b) == B] or batches
     seeds_dev = [torch.from_numpy(b).to(dev) for b in batches]
-    G = max(0, args.group) if args.group is not None else (6 if cfg.name.split("-")[0] in ("M1", "M2") else 0)
-    nws = max(1, args.inflight) if args.inflight is not None else (3 if G else 6)
+    G = max(0, args.group) if args.group is not None else (16 if cfg.name.split("-")[0] in ("M1", "M2") else 0)
+    nws = max(1, args.inflight) if args.inflight is not None else (2 if G else 6)
     per = max(1, G)  # batches per call
     wss = [[dci.workspace_create(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
     ldx = None if args.ldx == "pitch" else -(-cfg.D // 32) * 32

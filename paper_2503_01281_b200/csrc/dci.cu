@@ -395,6 +395,7 @@ void free_ctx(dci_ctx* c) {
   if (c->pre_ws) dci_workspace_destroy(c->pre_ws);
   if (c->pre_out_mem) cudaFree(c->pre_out_mem);
   if (c->gstream) cudaStreamDestroy(c->gstream);
+  if (c->gather_ev) cudaEventDestroy(c->gather_ev);
   if (c->d_dir) cudaFree(c->d_dir);
   if (c->d_acache) cudaFree(c->d_acache);
   release_feature_partitions(c);
@@ -459,7 +460,8 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
   if (!c->h_indptr) return bail(fail(DCI_ENOMEM, "host allocation failed"));
   // the context's gather stream (group gathers and serial gathers run one at a time on it);
   // created here so concurrent callers with distinct workspaces never race on it
-  if (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess)
+  if (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->gather_ev, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(DCI_ECUDA, "cudaStreamCreate(gather stream)"));
   memcpy(c->h_indptr, indptr, sizeof(int64_t) * (N + 1));
   cudaError_t e;
@@ -688,9 +690,9 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     dci_status st = stage_header(ctx, ws[i], seeds[i], B[i], seed, s);
     if (st != DCI_OK) return st;
   }
-  // ---- the group's sampling: every hop of all n batches is ONE launch (hop, scan), then one
-  // relabel of the last hop; captured as a CUDA graph on the first workspace, re-captured when
-  // the group (workspaces, outputs, fan-outs, caches) changes ----
+  // ---- the group's sampling: every hop of all n batches is ONE launch (hop, scan), captured as
+  // a CUDA graph on the first workspace, re-captured when the group (workspaces, outputs,
+  // fan-outs, caches) changes; the last hop's relabel follows the gather launch ----
   struct GroupSig {
     int32_t n, L;
     int32_t fan[DCI_MAX_LAYERS];
@@ -737,6 +739,11 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
       launch_scan_hop(ctx, ws, p, n, es);
       for (int i = 0; i < n; ++i) prev[i] = p[i];
     }
+  };
+  // the relabel of every batch's last hop: needed by the caller, not by the gather, so it runs
+  // on `stream` while the gather runs on the gather stream
+  auto enqueue_epilogue = [&](cudaStream_t es) {
+    HopParams p[DCI_MAX_GROUP];
     for (int i = 0; i < n; ++i) p[i] = epilogue_params(ws[i], L, fanouts, outs + i);
     launch_hop_epilogue(ctx, ws, p, n, es);
   };
@@ -765,6 +772,12 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
       w0->gg_sig_len = sizeof(GroupSig);
     }
   }
+  // phased schedule (default; DCI_PHASED=0 overlaps them): a group samples only after the previous
+  // group's gather has finished, so gathers and sampling alternate and each has the GPU to itself.
+  // Both are DRAM-bound, so overlapping them bought no throughput while it slowed
+  // each gather launch by ~20 %.
+  const bool phased = group_phased();
+  if (phased && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[0], s));
   if (use_graph) {
     ctx->launches += w0->gg_kernels;
@@ -792,6 +805,11 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     w0->staged = true;
   }
   launch_gather_many(ctx, ws, outs, n, L, stage, gs);
+  enqueue_epilogue(s);
+  if (phased) {
+    DCI_CUDA(cudaEventRecord(ctx->gather_ev, gs));
+    ctx->gather_ev_valid = true;
+  }
   if (tr) {
     DCI_CUDA(cudaEventRecord(tr->e[3], gs));
     tr->state |= 2;

@@ -94,6 +94,8 @@ struct dci_ctx {
   uint64_t presample_peak = 0;
   uint64_t launches = 0;
   cudaStream_t gstream = nullptr;  // shared gather stream (serial-gather mode)
+  cudaEvent_t gather_ev = nullptr;  // end of the last group gather (DCI_PHASED experiments)
+  bool gather_ev_valid = false;
   // live user workspaces (= batches the caller keeps in flight); shared with the workspaces so
   // either may be destroyed first
   std::shared_ptr<std::atomic<int>> live_ws = std::make_shared<std::atomic<int>>(0);
@@ -181,6 +183,10 @@ dci_status cuda_fail(cudaError_t e, const char* what);
     cudaError_t _e = (expr);                                            \
     if (_e != cudaSuccess) return ::dci::cuda_fail(_e, #expr);          \
   } while (0)
+
+// dci_sample_gather_many schedule: sampling of a group waits for the previous group's gather
+// (default) or overlaps it (DCI_PHASED=0)
+bool group_phased();
 
 // ---- kernel launchers (sample.cu / gather.cu / fill.cu) ----
 struct HopParams {

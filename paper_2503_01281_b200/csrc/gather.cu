@@ -652,6 +652,14 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
+bool group_phased() {
+  static const int mode = [] {
+    const char* e = getenv("DCI_PHASED");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return mode == 1;
+}
+
 bool gather_tma_mode() {
   static const int mode = [] {
     const char* e = getenv("DCI_GATHER");

@@ -81,6 +81,8 @@ struct HopLaunch {
   uint32_t pass;
   int32_t elem_policy;  // L2 policy of adjacency-cache element loads: 0 evict-last, 1 normal, 2 evict-first
   int32_t* edge_counts; // presample only (nullable, n = 1)
+  int32_t precheck;     // read the tag before the atomicMax (DCI_PRECHECK=1; measured slower on M2)
+  int32_t sweep;        // node-sweep sampling allowed (multi-batch hops covering >= N nodes)
   HopBatch b[DCI_MAX_GROUP];
 };
 
@@ -172,14 +174,43 @@ __device__ __forceinline__ void hop_prologue(const HopLaunch& a, const HopShared
   // relabel of hop h-1 (its scan has completed: kernel boundary); final ids are tagged
   const int pf = a.prev_f;
   const long long ptot = S.ppre[n];
-  for (long long q = tid; q < ptot; q += nthreads) {
-    const int b = batch_of(S.ppre, n, q);
-    const HopBatch& hb = a.b[b];
-    const int64_t ql = q - S.ppre[b];
-    const int64_t d = ql / pf;
-    const int s = (int)(ql - d * pf);
-    if (s < hb.prev_kcnt[d])
-      hb.prev_bsrc[hb.prev_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(hb.pos_of + hb.prev_cand[ql]));
+  // 4 independent items per thread and round, so their dependent loads (candidate -> tag) overlap
+  constexpr int U = 4;
+  int bh = 0;  // items only grow along a thread's loop: the batch index only advances
+  for (long long q0 = tid; q0 < ptot; q0 += U * nthreads) {
+    int bu[U];
+    int64_t du[U];
+    int su[U];
+    int32_t ku[U], cu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long q = q0 + u * nthreads;
+      ku[u] = 0;
+      if (q < ptot) {
+        while (bh + 1 < n && q >= S.ppre[bh + 1]) ++bh;
+        bu[u] = bh;
+        const HopBatch& hb = a.b[bu[u]];
+        const uint32_t ql = (uint32_t)(q - S.ppre[bu[u]]);  // < 2^31 per batch (|F_h| * (f + 1) < 2^31)
+        du[u] = ql / (uint32_t)pf;
+        su[u] = (int)(ql - (uint32_t)du[u] * (uint32_t)pf);
+        ku[u] = hb.prev_kcnt[du[u]];
+        cu[u] = hb.prev_cand[ql];
+      }
+    }
+    unsigned long long tu[U];
+    int32_t pu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (q0 + u * nthreads < ptot && su[u] < ku[u]) {
+        const HopBatch& hb = a.b[bu[u]];
+        tu[u] = __ldcg(hb.pos_of + cu[u]);
+        pu[u] = hb.prev_bptr[du[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q0 + u * nthreads < ptot && su[u] < ku[u])
+        a.b[bu[u]].prev_bsrc[pu[u] + su[u]] = (int32_t)(0xFFFFFFFFu - (uint32_t)tu[u]);
   }
   const long long ttot = S.tpre[n];
   for (long long t = tid; t < ttot; t += nthreads) {
@@ -187,6 +218,136 @@ __device__ __forceinline__ void hop_prologue(const HopLaunch& a, const HopShared
     a.b[b].prev_tiles[t - S.tpre[b]] = 0ull;
   }
   if (tid < n) a.b[tid].sc->tickets[h - 1] = 0;
+}
+
+// Rank selection of one dst group (O-4): lane gl of the group returns the gl-th smallest chosen
+// rank (its output position is gl); deg <= f: ranks 0..deg-1 in order.  Must be called by the
+// whole warp (shuffles); groups with floyd == false just return gl.
+template <int G>
+__device__ __forceinline__ int32_t select_rank(int gl, int lane, unsigned gmask, int f, int32_t deg, bool floyd,
+                                               unsigned long long seed, uint32_t pass, uint32_t h, uint32_t v) {
+  int32_t rank = gl;
+  if (__any_sync(0xffffffffu, floyd)) {
+    int32_t chosen = 0, j = 0;
+    const bool draw = floyd && gl < f;
+    if (draw) {
+      j = deg - f + gl;
+      const uint64_t u = philox_u64(seed, pass, h, v, (uint32_t)gl);
+      chosen = (int32_t)__umul64hi(u, (uint64_t)(j + 1));
+    }
+    // Floyd: slot i keeps t_i unless an earlier slot already chose it, then takes j_i.  While
+    // no earlier slot collided, chosen[k] = t_k, so slot i collides iff t_i repeats an earlier
+    // t: when all of a group's draws are distinct (most groups when deg >> f) nothing changes,
+    // and one __match_any_sync over (group, t) detects that.  Otherwise resolve in slot order.
+    const unsigned long long key = draw ? (((unsigned long long)(lane / G) << 32) | (uint32_t)chosen)
+                                        : (0xFFFFFFFF00000000ull | (unsigned)lane);
+    const bool dup = __popc(__match_any_sync(0xffffffffu, key)) > 1;
+    if (__any_sync(0xffffffffu, dup)) {
+      for (int i = 1; i < f; ++i) {
+        const int32_t ti = __shfl_sync(0xffffffffu, chosen, i, G);
+        const unsigned coll = __ballot_sync(0xffffffffu, gl < i && chosen == ti) & gmask;
+        if (gl == i && coll) chosen = j;
+      }
+    }
+    // ascending order within the group: bitonic network over the G lanes (pads sort last)
+    int32_t val = draw ? chosen : (floyd ? 0x7FFFFFFF : gl);
+#pragma unroll
+    for (int kk = 2; kk <= G; kk <<= 1) {
+#pragma unroll
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        const int32_t o = __shfl_xor_sync(0xffffffffu, val, jj, G);
+        const bool keep_min = ((gl & jj) == 0) == ((gl & kk) == 0);
+        val = keep_min ? min(val, o) : max(val, o);
+      }
+    }
+    if (floyd) rank = val;
+  }
+  return rank;
+}
+
+// ------------------------------------------------------------------------------------
+// Node-sweep sampling of a multi-batch hop (2+ batches whose frontiers together hold >= N nodes):
+// the draws of (node v, hop h) do not depend on the batch (C4), so each node is sampled ONCE
+// (one directory read, one selection, one element read per slot) and the result is written into
+// every batch whose F_h holds v, at that batch's position d_b (v's tag in the batch's table:
+// current epoch and id < |F_h(b)|).  The insertions into each batch's table and its candidate
+// array are exactly those of the frontier-order loop, so the scan that follows sees the same
+// state.  Cuts the hop's random element reads from sum_b |F_h(b)| * f to |union| * f.
+// ------------------------------------------------------------------------------------
+constexpr int kSweepChunks = DCI_MAX_GROUP / 4;  // batches per probing lane (G >= 4)
+
+template <int G>
+__device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, int64_t warp_id, int64_t nwarps,
+                                             uint64_t keep, uint64_t epol) {
+  const int h = a.hop, f = a.f, n = a.n;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+  const int GPW = 32 / G;
+  for (int64_t vbase = warp_id * GPW; vbase < a.N; vbase += nwarps * GPW) {
+    const int64_t vv = vbase + lane / G;
+    const bool in = vv < a.N;
+    const int32_t v = (int32_t)vv;
+    // which batches hold v in F_h, and where: lane gl probes batches gl, gl + G, ... (G >= 4, so
+    // at most 4 per lane) and keeps the local ids for the write loop below
+    unsigned pm = 0;
+    uint32_t dd[kSweepChunks];
+#pragma unroll
+    for (int c = 0; c < kSweepChunks; ++c) {
+      const int bb = c * G + gl;
+      bool pres = false;
+      dd[c] = 0;
+      if (c * G < n) {
+        if (in && bb < n) {
+          const unsigned long long t = __ldcg(a.b[bb].pos_of + v);
+          dd[c] = 0xFFFFFFFFu - (uint32_t)t;
+          pres = (t >> 32) == (S.ehi[bb] >> 32) && dd[c] < (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
+        }
+        const unsigned bal = (__ballot_sync(0xffffffffu, pres) & gmask) >> gbase;
+        pm |= bal << (c * G);
+      }
+    }
+    int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
+    if (pm) {
+      const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
+      e0 = ld_keep_v4(ep, keep);
+      e1 = ld_keep_v4(ep + 1, keep);
+    }
+    const int64_t host_off = ((int64_t)(uint32_t)e0.y << 32) | (uint32_t)e0.x;
+    const int64_t cache_off = ((int64_t)(uint32_t)e0.w << 32) | (uint32_t)e0.z;
+    const int32_t deg = e1.x;
+    const int32_t cached_len = e1.y;
+    const int k = deg < f ? deg : f;
+    const bool floyd = deg > f;
+    const int32_t rank = select_rank<G>(gl, lane, gmask, f, deg, floyd, S.seed[0], a.pass, (uint32_t)h, (uint32_t)v);
+    const bool valid = pm && gl < k;
+    int32_t x = -1;
+    bool hit = false;
+    if (valid) {
+      hit = rank < cached_len;
+      x = hit ? ld_keep_i32(a.acache + cache_off + rank, epol) : ld_host_i32(a.uidx + host_off + rank);
+    }
+    // write the sample into every batch holding v (local id shuffled from the probing lane)
+#pragma unroll
+    for (int c = 0; c < kSweepChunks; ++c) {
+      if (c * G >= n) break;
+      for (int r = 0; r < G && c * G + r < n; ++r) {
+        const int bb = c * G + r;
+        const uint32_t d = __shfl_sync(0xffffffffu, dd[c], gbase + r);
+        if (!((pm >> bb) & 1u)) continue;
+        const HopBatch& hb = a.b[bb];
+        if (gl < f) hb.cand[(int64_t)d * f + gl] = x;
+        if (gl == 0) hb.kcnt[d] = k;
+        if (valid) {
+          const uint32_t n_h = (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
+          const unsigned long long tag = S.ehi[bb] | (0xFFFFFFFFu - (n_h + d * (uint32_t)f + (uint32_t)gl));
+          if (!a.precheck || __ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
+          atomicAdd(&S.cnt[bb][hit ? 0 : 1], 1u);
+        }
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -226,23 +387,47 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   const int64_t nwarps = nthreads >> 5;
   const uint64_t keep = policy_evict_last();
   const uint64_t epol = policy_by(a.elem_policy);
-  for (int64_t dbase = warp_id * GPW; dbase < total; dbase += nwarps * GPW) {
+  if (G >= 4 && a.sweep && a.n >= 2 && total >= a.N && a.edge_counts == nullptr) {
+    sample_sweep<(G >= 4 ? G : 4)>(a, S, warp_id, nwarps, keep, epol);
+    hop_shared_flush(a, S);
+    return;
+  }
+  // Software pipeline over this warp's dst groups: the frontier id of iteration i+2 and the
+  // directory entry of iteration i+1 are in flight while iteration i draws, reads its elements and
+  // inserts them, so the dependent F -> dir -> element chain costs one latency per iteration.
+  const int64_t stride = nwarps * GPW;
+  auto fetch_v = [&](int64_t db, int bb) -> int32_t {  // bb: a batch index <= that of db
+    const int64_t qq = db + lane / G;
+    if (qq >= total) return -1;
+    while (bb + 1 < a.n && qq >= S.pre[bb + 1]) ++bb;
+    return S.Fin[bb][qq - S.pre[bb]];
+  };
+  auto fetch_dir = [&](int32_t vv, int4& x0, int4& x1) {
+    x0 = make_int4(0, 0, 0, 0);
+    x1 = make_int4(0, 0, 0, 0);
+    if (vv >= 0 && (int64_t)vv < a.N) {
+      const int4* ep = reinterpret_cast<const int4*>(a.dir + vv);
+      x0 = ld_keep_v4(ep, keep);
+      x1 = ld_keep_v4(ep + 1, keep);
+    }
+  };
+  int64_t dbase = warp_id * GPW;
+  int b = 0;
+  int32_t v = fetch_v(dbase, 0);
+  int4 e0, e1;
+  fetch_dir(v, e0, e1);
+  int32_t v_next = fetch_v(dbase + stride, 0);
+  for (; dbase < total; dbase += stride) {
+    int4 e0_next, e1_next;
+    fetch_dir(v_next, e0_next, e1_next);
+    const int32_t v_next2 = fetch_v(dbase + 2 * stride, b);
     const int64_t q = dbase + lane / G;
     const bool active = q < total;
-    const int b = active ? batch_of(S.pre, a.n, q) : 0;
+    if (active)  // q only grows along a warp's loop: advance the batch index
+      while (b + 1 < a.n && q >= S.pre[b + 1]) ++b;
     const HopBatch& hb = a.b[b];
     const int64_t d = q - S.pre[b];
     const int64_t n_h = S.pre[b + 1] - S.pre[b];
-    int32_t v = -1;
-    int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
-    if (active) {
-      v = S.Fin[b][d];
-      if (v >= 0 && (int64_t)v < a.N) {
-        const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
-        e0 = ld_keep_v4(ep, keep);
-        e1 = ld_keep_v4(ep + 1, keep);
-      }
-    }
     const int64_t host_off = ((int64_t)(uint32_t)e0.y << 32) | (uint32_t)e0.x;
     const int64_t cache_off = ((int64_t)(uint32_t)e0.w << 32) | (uint32_t)e0.z;
     const int32_t deg = e1.x;
@@ -250,33 +435,8 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     const int k = deg < f ? deg : f;
     const bool floyd = deg > f;
 
-    int32_t rank = gl;
-    int pos = gl;
-    if (__any_sync(0xffffffffu, floyd)) {
-      int32_t chosen = 0, j = 0;
-      if (floyd && gl < f) {
-        j = deg - f + gl;
-        const uint64_t u = philox_u64(S.seed[b], a.pass, (uint32_t)h, (uint32_t)v, (uint32_t)gl);
-        chosen = (int32_t)__umul64hi(u, (uint64_t)(j + 1));
-      }
-      // Floyd: slot i keeps t_i unless an earlier slot already chose it, then takes j_i.
-      for (int i = 1; i < f; ++i) {
-        const int32_t ti = __shfl_sync(0xffffffffu, chosen, i, G);
-        const unsigned coll = __ballot_sync(0xffffffffu, gl < i && chosen == ti) & gmask;
-        if (gl == i && coll) chosen = j;
-      }
-      // ascending order: position = number of smaller chosen ranks in the group
-      int cnt = 0;
-      for (int i = 0; i < f; ++i) {
-        const int32_t c = __shfl_sync(0xffffffffu, chosen, i, G);
-        cnt += (c < chosen) ? 1 : 0;
-      }
-      if (floyd) {
-        rank = chosen;
-        pos = cnt;
-      }
-    }
-
+    const int32_t rank = select_rank<G>(gl, lane, gmask, f, deg, floyd, S.seed[b], a.pass, (uint32_t)h, (uint32_t)v);
+    const int pos = gl;
     const bool valid = active && gl < k;
     int32_t x = -1;
     if (valid) {
@@ -291,9 +451,13 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     if (active && gl == 0) hb.kcnt[d] = k;
     if (valid) {
       const unsigned long long tag = S.ehi[b] | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
-      if (__ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
+      if (!a.precheck || __ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
       if (a.edge_counts) atomicAdd(a.edge_counts + host_off + rank, 1);
     }
+    v = v_next;
+    e0 = e0_next;
+    e1 = e1_next;
+    v_next = v_next2;
   }
   hop_shared_flush(a, S);
 }
@@ -610,6 +774,16 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
   a.pass = p[0].pass;
   a.elem_policy = elem_policy;
   a.edge_counts = p[0].edge_counts;
+  static const int precheck = [] {
+    const char* e = getenv("DCI_PRECHECK");
+    return e ? atoi(e) : 0;
+  }();
+  a.precheck = precheck;
+  static const int sweep = [] {
+    const char* e = getenv("DCI_SAMPLE_SWEEP");
+    return e ? atoi(e) : 1;
+  }();
+  a.sweep = sweep;
   for (int i = 0; i < n; ++i) {
     HopBatch& b = a.b[i];
     const int h = p[i].hop;
@@ -636,13 +810,13 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
   const HopLaunch a = hop_launch(ctx, ws, p, n);
-  // resident blocks per SM of the sampling grids: 8 for one batch per call; 2 inside a
-  // dci_sample_gather_many group (measured)
+  // resident blocks per SM of the sampling grids: 8 (the whole GPU); 2 when a group's sampling
+  // overlaps the previous group's gather (DCI_PHASED=0; measured)
   static const int forced = [] {
     const char* e = getenv("DCI_SAMPLE_BPS");
     return e ? atoi(e) : 0;
   }();
-  const int bps = forced > 0 ? forced : (ws[0]->in_group ? 2 : 8);
+  const int bps = forced > 0 ? forced : (ws[0]->in_group && !group_phased() ? 2 : 8);
   // Grid: persistent (SM count x resident blocks), but no larger than the worst-case frontier of
   // this hop needs (small frontiers would otherwise start hundreds of idle blocks); the fused
   // relabel of hop h-1 (|F_{h-1}| * f_{h-1} items) is covered by the grid-stride loops either way.
