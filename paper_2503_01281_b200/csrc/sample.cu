@@ -285,11 +285,33 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
   const int gbase = lane & ~(G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const int GPW = 32 / G;
-  for (int64_t vbase = warp_id * GPW; vbase < a.N; vbase += nwarps * GPW) {
+  // the next node group's table probes and directory entry (contiguous: ids are consecutive)
+  // are loaded while the current group samples and writes
+  const int64_t vstride = nwarps * GPW;
+  auto probe = [&](int64_t vb, unsigned long long* t, int4& x0, int4& x1) {
+    const int64_t vv = vb + lane / G;
+    x0 = make_int4(0, 0, 0, 0);
+    x1 = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < kSweepChunks; ++c) {
+      const int bb = c * G + gl;
+      t[c] = (vv < a.N && bb < n) ? __ldcg(a.b[bb].pos_of + vv) : 0ull;
+    }
+    if (vv < a.N) {
+      const int4* ep = reinterpret_cast<const int4*>(a.dir + vv);
+      x0 = ld_keep_v4(ep, keep);
+      x1 = ld_keep_v4(ep + 1, keep);
+    }
+  };
+  unsigned long long tc[kSweepChunks], tn[kSweepChunks];
+  int4 e0, e1, e0n, e1n;
+  probe(warp_id * GPW, tc, e0, e1);
+  for (int64_t vbase = warp_id * GPW; vbase < a.N; vbase += vstride) {
+    probe(vbase + vstride, tn, e0n, e1n);
     const int64_t vv = vbase + lane / G;
     const bool in = vv < a.N;
     const int32_t v = (int32_t)vv;
-    // which batches hold v in F_h, and where: lane gl probes batches gl, gl + G, ... (G >= 4, so
+    // which batches hold v in F_h, and where: lane gl probed batches gl, gl + G, ... (G >= 4, so
     // at most 4 per lane) and keeps the local ids for the write loop below
     unsigned pm = 0;
     uint32_t dd[kSweepChunks];
@@ -297,22 +319,17 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
     for (int c = 0; c < kSweepChunks; ++c) {
       const int bb = c * G + gl;
       bool pres = false;
-      dd[c] = 0;
+      dd[c] = 0xFFFFFFFFu - (uint32_t)tc[c];
       if (c * G < n) {
-        if (in && bb < n) {
-          const unsigned long long t = __ldcg(a.b[bb].pos_of + v);
-          dd[c] = 0xFFFFFFFFu - (uint32_t)t;
-          pres = (t >> 32) == (S.ehi[bb] >> 32) && dd[c] < (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
-        }
+        if (in && bb < n)
+          pres = (tc[c] >> 32) == (S.ehi[bb] >> 32) && dd[c] < (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
         const unsigned bal = (__ballot_sync(0xffffffffu, pres) & gmask) >> gbase;
         pm |= bal << (c * G);
       }
     }
-    int4 e0 = make_int4(0, 0, 0, 0), e1 = make_int4(0, 0, 0, 0);
-    if (pm) {
-      const int4* ep = reinterpret_cast<const int4*>(a.dir + v);
-      e0 = ld_keep_v4(ep, keep);
-      e1 = ld_keep_v4(ep + 1, keep);
+    if (!pm) {  // no batch holds v: nothing to sample (its directory entry is simply unused)
+      e0 = make_int4(0, 0, 0, 0);
+      e1 = make_int4(0, 0, 0, 0);
     }
     const int64_t host_off = ((int64_t)(uint32_t)e0.y << 32) | (uint32_t)e0.x;
     const int64_t cache_off = ((int64_t)(uint32_t)e0.w << 32) | (uint32_t)e0.z;
@@ -347,6 +364,10 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
         }
       }
     }
+#pragma unroll
+    for (int c = 0; c < kSweepChunks; ++c) tc[c] = tn[c];
+    e0 = e0n;
+    e1 = e1n;
   }
 }
 
