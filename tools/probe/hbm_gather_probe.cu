@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <numeric>
 #include <random>
+#include <type_traits>
 #include <vector>
 
 #define CK(x)                                                                   \
@@ -166,9 +167,10 @@ int main(int argc, char** argv) {
         printf("{\"pattern\": \"%s\", \"bps\": %d, \"rows_per_warp\": %d, \"us\": %.1f, \"GBps\": %.1f}\n", pt.name,
                bps, rows, t * 1e3, bytes / t / 1e6);
       }
-  // multi-destination writes (row16 <= 160 only)
-  if (row16 <= 160) {
-    constexpr int M = 5;
+  // multi-destination writes (row16 <= 160 only): a row read once, written to M random rows of M
+  // outputs (the node-sweep gather's pattern; M ~ 0.61 x group size on M2)
+  auto multi = [&](auto mconst) {
+    constexpr int M = decltype(mconst)::value;
     int4* mdst;
     CK(cudaMalloc(&mdst, (size_t)M * n * P));
     const double mbytes = (double)n * P * (1 + M);
@@ -177,6 +179,14 @@ int main(int argc, char** argv) {
       printf("{\"pattern\": \"read1_write%d\", \"bps\": %d, \"us\": %.1f, \"GBps\": %.1f}\n", M, bps, t * 1e3,
              mbytes / t / 1e6);
     }
+    CK(cudaFree(mdst));
+  };
+  if (row16 <= 160) {
+    multi(std::integral_constant<int, 5>{});
+    multi(std::integral_constant<int, 10>{});
+    constexpr int M = 5;
+    int4* mdst;
+    CK(cudaMalloc(&mdst, (size_t)M * n * P));
     // pure sequential write of the same bytes (memset)
     float t = timeit([&] { CK(cudaMemsetAsync(mdst, 0, (size_t)M * n * P)); });
     printf("{\"pattern\": \"memset\", \"us\": %.1f, \"GBps\": %.1f}\n", t * 1e3, (double)M * n * P / t / 1e6);
