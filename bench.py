@@ -50,6 +50,7 @@ def parse():
                          "HBM-resident (M1, M2), 0 for host-link-bound configs (M3, M4, M5)")
     ap.add_argument("--ldx", default="pitch", choices=["pitch", "line"],
                     help="X row stride: the 16-byte feature pitch, or rounded up to whole 128-byte lines")
+    ap.add_argument("--repeats", type=int, default=5, help="timed regions of K steps (value = median)")
     ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
     ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
     ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
@@ -402,28 +403,39 @@ def run_ours(args):
     parallel.barrier(local)
     torch.cuda.synchronize()
     main = torch.cuda.current_stream(dev)
-    ev_start = torch.cuda.Event(enable_timing=True)
-    ev_end = torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.launches
-    torch.cuda.nvtx.range_push("timed")
-    ev_start.record(main)
-    for s in streams:
-        s.wait_event(ev_start)
-    h0 = time.perf_counter()
-    for i in range(n_warm, nsteps_total):
-        step(i)
-    host_s = time.perf_counter() - h0
-    for s in streams:
-        e = torch.cuda.Event()
-        e.record(s)
-        main.wait_event(e)
-    ev_end.record(main)
-    torch.cuda.synchronize()
-    torch.cuda.nvtx.range_pop()
-    launches = ctx.launches - launches0
-    ms_local = ev_start.elapsed_time(ev_end)
-    parallel.barrier(local)
-    ms = parallel.max_over_ranks(ms_local, device=dev)
+    # the K timed steps, repeated R times (as the paper does): value = median
+    R = max(1, args.repeats)
+    ms_list, host_s, launches = [], 0.0, 0
+    for rep in range(R):
+        parallel.barrier(local)
+        torch.cuda.synchronize()
+        ev_start = torch.cuda.Event(enable_timing=True)
+        ev_end = torch.cuda.Event(enable_timing=True)
+        launches0 = ctx.launches
+        torch.cuda.nvtx.range_push("timed")
+        ev_start.record(main)
+        for s in streams:
+            s.wait_event(ev_start)
+        h0 = time.perf_counter()
+        off = rep * n_calls
+        for i in range(n_warm + off, nsteps_total + off):
+            step(i)
+        host_s += time.perf_counter() - h0
+        for s in streams:
+            e = torch.cuda.Event()
+            e.record(s)
+            main.wait_event(e)
+        ev_end.record(main)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+        launches += ctx.launches - launches0
+        ms_local = ev_start.elapsed_time(ev_end)
+        parallel.barrier(local)
+        ms_list.append(parallel.max_over_ranks(ms_local, device=dev))
+    ms = float(np.median(ms_list))
+    ms_tot = float(np.sum(ms_list))
+    host_s /= R
+    launches //= R
     sts = [w.stats(reset=True) for w in all_ws]
     D = cfg.D
     rows = sum(st["frontier_rows"] for st in sts)
@@ -437,11 +449,12 @@ def run_ours(args):
     alg_bytes = float(sum(st["gather_bytes"] for st in sts))
     tot = parallel.sum_over_ranks([sum(st["seeds"] for st in sts), launches, rows, alg_bytes, g_ms, s_ms, n_timed,
                                    n_glaunch, rows_read, *cn.tolist()], device=dev)
-    seeds_all = tot[0]
+    seeds_all = tot[0] / R  # per timed region
     value = seeds_all / (ms / 1e3)
+    rep_values = [seeds_all / (m / 1e3) for m in ms_list]
     cn = tot[9:13]
     hit_rates = {"adj_hit_rate": cn[0] / max(1, cn[0] + cn[1]), "feat_hit_rate": cn[2] / max(1, cn[2] + cn[3]),
-                 "adj_accesses_per_seed": (cn[0] + cn[1]) / max(1, seeds_all)}
+                 "adj_accesses_per_seed": (cn[0] + cn[1]) / max(1, tot[0])}
     if args.profile_only:
         clk.stop()
         print(json.dumps({"profile_only": True, "value": value, "ms_per_step": ms / steps_eff, **hit_rates}))
@@ -526,12 +539,12 @@ def run_ours(args):
     kernel = ("k_gather_tma (group of %d: %s; route + feature gather, S7-S8)"
               % (G, "node sweep, each row read once per group" if frac_read < 0.999 else "rows")) if G else \
         "k_gather (fused route + relabel + feature gather, S7-S8)"
-    aggregate_gbs = bind_b / (ms / 1e3) / 1e9  # all gather launches over the timed wall time
-    host_link = {"feature_miss_GBps": host_b / (ms / 1e3) / 1e9, "peak_GBps": host_peak,
-                 "feature_frac": host_b / (ms / 1e3) / 1e9 / host_peak,
-                 "adj_miss_Mreads_per_s": cn[1] / (ms / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
+    aggregate_gbs = bind_b / (ms_tot / 1e3) / 1e9  # all gather launches over the timed wall time
+    host_link = {"feature_miss_GBps": host_b / (ms_tot / 1e3) / 1e9, "peak_GBps": host_peak,
+                 "feature_frac": host_b / (ms_tot / 1e3) / 1e9 / host_peak,
+                 "adj_miss_Mreads_per_s": cn[1] / (ms_tot / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
                  "peak_kind": host_kind}
-    avg_fl = tot[2] / max(1, steps_eff * world)
+    avg_fl = tot[2] / max(1, steps_eff * world * R)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gather_traffic.json")
     if os.path.exists(tfile):
@@ -554,6 +567,8 @@ def run_ours(args):
         "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
                 "d2h_bytes_per_step": (8 * dci.RESULT_WORDS) if G else (8 * (L + 1) + 8 * 4 + 4)},
         "gpu_launches": int(tot[1]),
+        "repeats": {"n": R, "median": value, "min": min(rep_values), "max": max(rep_values),
+                    "values": rep_values, "note": "value = median seeds/s over R timed regions of K steps each"},
         "roofline": {"bound": "host-link" if host_bound else "hbm",
                      "kernel": kernel,
                      "achieved": achieved_gbs, "peak": bind_peak,
@@ -562,7 +577,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": bind_b / n_launch, "launches": int(tot[7]),
                      "avg_gather_ms": tot[4] / n_launch, "avg_sample_ms": tot[5] / max(1, tot[6]),
                      "rows_read_per_row": frac_read,
-                     "gather_busy_frac": tot[4] / ms if ms > 0 else None,
+                     "gather_busy_frac": tot[4] / ms_tot if ms_tot > 0 else None,
                      "aggregate_achieved": aggregate_gbs, "aggregate_frac": aggregate_gbs / bind_peak,
                      "alone": None if alone is None or host_bound else dict(alone, frac=alone["achieved"] / bind_peak),
                      "note": "achieved = algorithmic bytes per gather launch / mean live launch time (CUDA events "
