@@ -594,6 +594,7 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
       if ((e = cudaEventCreate(&r.e[i])) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_mid, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->gseeds_ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
                          cudaHostAllocPortable)) != cudaSuccess)
     return bail(e, "cudaHostAlloc(header ring)");
@@ -637,6 +638,9 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
   if (w->gg_exec) cudaGraphExecDestroy(w->gg_exec);
   if (w->stage) cudaFree(w->stage);
+  if (w->gseeds_host) cudaFreeHost(w->gseeds_host);
+  if (w->gseeds_dev) cudaFree(w->gseeds_dev);
+  if (w->gseeds_ev) cudaEventDestroy(w->gseeds_ev);
   free(w->gg_sig);
   if (w->live_ws) --*w->live_ws;
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
@@ -832,13 +836,38 @@ dci_status dci_sample_gather_many_host(dci_ctx* ctx, int32_t n, dci_workspace* c
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   DeviceGuard g(ctx->device);
   const int32_t* dseeds[DCI_MAX_GROUP];
+  int64_t total = 0;
   for (int i = 0; i < n; ++i) {
     if (!ws[i]) return fail(DCI_EINVAL, "null workspace");
     if (B[i] < 0 || B[i] > ws[i]->max_batch) return fail(DCI_EINVAL, "B exceeds the workspace's max_batch");
     if (B[i] > 0 && !seeds_host[i]) return fail(DCI_EINVAL, "seeds_host is null");
-    if (B[i] > 0)
-      DCI_CUDA(cudaMemcpyAsync(ws[i]->seeds_stage, seeds_host[i], sizeof(int32_t) * B[i], cudaMemcpyHostToDevice, s));
-    dseeds[i] = ws[i]->seeds_stage;
+    total += B[i];
+  }
+  // all seeds of the group in ONE host->device copy: packed into the first workspace's pinned
+  // staging block (its previous copy has finished: event), then scattered by pointer offsets
+  dci_workspace* w0 = ws[0];
+  if (total > w0->gseeds_cap) {
+    if (w0->gseeds_host) cudaFreeHost(w0->gseeds_host);
+    if (w0->gseeds_dev) cudaFree(w0->gseeds_dev);
+    w0->gseeds_host = nullptr;
+    w0->gseeds_dev = nullptr;
+    w0->gseeds_cap = 0;
+    DCI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w0->gseeds_host), sizeof(int32_t) * total, cudaHostAllocDefault));
+    DCI_CUDA(cudaMalloc(&w0->gseeds_dev, sizeof(int32_t) * total));
+    w0->gseeds_cap = total;
+  }
+  if (total > 0) {
+    DCI_CUDA(cudaEventSynchronize(w0->gseeds_ev));
+    int64_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      if (B[i] > 0) memcpy(w0->gseeds_host + off, seeds_host[i], sizeof(int32_t) * B[i]);
+      dseeds[i] = w0->gseeds_dev + off;
+      off += B[i];
+    }
+    DCI_CUDA(cudaMemcpyAsync(w0->gseeds_dev, w0->gseeds_host, sizeof(int32_t) * total, cudaMemcpyHostToDevice, s));
+    DCI_CUDA(cudaEventRecord(w0->gseeds_ev, s));
+  } else {
+    for (int i = 0; i < n; ++i) dseeds[i] = ws[i]->seeds_stage;
   }
   // the group gather's last block also writes every batch's results into the first workspace's
   // device staging block, so one copy brings them all back

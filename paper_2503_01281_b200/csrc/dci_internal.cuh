@@ -166,6 +166,11 @@ struct dci_workspace {
   // dci_sample_gather_many_host: device block the group gather publishes all results into
   dci_batch_result* stage = nullptr;
   bool want_stage = false, staged = false;
+  // dci_sample_gather_many_host: the group's seeds packed for one host->device copy
+  int32_t* gseeds_host = nullptr;  // pinned
+  int32_t* gseeds_dev = nullptr;
+  int64_t gseeds_cap = 0;
+  cudaEvent_t gseeds_ev = nullptr;
   // host-side running totals of the event-timed stages (profiling on)
   uint64_t acc_timed = 0, acc_gather_launches = 0;
   double acc_sample_ms = 0.0, acc_gather_ms = 0.0;
