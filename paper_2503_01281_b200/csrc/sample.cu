@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   const int64_t nwarps = nthreads >> 5;
   const uint64_t keep = policy_evict_last();
   const uint64_t epol = policy_by(a.elem_policy);
-  if (G >= 4 && a.sweep && a.n >= 2 && total >= a.N && a.edge_counts == nullptr) {
+  // (not at hop 0: the seeds' table tags are written by this kernel's own prologue, so they are
+  // not final until the kernel ends; from hop 1 on, F_h's tags were finalised by the last scan)
+  if (G >= 4 && h >= 1 && a.sweep && a.n >= 2 && total >= a.N && a.edge_counts == nullptr) {
     sample_sweep<(G >= 4 ? G : 4)>(a, S, warp_id, nwarps, keep, epol);
     hop_shared_flush(a, S);
     return;

@@ -138,3 +138,61 @@ def test_knapsack_fill_parity(trial):
     o = oracle.sample_gather(ip, R_idx, ft, seeds, fan, 17, cl_o, slot_o)
     assert np.array_equal(g["F"], o.F) and np.array_equal(g["counters"], o.counters)
     assert np.array_equal(g["X"], o.X)
+
+
+@pytest.mark.parametrize("trial", range(40))
+def test_random_group_configuration(trial):
+    """dci_sample_gather_many on random graphs / fan-outs (1..40: frontier-order and node-sweep
+    sampling, G < 4 and G >= 4 lane groups, the wide kernel above 32) / group sizes 1..16 /
+    budgets: every batch bit-exact against the oracle; groups issued twice on two streams."""
+    rng = np.random.default_rng(9000 + trial)
+    ip, ix = _graph(rng, ["rmat", "hub", "uniform"][trial % 3])
+    N, E = len(ip) - 1, len(ix)
+    D = int(rng.choice([1, 4, 13, 64, 100]))
+    ft = synth.features(N, D).numpy()
+    L = int(rng.integers(1, 4))
+    fan = tuple(int(x) for x in rng.integers(1, 41 if trial % 5 == 0 else 17, L))
+    B = int(rng.integers(1, min(N, 128) + 1))
+    ctx = dci.load_graph(ip, ix, ft)
+    el = synth.eligible_nodes(ip)
+    if len(el) == 0:
+        pytest.skip("graph without edges")
+    pre = rng.permutation(el)[: min(len(el), 2 * B)].astype(np.int32)
+    nv = torch.zeros(N, dtype=torch.int32, device=DEV)
+    ec = torch.zeros(max(E, 1), dtype=torch.int32, device=DEV)
+    dci.presample(ctx, torch.from_numpy(pre).to(DEV), B, fan, 3, nv, ec)
+    nv_o, ec_o = oracle.presample(ip, ix, pre, B, fan, 3)
+    C = int(rng.integers(0, 2 * synth.data_bytes(N, E, D) + 64)) + 1
+    r = int(rng.integers(0, 101))
+    c_adj, c_feat = oracle.allocate(C, ratio=(r, 100))
+    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    R, cl, _, _ = oracle.adj_fill(ip, ix, ec_o, c_adj)
+    slot_o, _ = oracle.feat_fill(nv_o, c_feat // (4 * ((D + 3) // 4 * 4)))
+    n = int(rng.integers(1, 17))
+    streams = [torch.cuda.Stream(device=DEV) for _ in range(2)]
+    wss = [[dci.workspace_create(ctx, B, fan) for _ in range(n)] for _ in range(2)]
+    seed = int(rng.integers(0, 1 << 62))
+    expect = []
+    keep = []
+    for k in range(4):  # groups 0..3 on alternating streams, workspaces reused
+        group = []
+        for _ in range(n):
+            b = int(rng.integers(0, B + 1))
+            group.append(rng.choice(N, size=min(b, N), replace=False).astype(np.int32))
+        outs = [dci.BatchOut(ctx, B, fan) for _ in range(n)]
+        sd = [torch.from_numpy(g).to(DEV) for g in group]
+        keep.append(sd)
+        dci.sample_gather_many(ctx, wss[k % 2], sd, fan, seed, outs, stream=streams[k % 2])
+        expect += list(zip(group, outs))
+    torch.cuda.synchronize()
+    for seeds, og in expect:
+        g = og.result()
+        o = oracle.sample_gather(ip, R, ft, seeds, fan, seed, cl, slot_o)
+        assert g["status"] == 0
+        assert np.array_equal(g["F"], o.F)
+        assert np.array_equal(g["sizes"], o.sizes)
+        for h in range(L):
+            assert np.array_equal(g["bptr"][h], o.bptr[h])
+            assert np.array_equal(g["bsrc"][h], o.bsrc[h])
+        assert np.array_equal(g["counters"], o.counters)
+        assert np.array_equal(g["X"], o.X)
