@@ -106,6 +106,7 @@ struct HopShared {
   unsigned long long seed[DCI_MAX_GROUP];
   const int32_t* Fin[DCI_MAX_GROUP];
   unsigned cnt[DCI_MAX_GROUP][2];     // adjacency hits / misses of this block, per batch
+  int all_ok;                         // no batch has a seed error (status set by hop 0)
 };
 
 __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S) {
@@ -129,6 +130,9 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
     S.pre[a.n] = acc;
     S.ppre[a.n] = pacc;
     S.tpre[a.n] = tacc;
+    int ok = 1;
+    for (int b = 0; b < a.n; ++b) ok &= __ldcg(&a.b[b].sc->status) == 0;
+    S.all_ok = ok;
   }
   if (threadIdx.x < 2 * DCI_MAX_GROUP) (&S.cnt[0][0])[threadIdx.x] = 0u;
   __syncthreads();
@@ -410,7 +414,9 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   const uint64_t epol = policy_by(a.elem_policy);
   // (not at hop 0: the seeds' table tags are written by this kernel's own prologue, so they are
   // not final until the kernel ends; from hop 1 on, F_h's tags were finalised by the last scan)
-  if (G >= 4 && h >= 1 && a.sweep && a.n >= 2 && total >= a.N && a.edge_counts == nullptr) {
+  // (and not when a batch has a seed error: a bad or repeated seed has no table slot of its own,
+  // so the sweep would leave its candidate slots unwritten; frontier order fills them)
+  if (G >= 4 && h >= 1 && S.all_ok && a.sweep && a.n >= 2 && total >= a.N && a.edge_counts == nullptr) {
     sample_sweep<(G >= 4 ? G : 4)>(a, S, warp_id, nwarps, keep, epol);
     hop_shared_flush(a, S);
     return;

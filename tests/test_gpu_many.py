@@ -225,3 +225,28 @@ def test_many_host_results_in_one_copy(filled, ldx_pad):
         _assert_batch_equal(og.result(), o, len(fan))
         assert np.array_equal(r["sizes"], o.sizes) and np.array_equal(r["counters"], o.counters)
         assert r["status"] == 0
+
+
+def test_sweep_group_with_seed_errors(dense):
+    """A node-sweep group in which one batch has a bad seed and another a repeated seed: those
+    batches report DCI_ESEED / DCI_EDUP, every other batch stays bit-exact, and the workspaces
+    are clean for the next group (the sweep is skipped when a batch has a seed error)."""
+    ip, R, ft, ctx, cl, slot, fan, B = dense
+    batches = synth.inference_batches(ip, B)
+    n = 6
+    group = [batches[i % len(batches)].copy() for i in range(n)]
+    group[1][3] = ctx.N + 7          # out of range
+    group[4][5] = group[4][2]        # repeated
+    wss = [dci.workspace_create(ctx, B, fan) for _ in range(n)]
+    outs = [dci.BatchOut(ctx, B, fan) for _ in range(n)]
+    dci.sample_gather_many(ctx, wss, [torch.from_numpy(g).to(DEV) for g in group], fan, synth.SAMPLE_SEED, outs)
+    res = [o.result() for o in outs]
+    assert res[1]["status"] == dci.ESEED and res[4]["status"] == dci.EDUP
+    for i in (0, 2, 3, 5):
+        o = oracle.sample_gather(ip, R, ft, group[i], fan, synth.SAMPLE_SEED, cl, slot)
+        _assert_batch_equal(res[i], o, len(fan))
+    good = [batches[(i + 7) % len(batches)] for i in range(n)]
+    dci.sample_gather_many(ctx, wss, [torch.from_numpy(g).to(DEV) for g in good], fan, synth.SAMPLE_SEED, outs)
+    for g_, og in zip(good, outs):
+        o = oracle.sample_gather(ip, R, ft, g_, fan, synth.SAMPLE_SEED, cl, slot)
+        _assert_batch_equal(og.result(), o, len(fan))
