@@ -636,12 +636,14 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
   if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
   for (int i = 0; i < 3; ++i)
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
-  if (w->gg_exec) cudaGraphExecDestroy(w->gg_exec);
+  for (auto& c : w->gg) {
+    if (c.exec) cudaGraphExecDestroy(c.exec);
+    free(c.sig);
+  }
   if (w->stage) cudaFree(w->stage);
   if (w->gseeds_host) cudaFreeHost(w->gseeds_host);
   if (w->gseeds_dev) cudaFree(w->gseeds_dev);
   if (w->gseeds_ev) cudaEventDestroy(w->gseeds_ev);
-  free(w->gg_sig);
   if (w->live_ws) --*w->live_ws;
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   delete w;
@@ -753,28 +755,35 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   };
   w0->in_group = 1;
   const bool use_graph = graph_mode();
+  // two cached group graphs per first workspace (least recently used replaced): a caller that
+  // alternates two group shapes (e.g. a full group and a shorter last one) never re-captures
+  dci_workspace::GroupGraph* gg = nullptr;
   if (use_graph) {
-    const bool need = !(w0->gg_exec && w0->gg_sig_len == sizeof(GroupSig) && w0->gg_sig &&
-                        !memcmp(w0->gg_sig, sig, sizeof(GroupSig)));
-    if (need) {
-      if (w0->gg_exec) cudaGraphExecDestroy(w0->gg_exec);
-      w0->gg_exec = nullptr;
+    for (auto& c : w0->gg)
+      if (c.exec && c.sig && c.sig_len == sizeof(GroupSig) && !memcmp(c.sig, sig, sizeof(GroupSig))) gg = &c;
+    if (!gg) {
+      gg = &w0->gg[0];
+      for (auto& c : w0->gg)
+        if (!c.exec || c.last_use < gg->last_use) gg = &c;
+      if (gg->exec) cudaGraphExecDestroy(gg->exec);
+      gg->exec = nullptr;
       const uint64_t launches0 = ctx->launches;
       DCI_CUDA(cudaStreamBeginCapture(w0->cap_stream, cudaStreamCaptureModeThreadLocal));
       enqueue(w0->cap_stream);
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamEndCapture(w0->cap_stream, &graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-      w0->gg_kernels = ctx->launches - launches0;
+      gg->kernels = ctx->launches - launches0;
       ctx->launches = launches0;
-      e = cudaGraphInstantiate(&w0->gg_exec, graph, 0);
+      e = cudaGraphInstantiate(&gg->exec, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-      if (!w0->gg_sig) w0->gg_sig = malloc(sizeof(GroupSig));
-      if (!w0->gg_sig) return fail(DCI_ENOMEM, "host allocation failed");
-      memcpy(w0->gg_sig, sig, sizeof(GroupSig));
-      w0->gg_sig_len = sizeof(GroupSig);
+      if (!gg->sig) gg->sig = malloc(sizeof(GroupSig));
+      if (!gg->sig) return fail(DCI_ENOMEM, "host allocation failed");
+      memcpy(gg->sig, sig, sizeof(GroupSig));
+      gg->sig_len = sizeof(GroupSig);
     }
+    gg->last_use = ++w0->gg_clock;
   }
   // phased schedule (default; DCI_PHASED=0 overlaps them): a group samples only after the previous
   // group's gather has finished, so gathers and sampling alternate and each has the GPU to itself.
@@ -784,8 +793,8 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   if (phased && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[0], s));
   if (use_graph) {
-    ctx->launches += w0->gg_kernels;
-    DCI_CUDA(cudaGraphLaunch(w0->gg_exec, s));
+    ctx->launches += gg->kernels;
+    DCI_CUDA(cudaGraphLaunch(gg->exec, s));
   } else {
     enqueue(s);
   }

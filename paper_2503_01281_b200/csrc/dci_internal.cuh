@@ -159,10 +159,15 @@ struct dci_workspace {
   int32_t profiling = 0;
   int32_t in_group = 0;  // the batch being enqueued belongs to a dci_sample_gather_many group
   // dci_sample_gather_many: the group's sampling graph, cached on the group's first workspace
-  cudaGraphExec_t gg_exec = nullptr;
-  void* gg_sig = nullptr;
-  size_t gg_sig_len = 0;
-  uint64_t gg_kernels = 0;
+  struct GroupGraph {
+    cudaGraphExec_t exec = nullptr;
+    void* sig = nullptr;
+    size_t sig_len = 0;
+    uint64_t kernels = 0;
+    uint64_t last_use = 0;
+  };
+  GroupGraph gg[2];
+  uint64_t gg_clock = 0;
   // dci_sample_gather_many_host: device block the group gather publishes all results into
   dci_batch_result* stage = nullptr;
   bool want_stage = false, staged = false;

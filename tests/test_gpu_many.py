@@ -250,3 +250,21 @@ def test_sweep_group_with_seed_errors(dense):
     for g_, og in zip(good, outs):
         o = oracle.sample_gather(ip, R, ft, g_, fan, synth.SAMPLE_SEED, cl, slot)
         _assert_batch_equal(og.result(), o, len(fan))
+
+
+def test_group_shapes_alternate(filled):
+    """A first workspace caches two group graphs: alternating group sizes (and a third shape that
+    evicts one) on the same workspaces keeps every batch exact."""
+    ip, R, ft, ctx, cl, slot, fan, B = filled
+    batches = synth.inference_batches(ip, B)
+    wss = [dci.workspace_create(ctx, B, fan) for _ in range(5)]
+    outs = [dci.BatchOut(ctx, B, fan) for _ in range(5)]
+    k = 0
+    for n in [5, 3, 5, 3, 2, 5, 2, 3]:
+        group = [batches[(k + j) % len(batches)] for j in range(n)]
+        k += n
+        dci.sample_gather_many(ctx, wss[:n], [torch.from_numpy(g).to(DEV) for g in group], fan, synth.SAMPLE_SEED,
+                               outs[:n])
+        for g_, og in zip(group, outs[:n]):
+            o = oracle.sample_gather(ip, R, ft, g_, fan, synth.SAMPLE_SEED, cl, slot)
+            _assert_batch_equal(og.result(), o, len(fan))
