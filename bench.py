@@ -565,6 +565,18 @@ def run_ours(args):
         tj = json.load(open(tfile)).get(f"{cfg.name}/group{G}")
         if tj:  # ncu dram bytes per launch of this kernel and configuration
             traffic = tj.get("dram_bytes_per_launch")
+    # the access pattern's own measured rate (tools/probe/hbm_gather_probe.cu): context for the
+    # copy-peak fraction, not a replacement for it
+    pattern = None
+    pfile = os.path.join(ROOT, "profiles", "hbm_pattern_peaks.json")
+    if os.path.exists(pfile) and not host_bound:
+        pj = json.load(open(pfile))
+        wpr = 1.0 / max(frac_read, 1e-9)  # rows written per row read
+        key = ("read1_write10_GBps" if wpr >= 7.5 else "read1_write5_GBps") if G and frac_read < 0.999 \
+            else "gather_random_read_seq_write_GBps"
+        if achieved_gbs:
+            pattern = {"name": key.replace("_GBps", ""), "peak": pj[key], "frac": achieved_gbs / pj[key],
+                       "writes_per_read": wpr, "source": "profiles/hbm_pattern_peaks.json"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps_eff,
         "warmup": args.warmup, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": "weak",
@@ -594,6 +606,7 @@ def run_ours(args):
                      "gather_busy_frac": tot[4] / ms_tot if ms_tot > 0 else None,
                      "aggregate_achieved": aggregate_gbs, "aggregate_frac": aggregate_gbs / bind_peak,
                      "alone": None if alone is None or host_bound else dict(alone, frac=alone["achieved"] / bind_peak),
+                     "pattern": pattern,
                      "note": "achieved = algorithmic bytes per gather launch / mean live launch time (CUDA events "
                              "on the launch stream); group gathers run one at a time on the gather stream. "
                              "aggregate_achieved = the same bytes / timed wall time; alone = the same launch "
