@@ -227,8 +227,9 @@ void launch_hop_epilogue(dci_ctx* ctx, dci_workspace* const* ws, const HopParams
 // must run launch_hop_epilogue on the sampling stream.
 bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_batch_out* out,
                          const HopParams& last, int32_t* node_visits, cudaStream_t s);
-// The TMA (bulk-copy) gather handles this output (default; env DCI_GATHER=ldg selects the
-// register-copy kernel).  It then runs serialised on the context's gather stream.
+// A single-batch call uses the TMA (bulk-copy) gather for this output (only with env
+// DCI_GATHER=tma; the default single-batch gather is the register-copy k_gather).  It then runs
+// serialised on the context's gather stream.
 bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out);
 // Multi-batch TMA gather (dci_sample_gather_many): every output takes bulk stores.
 bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t n);

@@ -1,4 +1,6 @@
-// S7 + S8 of the hot path, one kernel per batch:
+// S7 + S8 of the hot path.
+//
+// k_gather: one kernel per batch (dci_sample_gather, dci_presample):
 //  - relabel of the last hop's candidates into its block CSR (table tag -> local id)
 //  - feature-cache route inline through the remap table: slot = dir[F[i]].slot
 //  - feature gather: X[i] = fcache[slot] on a hit (HBM -> HBM) or feats[v] on a
@@ -7,6 +9,9 @@
 //  - presample: node_visits[v] += 1 (C7)
 //  - the last block to finish publishes sizes / counters / status and resets the
 //    workspace scalars for the next batch.
+//
+// k_gather_tma: one kernel per group of batches (dci_sample_gather_many): Blackwell bulk copies
+// through a shared-memory ring, in row mode or node-sweep mode (see the kernel's comments).
 #include <cuda_runtime.h>
 
 #include <algorithm>
