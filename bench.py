@@ -618,17 +618,23 @@ def run_ours(args):
                   "c_adj": c_adj, "c_feat": c_feat, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
                   "e2e_ms_per_step": ems / steps_eff, "host_enqueue_ms_per_step": host_s * 1e3 / steps_eff},
     }
-    def check_batches():
-        """Two full-size batches through the same call the timed region used (group or single)."""
-        bs = batches[:2]
-        os_ = [dci.BatchOut(ctx, B, fan) for _ in bs]
+    def check_batches(nchk=3):
+        """Full-size batches through the same call the timed region used: a whole group of `per`
+        batches (the same node-sweep sampling and gather paths), of which the first `nchk` are
+        checked against the oracle; or single calls."""
         if G >= 2:
-            dci.sample_gather_many(ctx, wss[0][:2], [torch.from_numpy(b).to(dev) for b in bs], fan, synth.SAMPLE_SEED,
-                                   os_)
+            bs = [batches[j % len(batches)] for j in range(per)]
+            os_ = [dci.BatchOut(ctx, B, fan) for _ in bs]
+            dci.sample_gather_many(ctx, wss[0], [torch.from_numpy(b).to(dev) for b in bs], fan, synth.SAMPLE_SEED, os_)
         else:
+            bs = batches[:nchk]
+            os_ = [dci.BatchOut(ctx, B, fan) for _ in bs]
             for b, o in zip(bs, os_):
                 dci.sample_gather(ctx, wss[0][0], torch.from_numpy(b).to(dev), fan, synth.SAMPLE_SEED, o)
-        return [(b, o.result()) for b, o in zip(bs, os_)]
+        torch.cuda.synchronize()
+        res = [(b, o.result()) for b, o in list(zip(bs, os_))[:nchk]]
+        del os_
+        return res
 
     if not args.profile_only and world == 1 and args.check_light:
         gpu_results = check_batches()
@@ -642,6 +648,9 @@ def run_ours(args):
         line["cpu_baseline"] = res
         if check:
             line["parity_check"] = check
+    if "parity_check" in line:
+        line["parity_check"]["call"] = (f"dci_sample_gather_many, one group of {per} (as timed), first "
+                                        f"{line['parity_check']['batches']} checked") if G >= 2 else "dci_sample_gather"
     print(json.dumps(line), flush=True)
     parallel.barrier(local)
 
