@@ -15,7 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run(args):
-    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--no-cpu-baseline", "--steps", "300", "--warmup", "10"] + args
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--no-cpu-baseline", "--no-check", "--steps", "300", "--warmup", "10",
+           "--repeats", "1"] + args
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=900)
     if r.returncode != 0:
         return {"error": r.stderr[-500:], "args": args}
