@@ -302,6 +302,23 @@ class BatchOut:
         return out
 
 
+def _device_i32(t, what, device=None):
+    """Arguments passed to the ABI as device int32 pointers must be contiguous int32 CUDA tensors
+    (the ABI sees only the pointer, so a wrong dtype or a strided view would be read as garbage)."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()):
+        raise TypeError(f"{what}: expected a contiguous int32 CUDA tensor, got "
+                        f"{getattr(t, 'dtype', type(t))} on {getattr(t, 'device', '?')}")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{what}: tensor on cuda:{t.device.index}, context on cuda:{device}")
+
+
+def _host_i32(t, what):
+    import torch
+    if not (isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()):
+        raise TypeError(f"{what}: expected a contiguous int32 CPU (pinned) tensor")
+
+
 def _record(tensor, stream):
     """The batch reads `tensor` asynchronously on `stream`: tell torch's caching allocator, so a
     tensor the caller drops is not handed to another allocation before the batch has run."""
@@ -314,6 +331,7 @@ def sample_gather(ctx: Context, ws: Workspace, seeds, fanouts, seed: int, out: B
     seeds: int32 CUDA tensor on ctx.device."""
     import torch
     fan = np.ascontiguousarray(fanouts, np.int32)
+    _device_i32(seeds, "seeds", ctx.device)
     st = torch.cuda.current_stream() if stream is None else stream
     _record(seeds, st)
     out.record_stream(st)
@@ -326,7 +344,10 @@ def sample_gather_many(ctx: Context, wss, seeds_list, fanouts, seed: int, outs, 
     concurrently and gathered by ONE TMA gather launch; asynchronous on `stream`."""
     import torch
     n = len(wss)
-    assert n == len(seeds_list) == len(outs)
+    if not n == len(seeds_list) == len(outs):
+        raise ValueError("wss, seeds_list and outs must have the same length")
+    for sd in seeds_list:
+        _device_i32(sd, "seeds", ctx.device)
     fan = np.ascontiguousarray(fanouts, np.int32)
     st = torch.cuda.current_stream() if stream is None else stream
     for sd in seeds_list:
@@ -368,6 +389,10 @@ def sample_gather_many_host(ctx: Context, wss, seeds_host_list, fanouts, seed: i
     status come back in ONE copy into results_host (see result_buffer / parse_results), valid
     after synchronising `stream`."""
     n = len(wss)
+    if not n == len(seeds_host_list) == len(outs):
+        raise ValueError("wss, seeds_host_list and outs must have the same length")
+    for sd in seeds_host_list:
+        _host_i32(sd, "seeds_host")
     fan = np.ascontiguousarray(fanouts, np.int32)
     if stream is not None:
         for o in outs:
@@ -388,6 +413,7 @@ def sample_gather_host(ctx: Context, ws: Workspace, seeds_host, fanouts, seed: i
     to host buffers (pinned torch tensors) on the same stream.  The host tensors must stay alive
     until the stream has been synchronised (the copies are asynchronous)."""
     import torch
+    _host_i32(seeds_host, "seeds_host")
     fan = np.ascontiguousarray(fanouts, np.int32)
     if stream is not None:
         out.record_stream(stream)
@@ -423,6 +449,10 @@ def mean_aggregate(ctx: Context, out: BatchOut, hop: int | None = None, H=None, 
 def presample(ctx: Context, seeds, batch: int, fanouts, seed: int, node_visits, edge_counts, stream=None):
     """dci_presample (S1): accumulates into node_visits int32[N] / edge_counts int32[E] (CUDA
     tensors); returns host uint64 arrays (t_sample_ns, t_feature_ns), one entry per batch."""
+    _device_i32(seeds, "seeds", ctx.device)
+    _device_i32(node_visits, "node_visits", ctx.device)
+    if ctx.E:
+        _device_i32(edge_counts, "edge_counts", ctx.device)
     fan = np.ascontiguousarray(fanouts, np.int32)
     n = int(seeds.numel())
     nb = (n + batch - 1) // batch

@@ -86,3 +86,25 @@ def test_product_package_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "dci_oracle" not in txt, fn
+
+
+def test_binding_rejects_wrong_seed_tensors():
+    """The ABI sees only pointers, so the binding checks dtype / device / layout first (no GPU
+    needed: the checks run before any library call)."""
+    import types
+
+    import pytest
+    import torch
+
+    import paper_2503_01281_b200 as dci
+    ctx = types.SimpleNamespace(device=0, handle=None, E=1)
+    with pytest.raises(TypeError):
+        dci.sample_gather(ctx, None, torch.zeros(4, dtype=torch.int64), (2,), 1, None)
+    with pytest.raises(TypeError):
+        dci.sample_gather(ctx, None, torch.zeros(4, dtype=torch.int32), (2,), 1, None)  # CPU, not CUDA
+    with pytest.raises(ValueError):
+        dci.sample_gather_many(ctx, [None, None], [torch.zeros(4, dtype=torch.int32)], (2,), 1, [None])
+    with pytest.raises(TypeError):
+        dci.sample_gather_many_host(ctx, [None], [torch.zeros(4, dtype=torch.int64)], (2,), 1, [None])
+    with pytest.raises(TypeError):
+        dci.presample(ctx, torch.zeros(4, dtype=torch.int32), 2, (2,), 1, None, None)
