@@ -319,6 +319,17 @@ def _host_i32(t, what):
         raise TypeError(f"{what}: expected a contiguous int32 CPU (pinned) tensor")
 
 
+def _counts_ok(ctx, node_visits, edge_counts):
+    """Presample histograms: device int32[N] and int32[E]."""
+    _device_i32(node_visits, "node_visits", ctx.device)
+    if node_visits.numel() < ctx.N:
+        raise ValueError("node_visits must hold N counts")
+    if ctx.E:
+        _device_i32(edge_counts, "edge_counts", ctx.device)
+        if edge_counts.numel() < ctx.E:
+            raise ValueError("edge_counts must hold E counts")
+
+
 def _record(tensor, stream):
     """The batch reads `tensor` asynchronously on `stream`: tell torch's caching allocator, so a
     tensor the caller drops is not handed to another allocation before the batch has run."""
@@ -481,6 +492,7 @@ def allocate(ctx: Context | None, C_bytes: int, t_sample=(), t_feature=(), ratio
 
 def fill(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat: int, stream=None):
     """dci_fill (S3 + S4)."""
+    _counts_ok(ctx, node_visits, edge_counts)
     _check(lib().dci_fill(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None, c_adj,
                           c_feat, _stream_ptr(stream)), "dci_fill")
 
@@ -489,6 +501,7 @@ def fill_partitioned(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat:
                      stream=None):
     """dci_fill_partitioned (NEXT F1): the feature cache spans `world` partitions (c_feat per
     partition); rank -1 = all partitions on this device (emulation)."""
+    _counts_ok(ctx, node_visits, edge_counts)
     _check(lib().dci_fill_partitioned(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None,
                                       c_adj, c_feat, world, rank, _stream_ptr(stream)), "dci_fill_partitioned")
 
@@ -496,6 +509,7 @@ def fill_partitioned(ctx: Context, node_visits, edge_counts, c_adj: int, c_feat:
 def fill_knapsack(ctx: Context, node_visits, edge_counts, C_bytes: int, cost_feat: float, cost_adj: float,
                   stream=None):
     """dci_fill_knapsack (NEXT F4): DUCATI-style unified-budget greedy fill (comparison)."""
+    _counts_ok(ctx, node_visits, edge_counts)
     _check(lib().dci_fill_knapsack(ctx.handle, node_visits.data_ptr(), _t_ptr(edge_counts) if ctx.E else None,
                                    C_bytes, float(cost_feat), float(cost_adj), _stream_ptr(stream)),
            "dci_fill_knapsack")
