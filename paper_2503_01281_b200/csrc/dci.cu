@@ -640,6 +640,10 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     if (c.exec) cudaGraphExecDestroy(c.exec);
     free(c.sig);
   }
+  if (w->ghdr_ring) cudaFreeHost(w->ghdr_ring);
+  if (w->ghdr_dev) cudaFree(w->ghdr_dev);
+  for (auto& ev : w->ghdr_ev)
+    if (ev) cudaEventDestroy(ev);
   if (w->stage) cudaFree(w->stage);
   if (w->gseeds_host) cudaFreeHost(w->gseeds_host);
   if (w->gseeds_dev) cudaFree(w->gseeds_dev);
@@ -692,9 +696,36 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     tr = &w0->trec[w0->trec_cur];
     tr->nb = n;
   }
-  for (int i = 0; i < n; ++i) {
-    dci_status st = stage_header(ctx, ws[i], seeds[i], B[i], seed, s);
-    if (st != DCI_OK) return st;
+  const bool use_graph = graph_mode();
+  if (!use_graph) {
+    for (int i = 0; i < n; ++i) {
+      dci_status st = stage_header(ctx, ws[i], seeds[i], B[i], seed, s);
+      if (st != DCI_OK) return st;
+    }
+  } else {
+    // all n headers in ONE copy (pinned ring slot -> the first workspace's staging block); the
+    // group's graph scatters them into the workspaces' scalars as its first node
+    if (!w0->ghdr_ring) {
+      DCI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w0->ghdr_ring),
+                             sizeof(BatchHeader) * DCI_MAX_GROUP * dci_workspace::kGroupHdrRing, cudaHostAllocDefault));
+      DCI_CUDA(cudaMalloc(&w0->ghdr_dev, sizeof(BatchHeader) * DCI_MAX_GROUP));
+      for (auto& ev : w0->ghdr_ev) DCI_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    const int slot = (int)(w0->gcalls++ % dci_workspace::kGroupHdrRing);
+    DCI_CUDA(cudaEventSynchronize(w0->ghdr_ev[slot]));  // the copy that last used this slot is done
+    BatchHeader* hh = w0->ghdr_ring + (size_t)slot * DCI_MAX_GROUP;
+    for (int i = 0; i < n; ++i) {
+      if (++ws[i]->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
+        DCI_CUDA(cudaMemsetAsync(ws[i]->pos_of, 0, sizeof(unsigned long long) * ctx->N, s));
+        ws[i]->epoch = 1;
+      }
+      hh[i].seeds = seeds[i];
+      hh[i].seed = seed;
+      hh[i].B = B[i];
+      hh[i].epoch = ws[i]->epoch;
+    }
+    DCI_CUDA(cudaMemcpyAsync(w0->ghdr_dev, hh, sizeof(BatchHeader) * n, cudaMemcpyHostToDevice, s));
+    DCI_CUDA(cudaEventRecord(w0->ghdr_ev[slot], s));
   }
   // ---- the group's sampling: every hop of all n batches is ONE launch (hop, scan), captured as
   // a CUDA graph on the first workspace, re-captured when the group (workspaces, outputs,
@@ -754,7 +785,6 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     launch_hop_epilogue(ctx, ws, p, n, es);
   };
   w0->in_group = 1;
-  const bool use_graph = graph_mode();
   // two cached group graphs per first workspace (least recently used replaced): a caller that
   // alternates two group shapes (e.g. a full group and a shorter last one) never re-captures
   dci_workspace::GroupGraph* gg = nullptr;
@@ -769,6 +799,7 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
       gg->exec = nullptr;
       const uint64_t launches0 = ctx->launches;
       DCI_CUDA(cudaStreamBeginCapture(w0->cap_stream, cudaStreamCaptureModeThreadLocal));
+      launch_scatter_headers(ctx, ws, w0->ghdr_dev, n, w0->cap_stream);
       enqueue(w0->cap_stream);
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamEndCapture(w0->cap_stream, &graph);

@@ -168,6 +168,12 @@ struct dci_workspace {
   };
   GroupGraph gg[2];
   uint64_t gg_clock = 0;
+  // the group's headers: a pinned ring of host blocks -> one copy into ghdr_dev per call
+  static constexpr int kGroupHdrRing = 8;
+  dci::BatchHeader* ghdr_ring = nullptr;  // pinned [kGroupHdrRing][DCI_MAX_GROUP]
+  cudaEvent_t ghdr_ev[kGroupHdrRing] = {nullptr};
+  dci::BatchHeader* ghdr_dev = nullptr;   // [DCI_MAX_GROUP]
+  uint64_t gcalls = 0;
   // dci_sample_gather_many_host: device block the group gather publishes all results into
   dci_batch_result* stage = nullptr;
   bool want_stage = false, staged = false;
@@ -221,6 +227,9 @@ struct HopParams {
 // per kernel; a single call is n = 1.
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
+// A group's headers: src = device staging block of n headers -> ws[i]->scal->hdr.
+void launch_scatter_headers(dci_ctx* ctx, dci_workspace* const* ws, const BatchHeader* src, int32_t n,
+                            cudaStream_t s);
 // Relabel of the last hop (p[i].hop = L, prev_* = hop L-1) when the gather does not fuse it.
 void launch_hop_epilogue(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
 // Returns true when the kernel also relabelled the last hop; false (TMA gather) when the caller

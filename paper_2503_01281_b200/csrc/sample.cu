@@ -598,6 +598,19 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
   hop_shared_flush(a, S);
 }
 
+// k_scatter_headers: a group's per-batch headers (seeds pointer, B, seed, epoch) arrive in ONE
+// host->device copy into a staging block; this first node of the group's graph puts each into
+// its workspace's scalars, where every kernel of the batch reads it.
+struct HeaderScatter {
+  const BatchHeader* src;
+  BatchScalars* dst[DCI_MAX_GROUP];
+  int32_t n;
+};
+
+__global__ void k_scatter_headers(const __grid_constant__ HeaderScatter a) {
+  if ((int)threadIdx.x < a.n) a.dst[threadIdx.x]->hdr = a.src[threadIdx.x];
+}
+
 // k_hop_epilogue: the hop_prologue of a virtual hop L, i.e. the relabel of the last hop into its
 // block CSR and the clear of its scan state (launched after the last scan; the gather of a
 // group / TMA gather does not fuse it).
@@ -890,6 +903,17 @@ void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p,
   int64_t grid = persistent_grid(ctx, k_scan_hop, kScanTile, 8);
   if (tiles < grid) grid = tiles > 0 ? tiles : 1;
   k_scan_hop<<<(unsigned)grid, kScanTile, 0, s>>>(a);
+  ++ctx->launches;
+}
+
+void launch_scatter_headers(dci_ctx* ctx, dci_workspace* const* ws, const BatchHeader* src, int32_t n,
+                            cudaStream_t s) {
+  HeaderScatter a;
+  memset(&a, 0, sizeof(a));
+  a.src = src;
+  a.n = n;
+  for (int i = 0; i < n; ++i) a.dst[i] = ws[i]->scal;
+  k_scatter_headers<<<1, 32, 0, s>>>(a);
   ++ctx->launches;
 }
 
