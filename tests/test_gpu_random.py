@@ -138,6 +138,16 @@ def test_knapsack_fill_parity(trial):
     o = oracle.sample_gather(ip, R_idx, ft, seeds, fan, 17, cl_o, slot_o)
     assert np.array_equal(g["F"], o.F) and np.array_equal(g["counters"], o.counters)
     assert np.array_equal(g["X"], o.X)
+    # the same caches through a group call
+    grp = [rng.choice(N, size=min(B, N), replace=False).astype(np.int32) for _ in range(4)]
+    wss = [dci.workspace_create(ctx, B, fan) for _ in grp]
+    outs = [dci.BatchOut(ctx, B, fan) for _ in grp]
+    dci.sample_gather_many(ctx, wss, [torch.from_numpy(x).to(DEV) for x in grp], fan, 17, outs)
+    for x, og in zip(grp, outs):
+        g = og.result()
+        o = oracle.sample_gather(ip, R_idx, ft, x, fan, 17, cl_o, slot_o)
+        assert np.array_equal(g["F"], o.F) and np.array_equal(g["counters"], o.counters)
+        assert np.array_equal(g["X"], o.X)
 
 
 @pytest.mark.parametrize("trial", range(40))
