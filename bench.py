@@ -388,9 +388,12 @@ def run_ours(args):
         return [per] * (k // per) + ([k % per] if k % per else [])
 
     sizes = call_sizes(args.steps)
-    wsizes = call_sizes(args.warmup)
-    if G and args.steps % per:  # warm the short shape on every stream slot too
-        wsizes += [args.steps % per] * nws
+    if G:
+        # warm-up: at least W batches, in full groups on every stream slot, then the short last
+        # shape (if any) on every slot, so both cached group graphs of each slot are the timed ones
+        wsizes = [per] * max(-(-args.warmup // per), nws) + ([args.steps % per] * nws if args.steps % per else [])
+    else:
+        wsizes = call_sizes(args.warmup)
     n_calls = len(sizes)
     n_warm = len(wsizes)
     steps_eff = args.steps
