@@ -589,7 +589,7 @@ def run_ours(args):
                    "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
                                                     if args.partitioned and world > 1 else "replicated caches") + ")",
-                   "inflight": nws, "group": G, "ldx": outs[0][0].ldx,
+                   "inflight": nws, "group": G, "ldx": outs[0][0].ldx, "warmup_batches_run": int(sum(wsizes)),
                    "l2": "inputs larger than L2 (feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
                          % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
                             avg_fl * D * 4 / 1e6)},
