@@ -112,10 +112,12 @@ dci_status dci_output_bounds(const dci_ctx* ctx, int32_t B, const int32_t* fanou
  * Workspace: per-stream scratch for one in-flight batch (epoch-tagged node->position table
  * of N uint64, candidate / count arrays, scan tile state, batch scalars, stage events).
  * Sized for batches of up to max_batch seeds with fan-outs up to max_fanouts[.] (L hops).
- * Use one workspace per concurrently in-flight batch, and issue a workspace's batches in order
- * on one stream (its scratch is reused by the next batch).  The number of live workspaces also
- * tells the library how many batches are in flight: the gather kernel takes 4 blocks per SM
- * with one, 2 with two or three, 1 with four or more (override: env DCI_GATHER_BPS).
+ * Use one workspace per concurrently in-flight batch (a dci_sample_gather_many group uses one
+ * per batch of the group), and issue a workspace's batches in order on one stream (its scratch
+ * is reused by the next batch).  The number of live workspaces also tells the library how many
+ * single-batch calls are in flight: their register-copy gather takes 4 blocks per SM with one
+ * live workspace, 2 with two or three, 1 with four or more (override: env DCI_GATHER_BPS).
+ * Memory: 8 N bytes of position table + candidate arrays of max |F_h| * f_h int32 (x2) + small.
  * ------------------------------------------------------------------------------------ */
 dci_status dci_workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_t* max_fanouts, int32_t L,
                                 dci_workspace** out);
