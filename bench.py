@@ -46,7 +46,7 @@ def parse():
                          "groups, or 6 single batches")
     ap.add_argument("--group", type=int, default=None,
                     help="batches per dci_sample_gather_many call (one TMA gather launch per group); 0 = one "
-                         "dci_sample_gather per batch.  Default (measured, DESIGN.md §9): 16 on HBM-resident data "
+                         "dci_sample_gather per batch.  Default (measured, DESIGN.md §9): 20 on HBM-resident data "
                          "(M1, M2), 8 on papers100M-shaped (M4, M4s), 0 on products-shaped (M3, M5)")
     ap.add_argument("--ldx", default="pitch", choices=["pitch", "line"],
                     help="X row stride: the 16-byte feature pitch, or rounded up to whole 128-byte lines")
@@ -369,9 +369,9 @@ def run_ours(args):
     batches = parallel.shard(synth.inference_batches(ip, B), rank, world)
     batches = [b for b in batches if len(b) == B] or batches
     seeds_dev = [torch.from_numpy(b).to(dev) for b in batches]
-    # measured defaults: groups of 16 on HBM-resident data (node sweeps), groups of 8
+    # measured defaults: groups of 20 on HBM-resident data (node sweeps), groups of 8
     # on papers100M-shaped host-resident data, one batch per call on products-shaped (400 B rows)
-    default_group = {"M1": 16, "M2": 16, "M4": 8, "M4s": 8}.get(cfg.name.split("-")[0], 0)
+    default_group = {"M1": 20, "M2": 20, "M4": 8, "M4s": 8}.get(cfg.name.split("-")[0], 0)
     G = max(0, args.group) if args.group is not None else default_group
     nws = max(1, args.inflight) if args.inflight is not None else (2 if G else 6)
     per = max(1, G)  # batches per call

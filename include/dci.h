@@ -29,7 +29,7 @@ extern "C" {
 
 #define DCI_VERSION 100          /* 1.0.0 */
 #define DCI_MAX_LAYERS 8         /* L <= 8 hops */
-#define DCI_MAX_GROUP 16          /* batches per dci_sample_gather_many call */
+#define DCI_MAX_GROUP 32          /* batches per dci_sample_gather_many call */
 #define DCI_MAX_FANOUT 1024      /* per-hop fan-out 1..1024 (<= 32: registers, else shared memory) */
 
 typedef enum dci_status {
@@ -145,7 +145,7 @@ dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* see
  * (one hop / scan launch per hop for the whole group, captured once as a CUDA graph on ws[0]);
  * then ONE feature-gather launch (Blackwell bulk copies, cp.async.bulk, through a shared-memory
  * ring) moves the rows of every batch on the context's gather stream, so group gathers run one at
- * a time while the next group samples.  When 2..16 batches together hold at least N rows, the
+ * a time while the next group samples.  When 2..32 batches together hold at least N rows, the
  * gather sweeps node ids and reads each feature row ONCE for all batches holding it (P:170's
  * hit/miss sources unchanged).  Results are identical to n dci_sample_gather calls (O-6, O-7;
  * the draws do not depend on the batch, C4).  Asynchronous on `stream`: work enqueued on `stream`

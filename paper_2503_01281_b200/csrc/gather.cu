@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 // the latency-bound sampling kernels of other batches.
 // ------------------------------------------------------------------------------------
 constexpr int kTmaMaxSlots = 16;
-constexpr int kTmaMaxWarps = 16;
+constexpr int kTmaMaxWarps = 8;
 constexpr int kTmaMaxBatches = DCI_MAX_GROUP;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -308,7 +308,7 @@ struct TmaBatches {
 // to every batch that holds it (one bulk store per (batch, row)).  Reads drop from sum_b |F_L(b)|
 // rows to |union_b F_L(b)| rows and are in ascending cache-slot order; X is bit-identical.
 // ------------------------------------------------------------------------------------
-constexpr int kSweepMax = 16;  // batches per sweep launch (masks are 16-bit)
+constexpr int kSweepMax = 32;  // batches per sweep launch (32-bit presence masks)
 
 template <int SMAX>
 
@@ -477,8 +477,10 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
     int* meta = reinterpret_cast<int*>(s_ring + t.meta_off) + wib * K * t.Rs * (1 + kSweepMax);
     if (nb <= 8)
       gather_sweep<8>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
-    else
+    else if (nb <= 16)
       gather_sweep<16>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
+    else
+      gather_sweep<32>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
   } else {
   // balanced contiguous row ranges per warp over the concatenated batches
   const int64_t lo = ntot * gw / nw, hi = ntot * (gw + 1) / nw;

@@ -278,11 +278,10 @@ __device__ __forceinline__ int32_t select_rank(int gl, int lane, unsigned gmask,
 // array are exactly those of the frontier-order loop, so the scan that follows sees the same
 // state.  Cuts the hop's random element reads from sum_b |F_h(b)| * f to |union| * f.
 // ------------------------------------------------------------------------------------
-constexpr int kSweepChunks = DCI_MAX_GROUP / 4;  // batches per probing lane (G >= 4)
-
 template <int G>
 __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, int64_t warp_id, int64_t nwarps,
                                              uint64_t keep, uint64_t epol) {
+  constexpr int CH = DCI_MAX_GROUP / G;  // batches probed per lane (G >= 4)
   const int h = a.hop, f = a.f, n = a.n;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
@@ -297,7 +296,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
     x0 = make_int4(0, 0, 0, 0);
     x1 = make_int4(0, 0, 0, 0);
 #pragma unroll
-    for (int c = 0; c < kSweepChunks; ++c) {
+    for (int c = 0; c < CH; ++c) {
       const int bb = c * G + gl;
       t[c] = (vv < a.N && bb < n) ? __ldcg(a.b[bb].pos_of + vv) : 0ull;
     }
@@ -307,7 +306,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       x1 = ld_keep_v4(ep + 1, keep);
     }
   };
-  unsigned long long tc[kSweepChunks], tn[kSweepChunks];
+  unsigned long long tc[CH], tn[CH];
   int4 e0, e1, e0n, e1n;
   probe(warp_id * GPW, tc, e0, e1);
   for (int64_t vbase = warp_id * GPW; vbase < a.N; vbase += vstride) {
@@ -318,9 +317,9 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
     // which batches hold v in F_h, and where: lane gl probed batches gl, gl + G, ... (G >= 4, so
     // at most 4 per lane) and keeps the local ids for the write loop below
     unsigned pm = 0;
-    uint32_t dd[kSweepChunks];
+    uint32_t dd[CH];
 #pragma unroll
-    for (int c = 0; c < kSweepChunks; ++c) {
+    for (int c = 0; c < CH; ++c) {
       const int bb = c * G + gl;
       bool pres = false;
       dd[c] = 0xFFFFFFFFu - (uint32_t)tc[c];
@@ -351,7 +350,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
     }
     // write the sample into every batch holding v (local id shuffled from the probing lane)
 #pragma unroll
-    for (int c = 0; c < kSweepChunks; ++c) {
+    for (int c = 0; c < CH; ++c) {
       if (c * G >= n) break;
       for (int r = 0; r < G && c * G + r < n; ++r) {
         const int bb = c * G + r;
@@ -369,7 +368,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       }
     }
 #pragma unroll
-    for (int c = 0; c < kSweepChunks; ++c) tc[c] = tn[c];
+    for (int c = 0; c < CH; ++c) tc[c] = tn[c];
     e0 = e0n;
     e1 = e1n;
   }

@@ -178,7 +178,7 @@ def test_random_group_configuration(trial):
     dci.fill(ctx, nv, ec, c_adj, c_feat)
     R, cl, _, _ = oracle.adj_fill(ip, ix, ec_o, c_adj)
     slot_o, _ = oracle.feat_fill(nv_o, c_feat // (4 * ((D + 3) // 4 * 4)))
-    n = int(rng.integers(1, 17))
+    n = int(rng.integers(1, 33))
     streams = [torch.cuda.Stream(device=DEV) for _ in range(2)]
     wss = [[dci.workspace_create(ctx, B, fan) for _ in range(n)] for _ in range(2)]
     seed = int(rng.integers(0, 1 << 62))

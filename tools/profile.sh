@@ -3,7 +3,7 @@
 # Only kernels inside bench.py's NVTX range "timed" are profiled.
 tag=${1:-run}; shift
 out=gpurun_out/prof_$tag; mkdir -p $out
-args="--profile-only --steps 32 --warmup 16 --repeats 1 --no-cpu-baseline $@"
+args="--profile-only --steps 40 --warmup 20 --repeats 1 --no-cpu-baseline $@"
 nv="--nvtx --nvtx-include timed/"
 ncu $nv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $out/launches.csv python bench.py $args > $out/launches.stdout 2>&1
