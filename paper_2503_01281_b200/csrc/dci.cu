@@ -705,11 +705,22 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   } else {
     // all n headers in ONE copy (pinned ring slot -> the first workspace's staging block); the
     // group's graph scatters them into the workspaces' scalars as its first node
-    if (!w0->ghdr_ring) {
-      DCI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w0->ghdr_ring),
-                             sizeof(BatchHeader) * DCI_MAX_GROUP * dci_workspace::kGroupHdrRing, cudaHostAllocDefault));
-      DCI_CUDA(cudaMalloc(&w0->ghdr_dev, sizeof(BatchHeader) * DCI_MAX_GROUP));
-      for (auto& ev : w0->ghdr_ev) DCI_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (!w0->ghdr_ring) {  // first group on this workspace: all three resources or none
+      BatchHeader* ring = nullptr;
+      BatchHeader* dev = nullptr;
+      cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&ring),
+                                    sizeof(BatchHeader) * DCI_MAX_GROUP * dci_workspace::kGroupHdrRing,
+                                    cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaMalloc(&dev, sizeof(BatchHeader) * DCI_MAX_GROUP);
+      for (auto& ev : w0->ghdr_ev)
+        if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) {
+        if (ring) cudaFreeHost(ring);
+        if (dev) cudaFree(dev);
+        return cuda_fail(e, "group header staging");
+      }
+      w0->ghdr_dev = dev;
+      w0->ghdr_ring = ring;
     }
     const int slot = (int)(w0->gcalls++ % dci_workspace::kGroupHdrRing);
     DCI_CUDA(cudaEventSynchronize(w0->ghdr_ev[slot]));  // the copy that last used this slot is done
