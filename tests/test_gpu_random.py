@@ -153,7 +153,7 @@ def test_knapsack_fill_parity(trial):
 @pytest.mark.parametrize("trial", range(40))
 def test_random_group_configuration(trial):
     """dci_sample_gather_many on random graphs / fan-outs (1..40: frontier-order and node-sweep
-    sampling, G < 4 and G >= 4 lane groups, the wide kernel above 32) / group sizes 1..16 /
+    sampling, G < 4 and G >= 4 lane groups, the wide kernel above 32) / group sizes 1..32 /
     budgets: every batch bit-exact against the oracle; groups issued twice on two streams."""
     rng = np.random.default_rng(9000 + trial)
     ip, ix = _graph(rng, ["rmat", "hub", "uniform"][trial % 3])
