@@ -765,7 +765,10 @@ static void tma_launch(dci_ctx* ctx, const TmaBatches& tb, const dci_batch_out* 
     smem_set = smem;
   }
   static const int bps = std::max(1, std::min(4, env_int("DCI_TMA_BPS", 1)));
-  k_gather_tma<<<ctx->num_sms * bps, 32 * warps, smem, s>>>(tb, t);
+  // DCI_TMA_SMS: SMs the gather grid covers (default all; a measurement knob)
+  static const int sms = env_int("DCI_TMA_SMS", 0);
+  const int nsm = (sms > 0 && sms < ctx->num_sms) ? sms : ctx->num_sms;
+  k_gather_tma<<<nsm * bps, 32 * warps, smem, s>>>(tb, t);
   ++ctx->launches;
 }
 
