@@ -1,0 +1,66 @@
+"""bench.py's JSON line (the measurement contract) on small runs: the required keys,
+their types and the relations between them (value = seeds / time, frac = achieved / peak, a
+bit-exact parity spot check), for the single-call and the group path and the reference arm."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = pytest.mark.gpu
+
+
+def run_bench(*args, timeout=900):
+    r = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, capture_output=True, text=True,
+                       timeout=timeout)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def check_common(d, steps, warmup):
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e"):
+        assert k in d, k
+    assert d["steps"] == steps and d["warmup"] == warmup and d["n_gpus"] == 1
+    assert d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert d["value"] > 0 and d["ms_per_step"] > 0
+    assert "workload" in d["config"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] >= 0 and e["d2h_bytes_per_step"] >= 0
+
+
+@pytest.mark.parametrize("group", [0, 4])
+def test_bench_line_m1(group):
+    steps, warmup = 24, 4
+    d = run_bench("--config", "M1", "--steps", str(steps), "--warmup", str(warmup), "--repeats", "2",
+                  "--group", str(group), "--cpu-seconds", "2")
+    check_common(d, steps, warmup)
+    assert d["gpu_launches"] > 0
+    assert d["config"]["group"] == group
+    # value = seeds of the K timed steps / the median timed region
+    B = d["config"]["global_batch"]
+    assert d["value"] == pytest.approx(B / (d["ms_per_step"] / 1e3), rel=1e-6)
+    assert len(d["repeats"]["values"]) == 2 and len(d["e2e"]["repeats"]) == 2
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "host-link") and r["unit"] == "GB/s"
+    if r["frac"] is not None:
+        assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-9)
+    c = d["clocks"]
+    assert c["sm_mhz"] > 0 and isinstance(c["reasons"], list)
+    assert d["parity_check"]["bit_exact"] is True
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["cores"] >= 1 and cb["unit"] == d["unit"]
+
+
+def test_bench_reference_arm_m1():
+    d = run_bench("--impl", "reference", "--config", "M1", "--steps", "3", "--warmup", "3")
+    check_common(d, 3, 3)
+    assert d["impl"] == "reference"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["value"] == d["value"]
