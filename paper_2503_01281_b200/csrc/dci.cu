@@ -638,6 +638,7 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     if (w->graph_exec[i]) cudaGraphExecDestroy(w->graph_exec[i]);
   for (auto& c : w->gg) {
     if (c.exec) cudaGraphExecDestroy(c.exec);
+    if (c.exec2) cudaGraphExecDestroy(c.exec2);
     free(c.sig);
   }
   if (w->ghdr_ring) cudaFreeHost(w->ghdr_ring);
@@ -762,9 +763,10 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   }
   sig->acache = ctx->d_acache;
   sig->uidx = ctx->u_idx_cur;
-  auto enqueue = [&](cudaStream_t es) {
+  // hops [h0, h1) of the group (the parameters of every hop are built, so a range can start late)
+  auto enqueue = [&](cudaStream_t es, int h0, int h1) {
     HopParams p[DCI_MAX_GROUP], prev[DCI_MAX_GROUP];
-    for (int h = 0; h < L; ++h) {
+    for (int h = 0; h < h1; ++h) {
       for (int i = 0; i < n; ++i) {
         HopParams& q = p[i];
         q = HopParams{};
@@ -783,11 +785,16 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
         }
         q.bptr = outs[i].bptr[h];
       }
-      launch_sample_hop(ctx, ws, p, n, es);
-      launch_scan_hop(ctx, ws, p, n, es);
+      if (h >= h0) {
+        launch_sample_hop(ctx, ws, p, n, es);
+        launch_scan_hop(ctx, ws, p, n, es);
+      }
       for (int i = 0; i < n; ++i) prev[i] = p[i];
     }
   };
+  // split schedule: hops [0, hs) before the wait for the previous group's gather, [hs, L) after
+  const bool phased = group_phased();
+  const int hs = (phased && group_split() && L >= 2) ? L - 1 : 0;
   // the relabel of every batch's last hop: needed by the caller, not by the gather, so it runs
   // on `stream` while the gather runs on the gather stream
   auto enqueue_epilogue = [&](cudaStream_t es) {
@@ -807,19 +814,31 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
       for (auto& c : w0->gg)
         if (!c.exec || c.last_use < gg->last_use) gg = &c;
       if (gg->exec) cudaGraphExecDestroy(gg->exec);
-      gg->exec = nullptr;
-      const uint64_t launches0 = ctx->launches;
-      DCI_CUDA(cudaStreamBeginCapture(w0->cap_stream, cudaStreamCaptureModeThreadLocal));
-      launch_scatter_headers(ctx, ws, w0->ghdr_dev, n, w0->cap_stream);
-      enqueue(w0->cap_stream);
-      cudaGraph_t graph = nullptr;
-      cudaError_t e = cudaStreamEndCapture(w0->cap_stream, &graph);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-      gg->kernels = ctx->launches - launches0;
-      ctx->launches = launches0;
-      e = cudaGraphInstantiate(&gg->exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      if (gg->exec2) cudaGraphExecDestroy(gg->exec2);
+      gg->exec = gg->exec2 = nullptr;
+      free(gg->sig);  // the entry matches no group until both graphs are built
+      gg->sig = nullptr;
+      gg->sig_len = 0;
+      // part 1: the header scatter and hops [0, hs) (all hops when not split); part 2: [hs, L)
+      for (int part = 0; part < (hs > 0 ? 2 : 1); ++part) {
+        const uint64_t launches0 = ctx->launches;
+        DCI_CUDA(cudaStreamBeginCapture(w0->cap_stream, cudaStreamCaptureModeThreadLocal));
+        if (part == 0) {
+          launch_scatter_headers(ctx, ws, w0->ghdr_dev, n, w0->cap_stream);
+          enqueue(w0->cap_stream, 0, hs > 0 ? hs : L);
+        } else {
+          enqueue(w0->cap_stream, hs, L);
+        }
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(w0->cap_stream, &graph);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+        (part == 0 ? gg->kernels : gg->kernels2) = ctx->launches - launches0;
+        ctx->launches = launches0;
+        e = cudaGraphInstantiate(part == 0 ? &gg->exec : &gg->exec2, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      }
+      if (hs == 0) gg->kernels2 = 0;
       if (!gg->sig) gg->sig = malloc(sizeof(GroupSig));
       if (!gg->sig) return fail(DCI_ENOMEM, "host allocation failed");
       memcpy(gg->sig, sig, sizeof(GroupSig));
@@ -831,14 +850,23 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   // group's gather has finished, so gathers and sampling alternate and each has the GPU to itself.
   // Both are DRAM-bound, so overlapping them bought no throughput while it slowed
   // each gather launch by ~20 %.
-  const bool phased = group_phased();
-  if (phased && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
+  // (DCI_PHASED=2 splits it: the hops before the last overlap the previous gather)
+  if (hs == 0 && phased && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[0], s));
   if (use_graph) {
     ctx->launches += gg->kernels;
     DCI_CUDA(cudaGraphLaunch(gg->exec, s));
   } else {
-    enqueue(s);
+    enqueue(s, 0, hs > 0 ? hs : L);
+  }
+  if (hs > 0) {
+    if (ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
+    if (use_graph) {
+      ctx->launches += gg->kernels2;
+      DCI_CUDA(cudaGraphLaunch(gg->exec2, s));
+    } else {
+      enqueue(s, hs, L);
+    }
   }
   if (tr) {
     DCI_CUDA(cudaEventRecord(tr->e[1], s));

@@ -161,9 +161,10 @@ struct dci_workspace {
   // dci_sample_gather_many: the group's sampling graph, cached on the group's first workspace
   struct GroupGraph {
     cudaGraphExec_t exec = nullptr;
+    cudaGraphExec_t exec2 = nullptr;  // split schedule: the last hop (launched after the wait)
     void* sig = nullptr;
     size_t sig_len = 0;
-    uint64_t kernels = 0;
+    uint64_t kernels = 0, kernels2 = 0;
     uint64_t last_use = 0;
   };
   GroupGraph gg[2];
@@ -203,6 +204,7 @@ dci_status cuda_fail(cudaError_t e, const char* what);
 // dci_sample_gather_many schedule: sampling of a group waits for the previous group's gather
 // (default) or overlaps it (DCI_PHASED=0)
 bool group_phased();
+bool group_split();
 
 // ---- kernel launchers (sample.cu / gather.cu / fill.cu) ----
 struct HopParams {

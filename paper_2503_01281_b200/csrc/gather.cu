@@ -659,13 +659,17 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
-bool group_phased() {
+static int phased_mode() {
   static const int mode = [] {
     const char* e = getenv("DCI_PHASED");
-    return (e && e[0] == '0') ? 0 : 1;
+    return (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
   }();
-  return mode == 1;
+  return mode;
 }
+bool group_phased() { return phased_mode() != 0; }
+// DCI_PHASED=2: only the last hop waits for the previous group's gather; the earlier (light)
+// hops overlap it
+bool group_split() { return phased_mode() == 2; }
 
 bool gather_tma_mode() {
   static const int mode = [] {
