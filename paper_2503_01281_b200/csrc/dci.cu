@@ -461,7 +461,7 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
   // the context's gather stream (group gathers and serial gathers run one at a time on it);
   // created here so concurrent callers with distinct workspaces never race on it
   if (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->gather_ev, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->gather_ev, kCrossStreamEvent) != cudaSuccess)
     return bail(fail(DCI_ECUDA, "cudaStreamCreate(gather stream)"));
   memcpy(c->h_indptr, indptr, sizeof(int64_t) * (N + 1));
   cudaError_t e;
@@ -592,8 +592,8 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
   for (auto& r : w->trec)
     for (int i = 0; i < 4; ++i)
       if ((e = cudaEventCreate(&r.e[i])) != cudaSuccess) return bail(e, "event");
-  if ((e = cudaEventCreateWithFlags(&w->ev_mid, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
-  if ((e = cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_mid, kCrossStreamEvent)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_done, kCrossStreamEvent)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->gseeds_ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
                          cudaHostAllocPortable)) != cudaSuccess)
@@ -846,11 +846,11 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     }
     gg->last_use = ++w0->gg_clock;
   }
-  // phased schedule (default; DCI_PHASED=0 overlaps them): a group samples only after the previous
-  // group's gather has finished, so gathers and sampling alternate and each has the GPU to itself.
-  // Both are DRAM-bound, so overlapping them bought no throughput while it slowed
-  // each gather launch by ~20 %.
-  // (DCI_PHASED=2 splits it: the hops before the last overlap the previous gather)
+  // Schedule of consecutive groups (DCI_PHASED): by default a group's sampling overlaps the
+  // previous group's gather (+6 % seeds/s on M2 against alternating them, although each gather
+  // launch runs ~3 % slower beside the sampler, exp60).  DCI_PHASED=1: a group
+  // samples only after the previous group's gather has finished; DCI_PHASED=2: only its last hop
+  // waits for it.
   if (hs == 0 && phased && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[0], s));
   if (use_graph) {

@@ -203,6 +203,12 @@ dci_status cuda_fail(cudaError_t e, const char* what);
 
 // dci_sample_gather_many schedule: sampling of a group waits for the previous group's gather
 // (default) or overlaps it (DCI_PHASED=0)
+// Flags of the events that order work ACROSS streams (sampling -> gather -> caller, and the
+// phased schedule's gather -> next group).  Timing-enabled on purpose: measured on B200 (driver
+// 580), a stream waiting on a cudaEventDisableTiming event started its next work later, which cost
+// 3-5 % of throughput whenever sampling and gathers overlap (exp60).  Events only
+// waited on by the host keep cudaEventDisableTiming.
+constexpr unsigned kCrossStreamEvent = cudaEventDefault;
 bool group_phased();
 bool group_split();
 

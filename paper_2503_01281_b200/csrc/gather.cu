@@ -662,7 +662,7 @@ int env_int(const char* name, int dflt) {
 static int phased_mode() {
   static const int mode = [] {
     const char* e = getenv("DCI_PHASED");
-    return (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
+    return !e ? 0 : e[0] == '1' ? 1 : e[0] == '2' ? 2 : 0;  // default: overlapped (exp60)
   }();
   return mode;
 }

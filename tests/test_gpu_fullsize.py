@@ -149,13 +149,13 @@ def test_workspace_stats_and_graph_recapture():
 
 
 @pytest.mark.parametrize("env", [{"DCI_GATHER": "tma"}, {"DCI_SWEEP": "0"}, {"DCI_GATHER_SERIAL": "0"},
-                                 {"DCI_TMA_WARPS": "2", "DCI_TMA_CHUNK": "2048"}, {"DCI_PHASED": "0"},
+                                 {"DCI_TMA_WARPS": "2", "DCI_TMA_CHUNK": "2048"}, {"DCI_PHASED": "1"},
                                  {"DCI_SAMPLE_SWEEP": "0"}, {"DCI_PRECHECK": "1"}, {"DCI_SAMPLE_BPS": "1"},
                                  {"DCI_TMA_SMS": "37"}, {"DCI_PHASED": "2"}, {"DCI_PHASED": "2", "DCI_GRAPH": "0"}])
 def test_gather_variants_subprocess(env):
     """Process-wide switches (read once per process): the TMA gather for single-batch
-    calls, row mode for groups, group gathers on the caller's stream, a small TMA ring, overlapped
-    (not phased) groups, frontier-order sampling only, the tag pre-read before atomicMax, one
+    calls, row mode for groups, group gathers on the caller's stream, a small TMA ring, phased
+    (not overlapped) groups, frontier-order sampling only, the tag pre-read before atomicMax, one
     sampling block per SM, a gather grid on a quarter of the SMs, the split schedule (graphs and
     direct launches)."""
     r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=ROOT,
