@@ -151,7 +151,8 @@ dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* see
  * the draws do not depend on the batch, C4).  Asynchronous on `stream`: work enqueued on `stream`
  * before the call happens before the group, and work enqueued after it sees every output; issue
  * a workspace's groups in order on one stream, and a context's groups from one host thread (they
- * share its gather stream and the phased schedule's event).  If an output cannot take bulk stores (X NULL,
+ * share its gather stream and, under DCI_PHASED=1/2, the schedule's event).  If an output cannot
+ * take bulk stores (X NULL,
  * ldx % 4 != 0 or X not 16-byte aligned) the batches run one by one on `stream`.  Timing
  * (profiling on ws[0]): the group's sampling and its gather launch are each timed once and
  * booked on ws[0] (dci_workspace_stats).
