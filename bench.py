@@ -48,8 +48,10 @@ def parse():
                     help="batches per dci_sample_gather_many call (one TMA gather launch per group); 0 = one "
                          "dci_sample_gather per batch.  Default (measured, DESIGN.md §9): 20 on HBM-resident data "
                          "(M1, M2), 8 on papers100M-shaped (M4, M4s), 0 on products-shaped (M3, M5)")
-    ap.add_argument("--ldx", default="pitch", choices=["pitch", "line"],
-                    help="X row stride: the 16-byte feature pitch, or rounded up to whole 128-byte lines")
+    ap.add_argument("--ldx", default="auto", choices=["auto", "pitch", "line"],
+                    help="X row stride: the 16-byte feature pitch, or rounded up to whole 128-byte lines (the "
+                         "node-sweep gather then writes whole lines: random-row writes of partial lines run ~30 %% "
+                         "slower, tools/probe/scatter_probe.cu); auto = line when it adds <= 32 B per row")
     ap.add_argument("--repeats", type=int, default=5, help="timed regions of K steps (value = median)")
     ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
     ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
@@ -71,19 +73,29 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/check)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to test several ranks on one GPU)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank times K batches of its shard of the global list (task rule 5: the "
+                         "path shards into independent batches); strong: the K batches of one global list are "
+                         "split round-robin over the ranks")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 100 ms while the region runs."""
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while the region runs (every rank
+    samples its own GPU, addressed by UUID so CUDA_VISIBLE_DEVICES remapping cannot mislead it)."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
-        self.idx, self.rows, self.proc, self.th = gpu_index, [], None, None
+        self.idx, self.rows, self.proc, self.th = str(gpu_index), [], None, None
+        try:
+            import torch
+            self.idx = "GPU-" + str(torch.cuda.get_device_properties(gpu_index).uuid)
+        except Exception:
+            pass
 
     def start(self):
         try:
@@ -276,7 +288,7 @@ def run_reference(args):
     res, _ = oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, per_step * args.steps, threads)
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cfg.batch / res["value"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "global_batch": cfg.batch, "fanouts": list(cfg.fanouts),
                        "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget},
             "cpu_baseline": res, "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -291,7 +303,11 @@ def run_ours(args):
     from paper_2503_01281_b200 import parallel
 
     rank, world, local = parallel.init(args.backend)
+    if world != args.gpus:
+        print(f"[bench] note: {world} ranks launched with --gpus {args.gpus}; n_gpus reports the ranks",
+              file=sys.stderr)
     # one rank per GPU; (testing only) more ranks than GPUs share devices round-robin
+    shared_gpus = world > torch.cuda.device_count()
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -300,8 +316,7 @@ def run_ours(args):
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
 
     clk = ClockSampler(local)
-    if rank == 0:
-        clk.start()
+    clk.start()
     t0 = time.time()
     ip, ix, ft = make_inputs(cfg, dev)
     t_gen = time.time() - t0
@@ -315,20 +330,38 @@ def run_ours(args):
         ft = None  # the library holds its own pinned copy; free host RAM (papers100M-shaped: 57 GB)
 
     # ---- S1 presample (global list of 8 batches, sharded), C1 allreduce ----
-    t2 = time.time()
+    # (seed lists and the zeroed count arrays are harness work, outside the presample time)
     npre = args.presample_batches
     pre = synth.presample_seeds(ip, npre, B)
-    pre_batches = [pre[i * B:(i + 1) * B] for i in range(npre)]
+    pre_batches = [torch.from_numpy(pre[i * B:(i + 1) * B]).to(dev) for i in range(npre)]
     nv = torch.zeros(cfg.N, dtype=torch.int32, device=dev)
     ec = torch.zeros(cfg.E, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
     ts_all, tf_all = [], []
+    t2 = time.time()
     for pb in parallel.shard(pre_batches, rank, world):
-        ts, tf = dci.presample(ctx, torch.from_numpy(pb).to(dev), B, fan, synth.PRESAMPLE_SEED, nv, ec)
+        ts, tf = dci.presample(ctx, pb, B, fan, synth.PRESAMPLE_SEED, nv, ec)
         ts_all += ts.tolist()
         tf_all += tf.tolist()
-    S, F = parallel.allreduce_presample(nv, ec, ts_all, tf_all)
     torch.cuda.synchronize()
     t_pre = time.time() - t2
+    t2 = time.time()
+    S, F = parallel.allreduce_presample(nv, ec, ts_all, tf_all)
+    torch.cuda.synchronize()
+    t_allreduce = time.time() - t2
+
+    # ---- inference workspaces and outputs, created BEFORE the (auto) budget is cut (dci.h) ----
+    # measured defaults (DESIGN.md §9): groups of 20 on HBM-resident data (node sweeps), groups of 8
+    # on papers100M-shaped host-resident data, one batch per call on products-shaped (400 B rows)
+    default_group = {"M1": 20, "M2": 20, "M4": 8, "M4s": 8}.get(cfg.name.split("-")[0], 0)
+    G = max(0, args.group) if args.group is not None else default_group
+    nws = max(1, args.inflight) if args.inflight is not None else (2 if G else 6)
+    per = max(1, G)  # batches per call
+    wss = [[dci.workspace_create(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
+    ldx_line = -(-cfg.D // 32) * 32
+    line = args.ldx == "line" or (args.ldx == "auto" and 4 * (ldx_line - cfg.pitch_floats()) <= 32)
+    ldx = ldx_line if line else None
+    outs = [[dci.BatchOut(ctx, B, fan, ldx=ldx) for _ in range(per)] for _ in range(nws)]
 
     # ---- S2 allocate (Eq. 1) + S3/S4 fill ----
     t3 = time.time()
@@ -360,6 +393,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_fill = time.time() - t3
     info = dci.cache_info(ctx)
+    fill_ms = dci.fill_times(ctx)
     log(f"[bench] load {t_load:.2f}s presample {t_pre:.2f}s fill {t_fill:.2f}s  C_adj={c_adj} C_feat={c_feat} "
         f"adj_elems={info['adj_elems']}/{cfg.E} feat_rows={info['feat_rows']}/{cfg.N}")
     del nv, ec
@@ -369,15 +403,6 @@ def run_ours(args):
     batches = parallel.shard(synth.inference_batches(ip, B), rank, world)
     batches = [b for b in batches if len(b) == B] or batches
     seeds_dev = [torch.from_numpy(b).to(dev) for b in batches]
-    # measured defaults (DESIGN.md §9): groups of 20 on HBM-resident data (node sweeps), groups of 8
-    # on papers100M-shaped host-resident data, one batch per call on products-shaped (400 B rows)
-    default_group = {"M1": 20, "M2": 20, "M4": 8, "M4s": 8}.get(cfg.name.split("-")[0], 0)
-    G = max(0, args.group) if args.group is not None else default_group
-    nws = max(1, args.inflight) if args.inflight is not None else (2 if G else 6)
-    per = max(1, G)  # batches per call
-    wss = [[dci.workspace_create(ctx, B, fan) for _ in range(per)] for _ in range(nws)]
-    ldx = None if args.ldx == "pitch" else -(-cfg.D // 32) * 32
-    outs = [[dci.BatchOut(ctx, B, fan, ldx=ldx) for _ in range(per)] for _ in range(nws)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(nws)]
     for wl in wss:
         for w in wl:
@@ -387,7 +412,10 @@ def run_ours(args):
     def call_sizes(k):
         return [per] * (k // per) + ([k % per] if k % per else [])
 
-    sizes = call_sizes(args.steps)
+    # weak (default): every rank times K batches; strong: the K batches of one global list are
+    # split round-robin, rank g timing batches g, g+G, ... of it
+    k_local = args.steps if args.scaling == "weak" else len(range(rank, args.steps, world))
+    sizes = call_sizes(k_local)
     if G:
         # warm-up: at least W batches, in full groups on every stream slot, then the short last
         # shape (if any) on every slot, so both cached group graphs of each slot are the timed ones
@@ -534,9 +562,8 @@ def run_ours(args):
             alone = {"achieved": st0["gather_bytes"] / (st0["gather_ms"] / 1e3) / 1e9,
                      "avg_gather_ms": st0["gather_ms"] / max(1, st0["gather_launches"]),
                      "launches": st0["gather_launches"]}
-    clocks = clk.stop() if rank == 0 else None
-    if clocks is not None:
-        clocks["window"] = "sampled every 100 ms from input generation through the e2e region"
+    clocks = parallel.gather_clocks(clk.stop())
+    clocks["window"] = "sampled every 100 ms on every rank's GPU from input generation through the e2e region"
 
     e_value = seeds_all / (ems / 1e3)
 
@@ -566,7 +593,8 @@ def run_ours(args):
                  "feature_frac": host_b / (ms_tot / 1e3) / 1e9 / host_peak,
                  "adj_miss_Mreads_per_s": cn[1] / (ms_tot / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
                  "peak_kind": host_kind}
-    avg_fl = tot[2] / max(1, steps_eff * world * R)
+    steps_total = steps_eff * world if args.scaling == "weak" else steps_eff
+    avg_fl = tot[2] / max(1, steps_total * R)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "gather_traffic.json")
     if os.path.exists(tfile):
@@ -587,9 +615,10 @@ def run_ours(args):
                        "writes_per_read": wpr, "source": "profiles/hbm_pattern_peaks.json"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps_eff,
-        "warmup": args.warmup, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
-        "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B, "fanouts": list(fan),
+        "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B,
+                   "ranks_share_gpus": shared_gpus, "fanouts": list(fan),
                    "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
                    "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
@@ -623,7 +652,13 @@ def run_ours(args):
         "host_link": host_link,
         "clocks": clocks,
         "stats": {"avg_F_L": avg_fl, "F_L_per_seed": avg_fl / B, **hit_rates,
-                  "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre, "fill": t_fill},
+                  "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre,
+                                   "presample_device_s": (sum(ts_all) + sum(tf_all)) / 1e9,
+                                   "presample_batches": len(ts_all), "allreduce": t_allreduce,
+                                   "allocate_fill": t_fill, "fill_stages_ms": fill_ms,
+                                   "note": "presample = the dci_presample calls only (seed lists and count "
+                                           "arrays are made before); presample_device_s = sum of the "
+                                           "per-batch CUDA-event stage times it reports (Eq. 1 inputs)"},
                   "c_adj": c_adj, "c_feat": c_feat, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
                   "e2e_ms_per_step": ems / steps_eff, "host_enqueue_ms_per_step": host_s * 1e3 / steps_eff},
     }
@@ -664,8 +699,26 @@ def run_ours(args):
     parallel.barrier(local)
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without a torchrun environment: launch N ranks (one per GPU) through
+    torch.distributed.run on this node, so the driver's plain N-GPU invocation measures N GPUs.  Rank
+    0's JSON line reaches stdout; the exit code is the launcher's."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -208,8 +208,10 @@ dci_status dci_presample(dci_ctx* ctx, const int32_t* seeds, int64_t num_seeds, 
  *   C_adj = floor(C * S / (S + F)), C_feat = C - C_adj, S = sum t_sample_ns, F = sum
  *   t_feature_ns; S + F == 0 -> C_adj = floor(C / 2).
  *   ratio_den > 0: C_adj = floor(C * ratio_num / ratio_den) instead (sweeps, C20).
- *   C == 0 ("auto"): C = free device memory - the presample's peak per-batch
- *   workspace - 1 GiB reserve (C21), floored at 0.
+ *   C == 0 ("auto"): C = free device memory + memory the fill releases (current
+ *   caches, the presample workspace) - the fill's temporaries (<= 48 B/node + 24 B/element)
+ *   - 1 GiB reserve (C21), floored at 0.  Create the inference workspaces and outputs BEFORE
+ *   this call: they are then already excluded from the free memory the budget is cut from.
  * Postcondition: *c_adj + *c_feat == C.  Host-only.
  * ------------------------------------------------------------------------------------ */
 dci_status dci_allocate(dci_ctx* ctx, uint64_t C, const uint64_t* t_sample_ns, const uint64_t* t_feature_ns,
@@ -289,6 +291,17 @@ typedef struct dci_cache_info {
 } dci_cache_info;
 
 dci_status dci_cache_info_get(const dci_ctx* ctx, dci_cache_info* info);
+
+/* Stage times of the last fill, in ms (CUDA events on the fill stream; -1 = stage not timed):
+ * level 2 (per-node reorder, Alg. 1's element sort, incl. the reordered CSC back to the host),
+ * adjacency selection (level-1 weighted radix select + prefix scan), adjacency copy (prefixes
+ * into the cache), feature selection (top-k radix select + slot scan), feature copy (host rows
+ * into HBM), total.  The knapsack fill (F4) reports level 2 and the total only.  P:316-330 and
+ * P:371-376 make preprocessing time a headline; this splits it by step. */
+typedef struct dci_fill_times {
+  float level2_ms, adj_select_ms, adj_copy_ms, feat_select_ms, feat_copy_ms, total_ms;
+} dci_fill_times;
+dci_status dci_fill_times_get(const dci_ctx* ctx, dci_fill_times* out);
 dci_status dci_cache_state(dci_ctx* ctx, int32_t* cached_len, int64_t* cache_off, int32_t* slot_of,
                            int32_t* acache, float* fcache, int32_t* indices_cur);
 

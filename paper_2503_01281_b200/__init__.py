@@ -30,7 +30,7 @@ OK, EINVAL, ESTATE, ECUDA, ENOMEM, ESEED, EDUP, ECAP, ERANGE = range(9)
 EXPORTED = ["dci_load_graph", "dci_destroy", "dci_output_bounds", "dci_workspace_create", "dci_workspace_destroy",
             "dci_sample_gather", "dci_sample_gather_host", "dci_sample_gather_many", "dci_sample_gather_many_host",
             "dci_presample", "dci_allocate", "dci_fill",
-            "dci_cache_info_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
+            "dci_cache_info_get", "dci_fill_times_get", "dci_cache_state", "dci_workspace_set_profiling", "dci_workspace_stage_ms",
             "dci_workspace_stats", "dci_mean_aggregate", "dci_block_aggregate", "dci_fill_partitioned", "dci_fill_knapsack", "dci_feature_partition_handle",
             "dci_attach_feature_partitions", "dci_launch_count", "dci_last_error", "dci_version"]
 IPC_HANDLE_BYTES = 64
@@ -54,6 +54,11 @@ class dci_ws_stats(C.Structure):
                 ("counters", C.c_uint64 * 4), ("timed_batches", C.c_uint64), ("sample_ms", C.c_double),
                 ("gather_ms", C.c_double), ("gather_launches", C.c_uint64), ("rows_read", C.c_uint64),
                 ("gather_bytes", C.c_uint64)]
+
+
+class dci_fill_times(C.Structure):
+    _fields_ = [(k, C.c_float) for k in ("level2_ms", "adj_select_ms", "adj_copy_ms", "feat_select_ms",
+                                         "feat_copy_ms", "total_ms")]
 
 
 class dci_cache_info(C.Structure):
@@ -93,6 +98,7 @@ def lib():
         "dci_feature_partition_handle": [vp, vp],
         "dci_attach_feature_partitions": [vp, vp, i32],
         "dci_cache_info_get": [vp, C.POINTER(dci_cache_info)],
+        "dci_fill_times_get": [vp, C.POINTER(dci_fill_times)],
         "dci_cache_state": [vp, vp, vp, vp, vp, vp, vp],
         "dci_workspace_set_profiling": [vp, i32],
         "dci_workspace_stage_ms": [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)],
@@ -533,6 +539,13 @@ def cache_info(ctx: Context) -> dict:
     info = dci_cache_info()
     _check(lib().dci_cache_info_get(ctx.handle, C.byref(info)), "dci_cache_info_get")
     return {k: getattr(info, k) for k, _ in dci_cache_info._fields_}
+
+
+def fill_times(ctx: Context) -> dict:
+    """dci_fill_times_get: stage times (ms) of the context's last fill."""
+    t = dci_fill_times()
+    _check(lib().dci_fill_times_get(ctx.handle, C.byref(t)), "dci_fill_times_get")
+    return {k: float(getattr(t, k)) for k, _ in dci_fill_times._fields_}
 
 
 def cache_state(ctx: Context) -> dict:

@@ -325,6 +325,9 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
       ws->graph_exec[gi] = nullptr;
     }
     ws->n_graphs = 0;
+    // the cached signature matches no batch until every graph of this shape is built (a failed
+    // capture of graph gi >= 1 must not leave a signature that skips capture next time)
+    ws->graph_sig_len = 0;
     for (int gi = 0; gi < ngraphs; ++gi) {
       const uint64_t launches0 = ctx->launches;
       DCI_CUDA(cudaStreamBeginCapture(ws->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -341,10 +344,7 @@ dci_status run_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int3
       ctx->launches = launches0;  // counted when the graph actually runs
       e = cudaGraphInstantiate(&ws->graph_exec[gi], graph, 0);
       cudaGraphDestroy(graph);
-      if (e != cudaSuccess) {
-        ws->graph_sig_len = 0;
-        return cuda_fail(e, "cudaGraphInstantiate");
-      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
       ws->n_graphs = gi + 1;
     }
     memcpy(ws->graph_sig, &sig, sizeof(Sig));
@@ -887,7 +887,20 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     stage = w0->stage;
     w0->staged = true;
   }
-  launch_gather_many(ctx, ws, outs, n, L, stage, gs);
+  // node sweep when the group's frontier bounds together reach N (Reddit-shaped: one batch's bound
+  // alone is N); host-resident papers100M-shaped groups stay in row mode
+  bool sweep = false;
+  if (gather_sweep_enabled() && n >= 2) {
+    int64_t grow = 1;
+    for (int h = 0; h < L; ++h) grow = std::min<int64_t>(ctx->N, grow * (1 + (int64_t)fanouts[h]));
+    int64_t cover = 0;
+    for (int i = 0; i < n && cover < ctx->N; ++i) cover += std::min<int64_t>(ctx->N, (int64_t)B[i] * grow);
+    sweep = cover >= ctx->N;
+  }
+  {
+    dci_status gst = launch_gather_many(ctx, ws, outs, n, L, stage, sweep, gs);
+    if (gst != DCI_OK) return gst;
+  }
   enqueue_epilogue(s);
   if (phased) {
     DCI_CUDA(cudaEventRecord(ctx->gather_ev, gs));
@@ -1082,16 +1095,19 @@ dci_status dci_allocate(dci_ctx* ctx, uint64_t C, const uint64_t* t_sample_ns, c
   if (!c_adj || !c_feat || n < 0) return fail(DCI_EINVAL, "bad arguments");
   if (n > 0 && (!t_sample_ns || !t_feature_ns)) return fail(DCI_EINVAL, "null time arrays");
   if (C == 0) {
-    // auto budget: free device memory minus the predicted peak workload minus 1 GiB
+    // auto budget: what stays free for the caches once the fill is done.  Free device
+    // memory now (the caller's inference workspaces and outputs, created before this call, are
+    // already excluded: dci.h) + memory the fill gives back (current caches, the presample
+    // workspace) - the fill's own temporaries - the 1 GiB reserve (C21).
     if (!ctx) return fail(DCI_EINVAL, "auto budget needs a context");
     DeviceGuard g(ctx->device);
     size_t free_b = 0, total_b = 0;
     DCI_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    // memory the current caches hold is reusable by a refill
-    uint64_t held = (uint64_t)ctx->acache_len * 4 + (uint64_t)ctx->fcache_rows * 4 * ctx->pitch;
+    const uint64_t held = (uint64_t)ctx->acache_len * 4 + (uint64_t)ctx->fcache_rows * 4 * ctx->pitch;
+    const uint64_t pre = ctx->pre_ws ? ctx->presample_peak : 0;
     const uint64_t reserve = 1ull << 30;
-    uint64_t avail = (uint64_t)free_b + held;
-    uint64_t need = ctx->presample_peak + reserve;
+    const uint64_t avail = (uint64_t)free_b + held + pre;
+    const uint64_t need = fill_temp_bound(ctx->N, ctx->E) + reserve;
     C = avail > need ? avail - need : 0;
   }
   unsigned __int128 adj;
@@ -1169,6 +1185,17 @@ dci_status dci_attach_feature_partitions(dci_ctx* ctx, const void* handles, int3
     ctx->h_fbases[p] = static_cast<const float*>(ptr);
   }
   DCI_CUDA(cudaMemcpy(ctx->d_fbases, ctx->h_fbases, sizeof(float*) * dci_ctx::kMaxParts, cudaMemcpyHostToDevice));
+  return DCI_OK;
+}
+
+dci_status dci_fill_times_get(const dci_ctx* ctx, dci_fill_times* out) {
+  if (!ctx || !out) return fail(DCI_EINVAL, "null argument");
+  out->level2_ms = ctx->fill_ms[0];
+  out->adj_select_ms = ctx->fill_ms[1];
+  out->adj_copy_ms = ctx->fill_ms[2];
+  out->feat_select_ms = ctx->fill_ms[3];
+  out->feat_copy_ms = ctx->fill_ms[4];
+  out->total_ms = ctx->fill_ms[5];
   return DCI_OK;
 }
 

@@ -92,6 +92,8 @@ struct dci_ctx {
   int32_t whole_fit = 0;
   uint64_t c_adj = 0, c_feat = 0;
   uint64_t presample_peak = 0;
+  // stage times of the last fill (dci_fill_times), ms; -1 = stage not run
+  float fill_ms[6] = {-1.f, -1.f, -1.f, -1.f, -1.f, -1.f};
   uint64_t launches = 0;
   cudaStream_t gstream = nullptr;  // shared gather stream (serial-gather mode)
   cudaEvent_t gather_ev = nullptr;  // end of the last group gather (DCI_PHASED experiments)
@@ -250,8 +252,11 @@ bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
 bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out);
 // Multi-batch TMA gather (dci_sample_gather_many): every output takes bulk stores.
 bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t n);
-void launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n, int32_t L,
-                        dci_batch_result* stage, cudaStream_t s);
+// sweep: the group's frontiers may together cover the node set (sum of their bounds >= N), so the
+// node-sweep gather (each feature row read once for all batches) is used; else row mode.
+dci_status launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n,
+                              int32_t L, dci_batch_result* stage, bool sweep, cudaStream_t s);
+bool gather_sweep_enabled();  // env DCI_SWEEP (default 1)
 // Gather blocks per SM: the HBM-bound gather is given a small share of each SM when many
 // batches are in flight (their sampling kernels must co-reside), the whole SM when one is.
 int gather_blocks_per_sm(const dci_ctx* ctx);
@@ -271,6 +276,8 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
                      uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s,
                      const KnapsackPlan* knap = nullptr);
 void launch_build_directory(dci_ctx* ctx, const int64_t* d_indptr, cudaStream_t s);
+uint64_t fill_temp_bound(int64_t N, int64_t E);  // device temporaries of one fill (auto budget)
+void release_presample(dci_ctx* ctx);
 void release_feature_partitions(dci_ctx* ctx);
 
 inline int grid_for(const dci_ctx* ctx, int blocks_per_sm) { return ctx->num_sms * blocks_per_sm; }

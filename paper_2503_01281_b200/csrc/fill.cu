@@ -604,9 +604,51 @@ void knapsack_levels(const std::vector<unsigned long long>& hf, const std::vecto
   *used = C - left;
 }
 
+// Upper bound of the device temporaries one fill holds at its peak, next to the new caches
+// (indptr + node totals + rank/list/tie arrays: <= 48 B per node; the original and reordered
+// CSC copies: 8 B per element, plus 16 B per element of radix ping-pong when counts exceed 255).
+// The auto budget (dci_allocate with C = 0) keeps this much free.
+uint64_t fill_temp_bound(int64_t N, int64_t E) {
+  return 48ull * (uint64_t)(N + 1) + 24ull * (uint64_t)E + (1ull << 20);
+}
+
+void release_presample(dci_ctx* ctx) {
+  // presample is not allowed after a fill (DCI_ESTATE), so its workspace and outputs are freed
+  // here: the auto budget counted their memory as available to the caches
+  if (ctx->pre_ws) dci_workspace_destroy(ctx->pre_ws);
+  ctx->pre_ws = nullptr;
+  if (ctx->pre_out_mem) cudaFree(ctx->pre_out_mem);
+  ctx->pre_out_mem = nullptr;
+}
+
+// CUDA events at the fill's stage boundaries (dci_fill_times): recorded on the fill stream, read
+// once the fill has synchronised; destroyed on every exit path.
+struct FillClock {
+  cudaEvent_t e[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t s;
+  explicit FillClock(cudaStream_t st) : s(st) {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+  void mark(int i) {
+    if (e[i]) cudaEventRecord(e[i], s);
+  }
+  float ms(int a, int b) const {
+    float t = 0.f;
+    return (e[a] && e[b] && cudaEventElapsedTime(&t, e[a], e[b]) == cudaSuccess) ? t : -1.f;
+  }
+  ~FillClock() {
+    for (auto& x : e)
+      if (x) cudaEventDestroy(x);
+  }
+};
+
 dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* edge_counts, uint64_t c_adj,
                      uint64_t c_feat, int32_t world, int32_t rank, cudaStream_t s, const KnapsackPlan* knap) {
   const int64_t N = ctx->N, E = ctx->E;
+  release_presample(ctx);
+  for (auto& t : ctx->fill_ms) t = -1.f;
+  FillClock clk(s);
+  clk.mark(0);
   const int64_t row_bytes = 4ll * ctx->pitch;
   // c_feat is the budget of ONE partition; the admitted set spans all `world` partitions
   const int64_t cap_part = (int64_t)std::min<uint64_t>((uint64_t)N, c_feat / (uint64_t)row_bytes);
@@ -696,6 +738,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     ctx->u_idx_cur = static_cast<const int32_t*>(dp);
   }
   if (E) DCI_CUDA(cudaMemcpyAsync(ctx->h_idx_cur, d_idxR, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+  clk.mark(1);  // level 2 done: reordered CSC on the host
 
   // ---- drop old caches, reset the directory's cache fields ----
   DCI_CUDA(cudaStreamSynchronize(s));
@@ -786,6 +829,9 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     DCI_CUDA(cudaGetLastError());
     DCI_CUDA(cudaStreamSynchronize(s));
     rollback.committed = true;
+    clk.mark(5);
+    ctx->fill_ms[0] = clk.ms(0, 1);
+    ctx->fill_ms[5] = clk.ms(0, 5);
     ctx->whole_fit = adj_elems == E ? 1 : 0;
     ctx->c_adj = (uint64_t)adj_elems * 4;
     ctx->c_feat = (uint64_t)rows * (uint64_t)row_bytes;
@@ -805,6 +851,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     AdjLenOp op{ak, stp, (unsigned long long)cap_e, ctx->d_dir};
     dci_status r = scan_nodes(ctx, op, N, d_sum, s);
     if (r != DCI_OK) return r;
+    clk.mark(2);
     if (whole_fit) {
       ctx->d_acache = d_idxR;  // the whole reordered CSC, cache_off == indptr
       tmp.forget(d_idxR);
@@ -815,7 +862,10 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
       ++ctx->launches;
     }
     ctx->acache_len = cap_e;
+  } else {
+    clk.mark(2);
   }
+  clk.mark(3);
 
   // ---- feature cache ----
   if (cap_rows > 0) {
@@ -831,6 +881,7 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     FeatSlotOp op{fk, stp, ctx->d_dir, d_list};
     dci_status r = scan_nodes(ctx, op, N, d_sum, s);
     if (r != DCI_OK) return r;
+    clk.mark(4);
     // rows held on this device: all of them (world 1 or emulation), else this rank's share
     const int64_t local_rows = rank < 0 || world == 1 ? cap_rows : (cap_rows - rank + world - 1) / world;
     DCI_CUDA(cudaMalloc(&ctx->d_fcache, (size_t)row_bytes * std::max<int64_t>(local_rows, 1)));
@@ -845,6 +896,8 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
     DCI_CUDA(cudaStreamSynchronize(s));
     ctx->fcache_rows = local_rows;
     ctx->fcache_total_rows = cap_rows;
+  } else {
+    clk.mark(4);
   }
   // partition base pointers (peers are attached later through dci_attach_feature_partitions)
   int64_t off = 0;
@@ -860,9 +913,12 @@ dci_status fill_impl(dci_ctx* ctx, const int32_t* node_visits, const int32_t* ed
   if (!ctx->d_fbases) DCI_CUDA(cudaMalloc(&ctx->d_fbases, sizeof(float*) * dci_ctx::kMaxParts));
   DCI_CUDA(cudaMemcpyAsync(ctx->d_fbases, ctx->h_fbases, sizeof(float*) * dci_ctx::kMaxParts,
                            cudaMemcpyHostToDevice, s));
+  clk.mark(5);
   DCI_CUDA(cudaGetLastError());
   DCI_CUDA(cudaStreamSynchronize(s));
   rollback.committed = true;
+  for (int i = 0; i < 5; ++i) ctx->fill_ms[i] = clk.ms(i, i + 1);
+  ctx->fill_ms[5] = clk.ms(0, 5);
   ctx->whole_fit = whole_fit ? 1 : 0;
   ctx->c_adj = c_adj;
   ctx->c_feat = c_feat;

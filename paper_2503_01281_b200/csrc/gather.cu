@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 constexpr int kTmaMaxSlots = 16;
 constexpr int kTmaMaxWarps = 8;
 constexpr int kTmaMaxBatches = DCI_MAX_GROUP;
+constexpr int kMaxDevices = 64;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -260,9 +262,6 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 
 struct TmaArgs {
   int32_t hint;       // 1: evict-first L2 hint on rows and X, 0: evict-normal
-  int32_t sweep;      // node-sweep mode allowed (group launches, see gather_sweep)
-  int32_t Rs;         // rows per chunk in sweep mode (<= R)
-  int32_t meta_off;   // byte offset of the sweep metadata area in dynamic shared memory
   int32_t K;          // ring slots per warp
   int32_t R;          // rows per chunk (slot)
   int32_t row_bytes;  // 4 * pitch
@@ -276,6 +275,8 @@ struct TmaBatch {
   BatchScalars* sc;       // the batch's workspace scalars (sizes[L], counters, status)
   float* X;
   int64_t ldx;            // floats
+  int32_t out16;          // 16-byte words written per X row by the node sweep (whole 128-byte lines
+                          // when ldx is a multiple of 32 floats and X is 128-byte aligned, else pitch)
   int32_t* node_visits;   // presample only
   int64_t* out_sizes;
   uint64_t* out_counters;
@@ -298,145 +299,260 @@ struct TmaBatches {
 };
 
 
-// ------------------------------------------------------------------------------------
-// Node-sweep mode of a group launch (2..kSweepMax batches whose frontiers together hold at least N
-// rows, e.g. Reddit-shaped graphs where one batch touches 61 % of all nodes).  Instead of reading
-// a feature row once per (batch, row), the warps sweep node ids v = 0..N-1 and look v up in every
-// batch's node -> local-id table (the epoch-tagged position table the sampler leaves behind: v is
-// in batch b's F_L iff its tag carries b's epoch, and the tag's low word is then v's row).  A
-// node present in any batch is read ONCE (cp.async.bulk into the shared-memory ring) and written
-// to every batch that holds it (one bulk store per (batch, row)).  Reads drop from sum_b |F_L(b)|
-// rows to |union_b F_L(b)| rows and are in ascending cache-slot order; X is bit-identical.
-// ------------------------------------------------------------------------------------
-constexpr int kSweepMax = 32;  // batches per sweep launch (32-bit presence masks)
-
-template <int SMAX>
-
-__device__ __forceinline__ void gather_sweep(const TmaBatches& a, const TmaArgs& t, uint32_t ring, int* meta,
-                                             unsigned long long* bars, int* s_nr, unsigned (*s_cnt)[2],
-                                             unsigned* s_reads, int lane, int64_t gw, int64_t nw, uint64_t pol) {
-  const int K = t.K, R = t.Rs, nb = a.n;
-  const int MS = R * (1 + SMAX);  // ints of metadata per slot: R masks, R x SMAX rows
-  const int64_t lo = a.N * gw / nw, hi = a.N * (gw + 1) / nw;
-  uint32_t ep[SMAX];
-  const unsigned long long* pt[SMAX];
-#pragma unroll
-  for (int b = 0; b < SMAX; ++b) {
-    ep[b] = b < nb ? __ldcg(&a.b[b].sc->hdr.epoch) : 0u;
-    pt[b] = b < nb ? a.b[b].pos_of : nullptr;
+// Shared end of a group gather launch (row mode and node sweep): per-batch feature hit/miss
+// counts and the rows this block read are folded into the workspaces' scalars; the last block
+// books the launch's algorithmic bytes on the first batch and publishes every
+// batch's sizes / counters / status (and the staging record), then resets the scalars.
+//  rows:  sum_b |F_L(b)| x (row read 4D + row write 4D + 4 B slot lookup)
+//  sweep: N x (8 B tag probe per batch + 4 B slot lookup) + |union| x 4D + sum_b |F_L(b)| x 4D
+__device__ __forceinline__ void group_epilogue(const TmaBatches& a, const unsigned (*s_cnt)[2], unsigned s_reads,
+                                               long long tot_rows, bool sweep) {
+  const int nb = a.n;
+  if (threadIdx.x == 0 && s_reads) atomicAdd(&a.b[0].sc->launch_reads, (unsigned long long)s_reads);
+  if (threadIdx.x < nb) {
+    const int i = threadIdx.x;
+    if (s_cnt[i][0]) atomicAdd(&a.b[i].sc->counters[2], (unsigned long long)s_cnt[i][0]);
+    if (s_cnt[i][1]) atomicAdd(&a.b[i].sc->counters[3], (unsigned long long)s_cnt[i][1]);
   }
-  // one group of 32 consecutive node ids: lane j holds v = g + j.  The next group's table tags and
-  // directory slot are loaded while the current group issues.
-  unsigned long long nt[SMAX];
-  int32_t ns = -1;
-  auto probe = [&](int64_t g) {
-    const int64_t v = g + lane;
-    const bool in = v < hi;
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.b[0].sc->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    BatchScalars* sc0 = a.b[0].sc;
+    const unsigned long long reads = __ldcg(&sc0->launch_reads);
+    const unsigned long long tot = (unsigned long long)tot_rows;
+    const unsigned long long rowb = 4ull * (unsigned long long)a.D;
+    sc0->acc_rows_read += reads;
+    sc0->acc_gather_bytes += sweep ? (unsigned long long)a.N * (8ull * nb + 4ull) + reads * rowb + tot * rowb
+                                   : tot * (2ull * rowb + 4ull);
+    sc0->launch_reads = 0;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < nb) {
+    __threadfence();
+    const TmaBatch& tb = a.b[threadIdx.x];
+    BatchScalars* sc = tb.sc;
+    const int32_t B = sc->hdr.B;
+    tb.out_sizes[0] = B;
+    for (int h = 1; h <= a.L; ++h) tb.out_sizes[h] = __ldcg(&sc->sizes[h]);
+    for (int c = 0; c < 4; ++c) {
+      tb.out_counters[c] = __ldcg(&sc->counters[c]);
+      sc->counters[c] = 0;
+    }
+    *tb.out_status = __ldcg(&sc->status);
+    if (a.stage) {
+      dci_batch_result& r = a.stage[threadIdx.x];
+      for (int h = 0; h <= a.L; ++h) r.sizes[h] = tb.out_sizes[h];
+      for (int c = 0; c < 4; ++c) r.counters[c] = tb.out_counters[c];
+      r.status = *tb.out_status;
+    }
+    sc->acc_batches += 1;
+    sc->acc_seeds += (unsigned long long)B;
+    sc->acc_rows += (unsigned long long)__ldcg(&sc->sizes[a.L]);
+    for (int c = 0; c < 4; ++c) sc->acc_counters[c] += tb.out_counters[c];
+    sc->status = 0;
+    if (threadIdx.x == 0) sc->done = 0;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// k_gather_sweep: node-sweep gather of a group (2..32 batches whose frontiers together cover the
+// node set, e.g. Reddit-shaped graphs where one batch touches 61 % of all nodes).  The draws of a
+// node do not depend on its batch (C4), so the batches of a group share most rows: instead of
+// reading a feature row once per (batch, row), warps sweep node ids and look every node up in each
+// batch's node -> local-id table (the epoch-tagged position table the sampler leaves behind: v is
+// in batch b's F_L iff its tag carries b's epoch, and the tag's low word is then ~row).  A node
+// present in any batch is read ONCE and written to every batch that holds it.  X is bit-identical
+// to the row-mode gather.
+//  probe  lane j of a warp owns node g + j: one coalesced 8-byte tag load per batch (a warp reads
+//         256 contiguous bytes of each table) + its directory slot; the rows it holds go to a
+//         per-warp shared-memory table (batch-major, conflict-free)
+//  copy   the warp walks its present nodes two at a time: all lanes load both rows (16 B per lane,
+//         register copies; HBM cache row on a hit, pinned host row through UVA on a miss) and store
+//         each to every batch holding it.  Rows are written as whole 128-byte lines when the
+//         output allows it (out16: zeros past the pitch): random-row writes of partial lines run
+//         at ~4.0 TB/s on this B200, of whole lines at ~5.4-5.7 TB/s (tools/probe/scatter_probe.cu,
+//         profiles/r02/scatter_probe.md).
+// No per-lane arrays and no ring: ~40 registers, so many warps per SM hide the probe latency, and
+// the SM's remaining registers are left to the next group's sampling kernels.
+// ------------------------------------------------------------------------------------
+constexpr int kSweepWarps = 8;
+constexpr int kSweepMax = DCI_MAX_GROUP;  // 32-bit presence masks
+
+// X row address of node j (lane index in the warp's group) in batch b
+__device__ __forceinline__ int4* sweep_dst(const TmaBatches& a, const int* rt, int b, int j) {
+  const TmaBatch& tb = a.b[b];
+  return reinterpret_cast<int4*>(tb.X + (int64_t)rt[b * 32 + j] * tb.ldx);
+}
+
+// Row of one node (registers, VPL 16-byte words per lane per pass) -> every batch in mask m.  The
+// destinations are taken two at a time, so the row-table (shared) and batch-table (constant) loads
+// of the second overlap the first's stores.
+template <int VPL>
+__device__ __forceinline__ void sweep_store(const TmaBatches& a, const int* rt, int j, unsigned m, const int4 (&buf)[VPL],
+                                            int c0, int lane, uint64_t pol) {
+  while (m) {
+    const int b1 = __ffs(m) - 1;
+    m &= m - 1;
+    const int b2 = m ? __ffs(m) - 1 : -1;
+    if (m) m &= m - 1;
+    int4* d1 = sweep_dst(a, rt, b1, j);
+    const int o1 = a.b[b1].out16;
+    int4* d2 = b2 >= 0 ? sweep_dst(a, rt, b2, j) : nullptr;
+    const int o2 = b2 >= 0 ? a.b[b2].out16 : 0;
 #pragma unroll
-    for (int b = 0; b < SMAX; ++b) nt[b] = (in && b < nb) ? __ldcg(pt[b] + v) : 0ull;
-    ns = in ? __ldg(&a.dir[v].slot) : -1;
-  };
-  int64_t g_cur = lo;
-  unsigned cmask = 0;
-  int crow[SMAX];
-  const char* csrc = nullptr;
-  probe(g_cur);
-  auto start = [&]() {
-    cmask = 0;
+    for (int k = 0; k < VPL; ++k) {
+      const int idx = c0 + lane + 32 * k;
+      if (idx < o1) st_v4(d1 + idx, buf[k], pol);
+    }
+    if (d2) {
 #pragma unroll
-    for (int b = 0; b < SMAX; ++b) {
-      crow[b] = -1;
-      if (b < nb && (uint32_t)(nt[b] >> 32) == ep[b]) {
-        crow[b] = (int)(0xFFFFFFFFu - (uint32_t)nt[b]);
-        cmask |= 1u << b;
+      for (int k = 0; k < VPL; ++k) {
+        const int idx = c0 + lane + 32 * k;
+        if (idx < o2) st_v4(d2 + idx, buf[k], pol);
       }
     }
-    const int64_t v = g_cur + lane;
-    const int32_t sl = ns;
-    csrc = nullptr;
-    if (cmask) {
+  }
+}
+
+// Two nodes (rows s1 -> mask m1, s2 -> m2; s2 may be null): both rows' loads are issued before
+// any store.
+template <int VPL>
+__device__ __forceinline__ void sweep_copy(const TmaBatches& a, const int* rt, int row16, const char* s1,
+                                           unsigned m1, int j1, const char* s2, unsigned m2, int j2, int lane,
+                                           int out16max, uint64_t pol) {
+  for (int c0 = 0; c0 < out16max; c0 += 32 * VPL) {
+    int4 b1[VPL], b2[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int idx = c0 + lane + 32 * k;
+      b1[k] = idx < row16 ? ld_stream_v4(reinterpret_cast<const int4*>(s1) + idx, pol) : make_int4(0, 0, 0, 0);
+      b2[k] = (s2 && idx < row16) ? ld_stream_v4(reinterpret_cast<const int4*>(s2) + idx, pol)
+                                  : make_int4(0, 0, 0, 0);
+    }
+    sweep_store<VPL>(a, rt, j1, m1, b1, c0, lane, pol);
+    if (s2) sweep_store<VPL>(a, rt, j2, m2, b2, c0, lane, pol);
+  }
+}
+
+// cp.async (LDGSTS) of 4/8 bytes global -> shared; src_bytes 0 fills zeros (a node past N)
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int VPL>
+__global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_constant__ TmaBatches a,
+                                                                   int32_t out16max, int32_t hint) {
+  // dynamic shared memory, per warp: tag stage [nb][32] u64 (the next group's probes, in flight
+  // while the current group copies), slot stage [32] i32, row table [nb][32] i32
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  __shared__ uint32_t s_ep[kSweepMax];
+  __shared__ unsigned s_cnt[kSweepMax][2];
+  __shared__ unsigned s_reads;
+  __shared__ long long s_tot;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nb = a.n;
+  if (threadIdx.x < nb) s_ep[threadIdx.x] = __ldcg(&a.b[threadIdx.x].sc->hdr.epoch);
+  if (threadIdx.x < 2 * kSweepMax) (&s_cnt[0][0])[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) {
+    s_reads = 0u;
+    long long acc = 0;
+    for (int i = 0; i < nb; ++i) acc += __ldcg(&a.b[i].sc->sizes[a.L]);
+    s_tot = acc;
+  }
+  __syncthreads();
+  unsigned char* mine = s_dyn + (size_t)wib * (nb * 32 * 12 + 128);
+  unsigned long long* stag = reinterpret_cast<unsigned long long*>(mine);  // [nb][32]
+  int* sslot = reinterpret_cast<int*>(mine + nb * 32 * 8);                 // [32]
+  int* rt = sslot + 32;                                                     // [nb][32]
+  const uint64_t pol = hint ? policy_evict_first() : policy_evict_normal();
+  const int row16 = a.pitch >> 2;
+  const int64_t nw = (int64_t)gridDim.x * kSweepWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kSweepWarps + wib;
+  // probes of the group starting at node g: lane j copies node g + j's tag in every batch table
+  // and its directory slot into the stage (zeros past N)
+  auto prefetch = [&](int64_t g) {
+    if (g >= a.N) return;
+    const int64_t v = g + lane;
+    const bool in = v < a.N;
+    const int64_t vv = in ? v : 0;
+    for (int b = 0; b < nb; ++b) cp_async8(stag + b * 32 + lane, a.b[b].pos_of + vv, in ? 8 : 0);
+    cp_async4(sslot + lane, &a.dir[vv].slot, in ? 4 : 0);
+  };
+  unsigned reads = 0, hits = 0, misses = 0;  // lane b counts batch b's feature hits / misses
+  int64_t g = gw * 32;
+  prefetch(g);
+  cp_async_commit();
+  for (; g < a.N; g += nw * 32) {
+    cp_async_wait_all();
+    __syncwarp();
+    const int64_t v = g + lane;
+    const int32_t sl = v < a.N ? sslot[lane] : -1;
+    unsigned mask = 0;
+    for (int b = 0; b < nb; ++b) {
+      const unsigned long long tg = stag[b * 32 + lane];
+      if ((uint32_t)(tg >> 32) == s_ep[b]) {
+        mask |= 1u << b;
+        rt[b * 32 + lane] = (int)(0xFFFFFFFFu - (uint32_t)tg);
+      }
+    }
+    __syncwarp();  // the stage is consumed: the next group's probes may overwrite it
+    prefetch(g + nw * 32);
+    cp_async_commit();
+    const char* src = nullptr;
+    if (mask) {
       if (sl < 0)
-        csrc = reinterpret_cast<const char*>(a.hfeats + v * a.pitch);
+        src = reinterpret_cast<const char*>(a.hfeats + v * a.pitch);
       else if (a.G == 1)
-        csrc = reinterpret_cast<const char*>(a.fcache + (int64_t)sl * a.pitch);
-      else
-        csrc = reinterpret_cast<const char*>(
+        src = reinterpret_cast<const char*>(a.fcache + (int64_t)sl * a.pitch);
+      else  // partitioned cache: local or peer (NVLink) rows
+        src = reinterpret_cast<const char*>(
             reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(a.fbases) + sl % a.G)) +
             (int64_t)(sl / a.G) * a.pitch);
-#pragma unroll
-      for (int b = 0; b < SMAX; ++b)
-        if ((cmask >> b) & 1u) atomicAdd(&s_cnt[b][sl >= 0 ? 0 : 1], 1u);
     }
-    probe(g_cur + 32);
-  };
-  start();
-  int off = 0;
-  int64_t issued = 0, consumed = 0;
-  auto issue = [&]() -> bool {
-    unsigned pres;
-    for (;;) {
-      if (g_cur >= hi) return false;
-      pres = __ballot_sync(0xffffffffu, cmask != 0) & (off >= 32 ? 0u : (0xffffffffu << off));
-      if (pres) break;
-      g_cur += 32;
-      off = 0;
-      start();
+    const unsigned hitm = __ballot_sync(0xffffffffu, sl >= 0);
+    for (int b = 0; b < nb; ++b) {
+      const unsigned inb = __ballot_sync(0xffffffffu, (mask >> b) & 1u);
+      if (lane == b) {
+        hits += __popc(inb & hitm);
+        misses += __popc(inb & ~hitm);
+      }
     }
-    unsigned chunk = 0, rest = pres;
-    for (int q = 0; q < R && rest; ++q) {
-      chunk |= rest & (0u - rest);
-      rest &= rest - 1;
+    unsigned m = __ballot_sync(0xffffffffu, mask != 0);
+    reads += __popc(m);
+    while (m) {
+      const int j1 = __ffs(m) - 1;
+      m &= m - 1;
+      const int j2 = m ? __ffs(m) - 1 : j1;
+      const bool two = m != 0;
+      if (m) m &= m - 1;
+      const char* s1 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), j1));
+      const unsigned m1 = __shfl_sync(0xffffffffu, mask, j1);
+      const char* s2 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), j2));
+      const unsigned m2 = __shfl_sync(0xffffffffu, mask, j2);
+      sweep_copy<VPL>(a, rt, row16, s1, m1, j1, two ? s2 : nullptr, two ? m2 : 0u, j2, lane, out16max, pol);
     }
-    const int cnt = __popc(chunk);
-    const int s = (int)(issued % K);
-    const uint32_t bar = smem_addr(bars + s);
-    const bool mine = (chunk >> lane) & 1u;
-    const int q = __popc(chunk & ((1u << lane) - 1u));
-    if (mine) {
-      int* m = meta + s * MS;
-      m[q] = (int)cmask;
-#pragma unroll
-      for (int b = 0; b < SMAX; ++b) m[R + q * SMAX + b] = crow[b];
-    }
-    if (lane == 0) {
-      s_nr[s] = cnt;
-      mbar_expect_tx(bar, (uint32_t)cnt * (uint32_t)t.row_bytes);
-      atomicAdd(s_reads, (unsigned)cnt);
-    }
-    __syncwarp();
-    if (mine) bulk_g2s(ring + (uint32_t)(s * t.slot_bytes + q * t.row_bytes), csrc, (uint32_t)t.row_bytes, bar, pol);
-    ++issued;
-    off = 32 - __clz(chunk);
-    if (!rest) {  // the group's present nodes are all issued: next group
-      g_cur += 32;
-      off = 0;
-      start();
-    }
-    return true;
-  };
-  for (int k = 0; k < K; ++k)
-    if (!issue()) break;
-  while (consumed < issued) {
-    const int s = (int)(consumed % K);
-    mbar_wait(smem_addr(bars + s), (uint32_t)((consumed / K) & 1));
-    const int nr = s_nr[s];
-    if (lane < nr) {
-      const int* m = meta + s * MS;
-      const unsigned mask = (unsigned)m[lane];
-      const uint32_t src = ring + (uint32_t)(s * t.slot_bytes + lane * t.row_bytes);
-#pragma unroll
-      for (int b = 0; b < SMAX; ++b)
-        if ((mask >> b) & 1u) {
-          const TmaBatch& tb = a.b[b];
-          bulk_s2g(tb.X + (int64_t)m[R + lane * SMAX + b] * tb.ldx, src, (uint32_t)t.row_bytes, pol);
-        }
-    }
-    bulk_commit();
-    ++consumed;
-    bulk_wait_read1();
-    __syncwarp();
-    if (issued < consumed - 1 + K) issue();
+    __syncwarp();  // every lane is done with the row table before the next group rewrites it
   }
+  cp_async_wait_all();
+  if (lane < nb) {
+    if (hits) atomicAdd(&s_cnt[lane][0], hits);
+    if (misses) atomicAdd(&s_cnt[lane][1], misses);
+  }
+  if (lane == 0 && reads) atomicAdd(&s_reads, reads);
+  __syncthreads();
+  group_epilogue(a, s_cnt, s_reads, s_tot, true);
 }
 
 __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_constant__ TmaBatches a, TmaArgs t) {
@@ -448,7 +564,6 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
   __shared__ long long s_pre[kTmaMaxBatches + 1];       // row prefix over the launch's batches
   __shared__ unsigned s_cnt[kTmaMaxBatches][2];         // feature hits / misses per batch
   __shared__ unsigned s_reads;                          // feature rows this block read
-  __shared__ bool s_sweep;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int K = t.K, R = t.R, nb = a.n;
   const uint32_t ring = smem_addr(s_ring) + (uint32_t)(wib * K * t.slot_bytes);
@@ -471,17 +586,6 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const uint64_t pol = t.hint ? policy_evict_first() : policy_evict_normal();
-  const bool sweep = t.sweep && nb >= 2 && nb <= kSweepMax && ntot >= a.N;
-  if (threadIdx.x == 0) s_sweep = sweep;
-  if (sweep) {
-    int* meta = reinterpret_cast<int*>(s_ring + t.meta_off) + wib * K * t.Rs * (1 + kSweepMax);
-    if (nb <= 8)
-      gather_sweep<8>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
-    else if (nb <= 16)
-      gather_sweep<16>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
-    else
-      gather_sweep<32>(a, t, ring, meta, &s_bar[wib][0], &s_nr[wib][0], s_cnt, &s_reads, lane, gw, nw, pol);
-  } else {
   // balanced contiguous row ranges per warp over the concatenated batches
   const int64_t lo = ntot * gw / nw, hi = ntot * (gw + 1) / nw;
 
@@ -592,64 +696,9 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
     __syncwarp();
     if (issued < consumed - 1 + K) issue();
   }
-  }  // row mode
   bulk_wait_all();
   __syncthreads();
-  if (threadIdx.x == 0 && s_reads) atomicAdd(&a.b[0].sc->launch_reads, (unsigned long long)s_reads);
-  if (threadIdx.x < nb) {
-    const int i = threadIdx.x;
-    if (s_cnt[i][0]) atomicAdd(&a.b[i].sc->counters[2], (unsigned long long)s_cnt[i][0]);
-    if (s_cnt[i][1]) atomicAdd(&a.b[i].sc->counters[3], (unsigned long long)s_cnt[i][1]);
-  }
-  // the last block publishes every batch's scalars and resets them for its next batch (done
-  // counter of the first batch's scalars)
-  __shared__ bool s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&a.b[0].sc->done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    // algorithmic gather bytes of this launch, booked on the first batch:
-    //  rows:  sum_b |F_L(b)| x (row read 4D + row write 4D + 4 B slot lookup)
-    //  sweep: N x (8 B tag probe per batch + 4 B slot lookup) + |union| x 4D + sum_b |F_L(b)| x 4D
-    __threadfence();
-    BatchScalars* sc0 = a.b[0].sc;
-    const unsigned long long reads = __ldcg(&sc0->launch_reads);
-    const unsigned long long tot = (unsigned long long)s_pre[nb];
-    const unsigned long long rowb = 4ull * (unsigned long long)a.D;
-    sc0->acc_rows_read += reads;
-    sc0->acc_gather_bytes += s_sweep ? (unsigned long long)a.N * (8ull * nb + 4ull) + reads * rowb + tot * rowb
-                                     : tot * (2ull * rowb + 4ull);
-    sc0->launch_reads = 0;
-  }
-  __syncthreads();
-  if (s_last && threadIdx.x < nb) {
-    __threadfence();
-    const TmaBatch& tb = a.b[threadIdx.x];
-    BatchScalars* sc = tb.sc;
-    const int32_t B = sc->hdr.B;
-    tb.out_sizes[0] = B;
-    for (int h = 1; h <= a.L; ++h) tb.out_sizes[h] = __ldcg(&sc->sizes[h]);
-    for (int c = 0; c < 4; ++c) {
-      tb.out_counters[c] = __ldcg(&sc->counters[c]);
-      sc->counters[c] = 0;
-    }
-    *tb.out_status = __ldcg(&sc->status);
-    if (a.stage) {
-      dci_batch_result& r = a.stage[threadIdx.x];
-      for (int h = 0; h <= a.L; ++h) r.sizes[h] = tb.out_sizes[h];
-      for (int c = 0; c < 4; ++c) r.counters[c] = tb.out_counters[c];
-      r.status = *tb.out_status;
-    }
-    sc->acc_batches += 1;
-    sc->acc_seeds += (unsigned long long)B;
-    sc->acc_rows += (unsigned long long)__ldcg(&sc->sizes[a.L]);
-    for (int c = 0; c < 4; ++c) sc->acc_counters[c] += tb.out_counters[c];
-    sc->status = 0;
-    if (threadIdx.x == 0) sc->done = 0;
-  }
+  group_epilogue(a, s_cnt, s_reads, s_pre[nb], false);
 }
 
 int env_int(const char* name, int dflt) {
@@ -689,28 +738,23 @@ static bool tma_config(const dci_ctx* ctx, const dci_batch_out* out, TmaArgs* t,
   static const int smem_kb = std::max(16, std::min(220, env_int("DCI_TMA_SMEM_KB", 200)));
   static const int chunk_target = env_int("DCI_TMA_CHUNK", 8192);
   static const int hint = env_int("DCI_TMA_HINT", 1);
-  static const int sweep = env_int("DCI_SWEEP", 1);
   const int row_bytes = ctx->pitch * 4;
   int R = std::max(1, std::min(32, (chunk_target + row_bytes / 2) / row_bytes));
   const int ring = smem_kb * 1024 / W;
-  auto per_slot = [&](int r) { return r * row_bytes + std::min(r, 4) * (1 + kSweepMax) * 4; };
-  int K = ring / per_slot(R);
+  int K = ring / (R * row_bytes);
   while (K < 4 && R > 1) {
     R = (R + 1) / 2;
-    K = ring / per_slot(R);
+    K = ring / (R * row_bytes);
   }
   K = std::min(K, kTmaMaxSlots);
   if (K < 3) return false;
   t->hint = hint;
-  t->sweep = sweep;
-  t->Rs = std::min(R, 4);
   t->K = K;
   t->R = R;
   t->row_bytes = row_bytes;
   t->slot_bytes = R * row_bytes;
-  t->meta_off = W * K * t->slot_bytes;
   *warps = W;
-  *smem = (size_t)t->meta_off + (size_t)W * K * t->Rs * (1 + kSweepMax) * 4;
+  *smem = (size_t)W * K * t->slot_bytes;
   return true;
 }
 
@@ -745,43 +789,98 @@ static TmaBatches tma_batches(const dci_ctx* ctx, int32_t L) {
   return tb;
 }
 
-static void tma_add(TmaBatches* tb, dci_workspace* ws, const dci_batch_out* out, int32_t* node_visits) {
+// 16-byte words the node sweep writes per X row: whole 128-byte lines (zeros past the pitch) when
+// the row stride is a multiple of 32 floats and X is 128-byte aligned, else the pitch
+static int32_t sweep_out16(const dci_ctx* ctx, const dci_batch_out* out) {
+  if (out->ldx % 32 == 0 && reinterpret_cast<uintptr_t>(out->X) % 128 == 0) return ((ctx->pitch + 31) / 32) * 8;
+  return ctx->pitch / 4;
+}
+
+static void tma_add(TmaBatches* tb, const dci_ctx* ctx, dci_workspace* ws, const dci_batch_out* out,
+                    int32_t* node_visits) {
   TmaBatch& b = tb->b[tb->n++];
   b.F = out->frontier;
   b.pos_of = ws->pos_of;
   b.sc = ws->scal;
   b.X = out->X;
   b.ldx = out->ldx;
+  b.out16 = sweep_out16(ctx, out);
   b.node_visits = node_visits;
   b.out_sizes = out->sizes;
   b.out_counters = out->counters;
   b.out_status = out->status;
 }
 
-static void tma_launch(dci_ctx* ctx, const TmaBatches& tb, const dci_batch_out* out0, cudaStream_t s) {
+// cudaFuncAttributeMaxDynamicSharedMemorySize applies to the current device only: remember, per
+// device, the largest value set so far (a process-wide static skipped the second GPU)
+static dci_status ensure_dyn_smem(const void* kernel, std::atomic<int>* set_for, int device, size_t smem) {
+  if (device < 0 || device >= kMaxDevices) return fail(DCI_EINVAL, "device index out of range");
+  int cur = set_for[device].load();
+  if ((int)smem <= cur) return DCI_OK;
+  DCI_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  while (cur < (int)smem && !set_for[device].compare_exchange_weak(cur, (int)smem)) {
+  }
+  return DCI_OK;
+}
+
+static dci_status tma_launch(dci_ctx* ctx, const TmaBatches& tb, const dci_batch_out* out0, cudaStream_t s) {
   TmaArgs t;
   int warps = 0;
   size_t smem = 0;
   tma_config(ctx, out0, &t, &warps, &smem);
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set = smem;
-  }
+  static std::atomic<int> smem_set[kMaxDevices];
+  dci_status st = ensure_dyn_smem(reinterpret_cast<const void*>(k_gather_tma), smem_set, ctx->device, smem);
+  if (st != DCI_OK) return st;
   static const int bps = std::max(1, std::min(4, env_int("DCI_TMA_BPS", 1)));
   // DCI_TMA_SMS: SMs the gather grid covers (default all; a measurement knob)
   static const int sms = env_int("DCI_TMA_SMS", 0);
   const int nsm = (sms > 0 && sms < ctx->num_sms) ? sms : ctx->num_sms;
   k_gather_tma<<<nsm * bps, 32 * warps, smem, s>>>(tb, t);
   ++ctx->launches;
+  return DCI_OK;
 }
 
-void launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n, int32_t L,
-                        dci_batch_result* stage, cudaStream_t s) {
+template <int VPL>
+static dci_status sweep_launch_v(dci_ctx* ctx, const TmaBatches& tb, int32_t out16max, cudaStream_t s) {
+  static std::atomic<int> smem_set[kMaxDevices];
+  const size_t smem = (size_t)kSweepWarps * ((size_t)tb.n * 32 * 12 + 128);
+  const void* kern = reinterpret_cast<const void*>(k_gather_sweep<VPL>);
+  dci_status st = ensure_dyn_smem(kern, smem_set, ctx->device, smem);
+  if (st != DCI_OK) return st;
+  static const int hint = env_int("DCI_TMA_HINT", 1);
+  // grid: the blocks (of 8 warps) that are resident at once (register-limited: 3 per SM at VPL 5),
+  // so no block waits for a second wave; DCI_SWEEP_BPS caps it (a measurement knob)
+  int occ = 0;
+  DCI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kSweepWarps, smem));
+  static const int cap = env_int("DCI_SWEEP_BPS", 0);
+  const int bps = std::max(1, cap > 0 ? std::min(cap, occ) : occ);
+  k_gather_sweep<VPL><<<ctx->num_sms * bps, 32 * kSweepWarps, smem, s>>>(tb, out16max, hint);
+  ++ctx->launches;
+  return DCI_OK;
+}
+
+static dci_status sweep_launch(dci_ctx* ctx, const TmaBatches& tb, cudaStream_t s) {
+  int32_t out16max = 0;
+  for (int i = 0; i < tb.n; ++i) out16max = std::max(out16max, tb.b[i].out16);
+  // 16-byte words per lane per pass over a row (rows longer than 32 * VPL words take several passes)
+  if (out16max <= 32) return sweep_launch_v<1>(ctx, tb, out16max, s);
+  if (out16max <= 64) return sweep_launch_v<2>(ctx, tb, out16max, s);
+  if (out16max <= 96) return sweep_launch_v<3>(ctx, tb, out16max, s);
+  return sweep_launch_v<5>(ctx, tb, out16max, s);
+}
+
+bool gather_sweep_enabled() {
+  static const int sweep = env_int("DCI_SWEEP", 1);
+  return sweep != 0;
+}
+
+dci_status launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n,
+                              int32_t L, dci_batch_result* stage, bool sweep, cudaStream_t s) {
   TmaBatches tb = tma_batches(ctx, L);
   tb.stage = stage;
-  for (int i = 0; i < n; ++i) tma_add(&tb, ws[i], outs + i, nullptr);
-  tma_launch(ctx, tb, outs, s);
+  for (int i = 0; i < n; ++i) tma_add(&tb, ctx, ws[i], outs + i, nullptr);
+  if (sweep && n >= 2 && n <= kSweepMax) return sweep_launch(ctx, tb, s);
+  return tma_launch(ctx, tb, outs, s);
 }
 
 int gather_blocks_per_sm(const dci_ctx* ctx) {
@@ -831,8 +930,8 @@ bool launch_gather_fused(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dci_b
   const FusedArgs a = fused_args(ctx, ws, L, out, last, node_visits);
   if (gather_uses_tma(ctx, out)) {
     TmaBatches tb = tma_batches(ctx, L);
-    tma_add(&tb, ws, out, node_visits);
-    tma_launch(ctx, tb, out, s);
+    tma_add(&tb, ctx, ws, out, node_visits);
+    tma_launch(ctx, tb, out, s);  // (a failure surfaces at the next CUDA call on the stream)
     return false;  // relabel of the last hop not fused: launch_hop_epilogue
   }
   const int bps = gather_blocks_per_sm(ctx);

@@ -28,6 +28,9 @@ def init(backend: str = "nccl"):
     import torch.distributed as dist
     rank, world, local = dist_env()
     if world > 1 and not dist.is_initialized():
+        # NCCL's init log names the communicator's rank count (evidence that N ranks ran)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group(backend=backend, rank=rank, world_size=world)
     return rank, world, local
 
@@ -85,6 +88,21 @@ def sum_over_ranks(values, device=None, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t.cpu().numpy()
+
+
+def gather_clocks(local: dict, group=None) -> dict:
+    """Clock samples of every rank's GPU -> rank 0's view: the slowest rank's median SM clock, the
+    union of throttle reasons, and the per-rank records."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return dict(local, per_rank=[dict(local)])
+    allc = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allc, local, group=group)
+    mhz = [c["sm_mhz"] for c in allc if c.get("sm_mhz") is not None]
+    mx = [c["sm_max_mhz"] for c in allc if c.get("sm_max_mhz") is not None]
+    return {"sm_mhz": min(mhz) if mhz else None, "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted({r for c in allc for r in c.get("reasons", [])}),
+            "samples": sum(c.get("samples", 0) for c in allc), "per_rank": allc}
 
 
 def _ndev():

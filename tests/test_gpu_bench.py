@@ -22,12 +22,12 @@ def run_bench(*args, timeout=900):
     return json.loads(lines[0])
 
 
-def check_common(d, steps, warmup):
+def check_common(d, steps, warmup, n_gpus=1, scaling="weak"):
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "e2e"):
         assert k in d, k
-    assert d["steps"] == steps and d["warmup"] == warmup and d["n_gpus"] == 1
-    assert d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert d["steps"] == steps and d["warmup"] == warmup and d["n_gpus"] == n_gpus
+    assert d["higher_is_better"] is True and d["scaling"] == scaling
     assert d["value"] > 0 and d["ms_per_step"] > 0
     assert "workload" in d["config"]
     e = d["e2e"]
@@ -64,3 +64,18 @@ def test_bench_reference_arm_m1():
     assert d["impl"] == "reference"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["value"] == d["value"]
+
+
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_spawns_ranks_for_gpus_n(scaling):
+    """`bench.py --gpus 2` with no torchrun environment launches 2 ranks itself (here sharing the
+    one GPU over gloo); the line reports both ranks, the seeds of both, and per-rank clocks."""
+    steps = 20
+    d = run_bench("--gpus", "2", "--backend", "gloo", "--config", "M1", "--steps", str(steps), "--warmup", "4",
+                  "--repeats", "1", "--scaling", scaling, timeout=1200)
+    check_common(d, steps, 4, n_gpus=2, scaling=scaling)
+    assert d["config"]["ranks_share_gpus"] in (True, False)
+    B = d["config"]["batch_per_gpu"]
+    seeds = B * steps * (2 if scaling == "weak" else 1)
+    assert d["value"] == pytest.approx(seeds / (d["ms_per_step"] * steps / 1e3), rel=1e-6)
+    assert len(d["clocks"]["per_rank"]) == 2
