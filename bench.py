@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/check)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to test several ranks on one GPU)")
+    ap.add_argument("--shm-graph", default="auto", choices=["auto", "on", "off"],
+                    help="several ranks: one node-shared host graph adopted in place by every rank (DCI_ADOPT_HOST), "
+                         "auto = when /dev/shm can hold it")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank times K batches of its shard of the global list (task rule 5: the "
                          "path shards into independent batches); strong: the K batches of one global list are "
@@ -317,14 +320,31 @@ def run_ours(args):
 
     clk = ClockSampler(local)
     clk.start()
+    # ---- inputs + S0 load.  Several ranks on one node share ONE host copy of the graph
+    # (parallel.SharedGraph: local rank 0 generates it into /dev/shm, every rank's context adopts it
+    # in place with DCI_ADOPT_HOST) instead of a copy per rank ----
+    use_shm = world > 1 and args.shm_graph != "off" and parallel.SharedGraph.fits(cfg.N, cfg.E, cfg.D)
+    if args.shm_graph == "on" and not use_shm:
+        raise SystemExit("--shm-graph on: /dev/shm cannot hold the graph (or a single rank)")
     t0 = time.time()
-    ip, ix, ft = make_inputs(cfg, dev)
+    sg = None
+    if use_shm:
+        def gen():
+            ip_d, ix_d = synth.rmat_csc(cfg.N, cfg.E, seed=synth.GRAPH_SEED, device=dev)
+            return ip_d, ix_d, synth.features(cfg.N, cfg.D, device=dev)
+
+        sg = parallel.SharedGraph(cfg.N, cfg.E, cfg.D, gen)
+        torch.cuda.empty_cache()
+        ip, ix, ft = sg.indptr, sg.indices[:cfg.E], None
+    else:
+        ip, ix, ft = make_inputs(cfg, dev)
     t_gen = time.time() - t0
-    log(f"[bench] {cfg.name}: N={cfg.N} E={cfg.E} D={cfg.D} generated in {t_gen:.1f}s")
+    log(f"[bench] {cfg.name}: N={cfg.N} E={cfg.E} D={cfg.D} generated in {t_gen:.1f}s"
+        + (" (node-shared host graph, adopted in place)" if use_shm else ""))
 
     # ---- S0 load ----
     t1 = time.time()
-    ctx = dci.load_graph(ip, ix, ft, device=local)
+    ctx = sg.load(local) if use_shm else dci.load_graph(ip, ix, ft, device=local)
     t_load = time.time() - t1
     if args.no_cpu_baseline or world > 1 or args.profile_only:
         ft = None  # the library holds its own pinned copy; free host RAM (papers100M-shaped: 57 GB)
@@ -493,8 +513,10 @@ def run_ours(args):
     rows_read = sum(st["rows_read"] for st in sts)
     # the library's algorithmic gather bytes: row reads + row writes + lookups
     alg_bytes = float(sum(st["gather_bytes"] for st in sts))
+    host_rows = sum(st["host_rows_read"] for st in sts)
+    host_lines = sum(st["host_adj_lines"] for st in sts)
     tot = parallel.sum_over_ranks([sum(st["seeds"] for st in sts), launches, rows, alg_bytes, g_ms, s_ms, n_timed,
-                                   n_glaunch, rows_read, *cn.tolist()], device=dev)
+                                   n_glaunch, rows_read, *cn.tolist(), host_rows, host_lines], device=dev)
     seeds_all = tot[0] / R  # per timed region
     value = seeds_all / (ms / 1e3)
     rep_values = [seeds_all / (m / 1e3) for m in ms_list]
@@ -585,14 +607,37 @@ def run_ours(args):
     bind_peak = host_peak if host_bound else hbm_peak
     n_launch = max(1.0, tot[7])
     achieved_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per launch (live events)
-    kernel = ("k_gather_tma (group of %d: %s; route + feature gather, S7-S8)"
-              % (G, "node sweep, each row read once per group" if frac_read < 0.999 else "rows")) if G else \
+    kernel = (("k_gather_sweep (group of %d: node sweep, each row read once per group; route + feature gather, "
+               "S7-S8)" % G) if frac_read < 0.999 else
+              ("k_gather_tma (group of %d: rows; route + feature gather, S7-S8)" % G)) if G else \
         "k_gather (fused route + relabel + feature gather, S7-S8)"
     aggregate_gbs = bind_b / (ms_tot / 1e3) / 1e9  # all gather launches over the timed wall time
+    # Whole-step roofline of SURVEY §8(d), over all timed regions: T_roof = max(B_hbm/BW_hbm,
+    # B_host/BW_host, N_req/R_req).  Algorithmic bytes: HBM = the gather's hit-row reads and all row
+    # writes (+ lookups) + the sampler's cached element reads and candidate writes (4 B each); host =
+    # miss rows + 4 B per adjacency miss.  Requests: host feature rows + distinct 128-byte host lines
+    # of the adjacency misses (the library counts both).  R_req = the probe's random-read rate for a
+    # pinned region of the graph's size (tools/probe, profiles/hostlink_peaks.json).
+    host_rows_read, host_adj_lines = tot[13], tot[14]
+    samples = cn[0] + cn[1]
+    B_hbm = hbm_b + 4.0 * cn[0] + 4.0 * samples
+    B_host = host_rows_read * 4.0 * D + 4.0 * cn[1]
+    N_req = host_rows_read + host_adj_lines
+    region = cfg.N * 4.0 * cfg.pitch_floats() + 4.0 * cfg.E
+    req_rate = min(host_req_peak, host_link_peaks(region)[0] * 1e9 / 512.0 / 1e6)  # M requests/s
+    T_terms = {"hbm_ms": B_hbm / (hbm_peak * 1e9) * 1e3, "host_bytes_ms": B_host / (host_link_peaks()[0] * 1e9) * 1e3,
+               "host_requests_ms": N_req / (req_rate * 1e6) * 1e3}
+    T_roof = max(T_terms.values())
     host_link = {"feature_miss_GBps": host_b / (ms_tot / 1e3) / 1e9, "peak_GBps": host_peak,
                  "feature_frac": host_b / (ms_tot / 1e3) / 1e9 / host_peak,
                  "adj_miss_Mreads_per_s": cn[1] / (ms_tot / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
-                 "peak_kind": host_kind}
+                 "peak_kind": host_kind,
+                 "requests_M_per_s": N_req / (ms_tot / 1e3) / 1e6, "request_peak_M_per_s": req_rate,
+                 "host_rows_read": host_rows_read, "host_adj_lines": host_adj_lines,
+                 "step_roofline": {"T_roof_ms": T_roof, "T_measured_ms": ms_tot, "frac": T_roof / ms_tot,
+                                   "binding": max(T_terms, key=T_terms.get), **T_terms,
+                                   "note": "whole timed regions (all steps); T_roof = max(B_hbm/BW_hbm, "
+                                           "B_host/BW_host, N_req/R_req), SURVEY §8(d)"}}
     steps_total = steps_eff * world if args.scaling == "weak" else steps_eff
     avg_fl = tot[2] / max(1, steps_total * R)
     traffic = None
@@ -618,7 +663,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
         "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B,
-                   "ranks_share_gpus": shared_gpus, "fanouts": list(fan),
+                   "ranks_share_gpus": shared_gpus, "host_graph": "node-shared (adopted)" if use_shm else "per rank", "fanouts": list(fan),
                    "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
                    "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"

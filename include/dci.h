@@ -45,6 +45,8 @@ typedef enum dci_status {
 } dci_status;
 
 typedef struct dci_ctx dci_ctx;
+
+#define DCI_ADOPT_HOST 1u /* dci_load_graph flag: register the caller's host buffers in place */
 typedef struct dci_workspace dci_workspace;
 
 /* Context lifecycle states (dci_cache_info.state). */
@@ -62,7 +64,13 @@ enum { DCI_STATE_LOADED = 1, DCI_STATE_FILLED = 2 };
  *  (feature rows padded to pitch = round_up(D, 4) floats so every row is 16-byte aligned;
  *  the pad is zero) and builds the per-node device directory.  The caller's buffers may
  *  be freed on return.  Validates the CSC invariants (O(E) host pass) -> DCI_EINVAL.
- *  flags: reserved, pass 0.
+ *  flags: 0, or DCI_ADOPT_HOST: indices and feats are NOT copied but registered in place
+ *    (cudaHostRegister, mapped + portable) and read through UVA; feats must then already hold
+ *    N rows of pitch = round_up(D, 4) floats (pad columns zero, 16-byte aligned rows).  The
+ *    library never writes adopted memory (the fill's level-2 reordered CSC is its own buffer),
+ *    so several contexts -- e.g. one rank per GPU -- may adopt one node-shared segment (P:52,
+ *    papers100M stays host-resident).  The buffers must outlive the context;
+ *    dci_destroy unregisters them.  Registration failure -> DCI_ECUDA.
  *  Limits: 1 <= N < 2^31, 0 <= E < 2^40, 1 <= D.  *out owns all device and pinned memory.
  * ------------------------------------------------------------------------------------ */
 dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const int64_t* indptr,
@@ -319,6 +327,11 @@ dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* ga
  * rows_read: feature rows the gather actually read (a node-sweep group reads each row once
  * for all its batches); gather_bytes: the gather's algorithmic bytes (row
  * reads + row writes + lookups), also booked on a group's first workspace.
+ * host_rows_read: feature rows read from pinned host memory (misses; once per row in a node
+ * sweep); host_adj_lines: distinct 128-byte host lines read by adjacency misses (per dst node and
+ * hop; a node-sweep hop reads a node's elements once for all batches) -- the host-link request
+ * count of the bench roofline (T_roof = max(B_hbm/BW_hbm, B_host/BW_host,
+ * N_req/R_req)).  Both are booked on the first workspace of a launch.
  * reset != 0 zeroes the totals after reading them. */
 typedef struct dci_ws_stats {
   uint64_t batches;
@@ -331,6 +344,8 @@ typedef struct dci_ws_stats {
   uint64_t gather_launches;
   uint64_t rows_read;
   uint64_t gather_bytes;
+  uint64_t host_rows_read;
+  uint64_t host_adj_lines;
 } dci_ws_stats;
 
 dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset);

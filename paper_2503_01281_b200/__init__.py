@@ -53,7 +53,7 @@ class dci_ws_stats(C.Structure):
     _fields_ = [("batches", C.c_uint64), ("seeds", C.c_uint64), ("frontier_rows", C.c_uint64),
                 ("counters", C.c_uint64 * 4), ("timed_batches", C.c_uint64), ("sample_ms", C.c_double),
                 ("gather_ms", C.c_double), ("gather_launches", C.c_uint64), ("rows_read", C.c_uint64),
-                ("gather_bytes", C.c_uint64)]
+                ("gather_bytes", C.c_uint64), ("host_rows_read", C.c_uint64), ("host_adj_lines", C.c_uint64)]
 
 
 class dci_fill_times(C.Structure):
@@ -166,17 +166,38 @@ class Context:
         return int(lib().dci_launch_count(self.handle))
 
 
-def load_graph(indptr, indices, feats, device: int = 0) -> Context:
+ADOPT_HOST = 1  # DCI_ADOPT_HOST
+
+
+def load_graph(indptr, indices, feats, device: int = 0, adopt: bool = False, D: int | None = None) -> Context:
     """dci_load_graph (S0).  indptr int64[N+1], indices int32[E], feats fp32[N, D]: host arrays
-    (numpy or CPU torch); copied into pinned, device-mapped memory."""
+    (numpy or CPU torch); copied into pinned, device-mapped memory.
+
+    adopt=True (DCI_ADOPT_HOST): indices and feats are registered IN PLACE (no copy; e.g. a
+    node-shared shm segment, see parallel.shared_graph) and must stay alive as long as the
+    context (the Context keeps references).  feats must then be [N, pitch] with pitch =
+    round_up(D, 4) (pad columns zero); pass the true D when pitch != D."""
     ip = np.ascontiguousarray(_to_np(indptr), np.int64)
-    ix = np.ascontiguousarray(_to_np(indices), np.int32)
-    ft = np.ascontiguousarray(_to_np(feats), np.float32)
-    N, E, D = len(ip) - 1, len(ix), ft.shape[1]
+    if adopt:
+        ix, ft = _to_np(indices), _to_np(feats)
+        if not (ix.dtype == np.int32 and ix.flags.c_contiguous and ft.dtype == np.float32 and ft.flags.c_contiguous):
+            raise TypeError("adopt=True needs C-contiguous int32 indices and float32 feats (no copies are made)")
+        D = int(D if D is not None else ft.shape[1])
+        if ft.shape[1] != (D + 3) // 4 * 4:
+            raise ValueError(f"adopt=True: feats must be [N, round_up(D, 4)] = [N, {(D + 3) // 4 * 4}], "
+                             f"got {ft.shape}")
+    else:
+        ix = np.ascontiguousarray(_to_np(indices), np.int32)
+        ft = np.ascontiguousarray(_to_np(feats), np.float32)
+        D = ft.shape[1]
+    N, E = len(ip) - 1, len(ix)
     h = C.c_void_p()
     _check(lib().dci_load_graph(C.byref(h), device, N, E, _np_ptr(ip), _np_ptr(ix) if E else None, _np_ptr(ft),
-                                D, 0), "dci_load_graph")
-    return Context(h, N, E, D, device)
+                                D, ADOPT_HOST if adopt else 0), "dci_load_graph")
+    ctx = Context(h, N, E, D, device)
+    if adopt:
+        ctx._adopted = (ix, ft)  # the registered memory must outlive the context
+    return ctx
 
 
 def _to_np(a):
@@ -231,7 +252,8 @@ class Workspace:
         return {"batches": st.batches, "seeds": st.seeds, "frontier_rows": st.frontier_rows,
                 "counters": [int(c) for c in st.counters], "timed_batches": st.timed_batches,
                 "sample_ms": st.sample_ms, "gather_ms": st.gather_ms, "gather_launches": st.gather_launches,
-                "rows_read": st.rows_read, "gather_bytes": st.gather_bytes}
+                "rows_read": st.rows_read, "gather_bytes": st.gather_bytes,
+                "host_rows_read": st.host_rows_read, "host_adj_lines": st.host_adj_lines}
 
     def stage_ms(self):
         s, g = C.c_float(), C.c_float()

@@ -402,8 +402,9 @@ void free_ctx(dci_ctx* c) {
   if (c->d_fbases) cudaFree(c->d_fbases);
   if (c->d_fcache) cudaFree(c->d_fcache);
   if (c->h_idx_cur && c->h_idx_cur != c->h_idx_orig) cudaFreeHost(c->h_idx_cur);
-  if (c->h_idx_orig) cudaFreeHost(c->h_idx_orig);
-  if (c->h_feats) cudaFreeHost(c->h_feats);
+  // adopted caller memory (DCI_ADOPT_HOST) is only unregistered, never freed
+  if (c->h_idx_orig) (c->adopted_idx ? cudaHostUnregister(c->h_idx_orig) : cudaFreeHost(c->h_idx_orig));
+  if (c->h_feats) (c->adopted_feats ? cudaHostUnregister(c->h_feats) : cudaFreeHost(c->h_feats));
   free(c->h_indptr);
   delete c;
 }
@@ -422,7 +423,8 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
                           const int32_t* indices, const float* feats, int32_t D, uint32_t flags) {
   if (!out) return fail(DCI_EINVAL, "out is null");
   *out = nullptr;
-  if (flags != 0) return fail(DCI_EINVAL, "flags must be 0");
+  if ((flags & ~(uint32_t)DCI_ADOPT_HOST) != 0) return fail(DCI_EINVAL, "unknown flags");
+  const bool adopt = (flags & DCI_ADOPT_HOST) != 0;
   if (N < 1 || N >= (1ll << 31)) return fail(DCI_EINVAL, "N must be in [1, 2^31)");
   if (E < 0 || E >= (1ll << 40)) return fail(DCI_EINVAL, "E must be in [0, 2^40)");
   if (D < 1) return fail(DCI_EINVAL, "D must be >= 1");
@@ -465,27 +467,46 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
     return bail(fail(DCI_ECUDA, "cudaStreamCreate(gather stream)"));
   memcpy(c->h_indptr, indptr, sizeof(int64_t) * (N + 1));
   cudaError_t e;
-  e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_idx_orig), sizeof(int32_t) * std::max<int64_t>(E, 1),
-                    cudaHostAllocMapped | cudaHostAllocPortable);
-  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(indices)"));
-  parallel_for(E, 1 << 24, [&](int64_t lo, int64_t hi) {
-    memcpy(c->h_idx_orig + lo, indices + lo, sizeof(int32_t) * (hi - lo));
-  });
-  c->h_idx_cur = c->h_idx_orig;
-  const size_t fbytes = sizeof(float) * (size_t)N * c->pitch;
-  e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_feats), fbytes, cudaHostAllocMapped | cudaHostAllocPortable);
-  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(feats)"));
   const int64_t pitch = c->pitch;
-  parallel_for(N, 1 << 16, [&](int64_t lo, int64_t hi) {
-    if (pitch == D) {
-      memcpy(c->h_feats + lo * pitch, feats + lo * D, sizeof(float) * D * (hi - lo));
-    } else {
-      for (int64_t v = lo; v < hi; ++v) {
-        memcpy(c->h_feats + v * pitch, feats + v * D, sizeof(float) * D);
-        memset(c->h_feats + v * pitch + D, 0, sizeof(float) * (pitch - D));
-      }
+  const size_t fbytes = sizeof(float) * (size_t)N * c->pitch;
+  if (adopt) {
+    // DCI_ADOPT_HOST: register the caller's buffers in place (pinned + mapped, portable), e.g. one
+    // node-shared POSIX shm segment that every rank's context adopts; the library never writes them
+    if (E > 0) {
+      e = cudaHostRegister(const_cast<int32_t*>(indices), sizeof(int32_t) * (size_t)E,
+                           cudaHostRegisterMapped | cudaHostRegisterPortable);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostRegister(indices)"));
+      c->h_idx_orig = const_cast<int32_t*>(indices);
+      c->adopted_idx = true;
     }
-  });
+    e = cudaHostRegister(const_cast<float*>(feats), fbytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostRegister(feats)"));
+    c->h_feats = const_cast<float*>(feats);
+    c->adopted_feats = true;
+  }
+  if (!c->adopted_idx) {
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_idx_orig), sizeof(int32_t) * std::max<int64_t>(E, 1),
+                      cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(indices)"));
+    parallel_for(E, 1 << 24, [&](int64_t lo, int64_t hi) {
+      memcpy(c->h_idx_orig + lo, indices + lo, sizeof(int32_t) * (hi - lo));
+    });
+  }
+  c->h_idx_cur = c->h_idx_orig;
+  if (!c->adopted_feats) {
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_feats), fbytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaHostAlloc(feats)"));
+    parallel_for(N, 1 << 16, [&](int64_t lo, int64_t hi) {
+      if (pitch == D) {
+        memcpy(c->h_feats + lo * pitch, feats + lo * D, sizeof(float) * D * (hi - lo));
+      } else {
+        for (int64_t v = lo; v < hi; ++v) {
+          memcpy(c->h_feats + v * pitch, feats + v * D, sizeof(float) * D);
+          memset(c->h_feats + v * pitch + D, 0, sizeof(float) * (pitch - D));
+        }
+      }
+    });
+  }
   void* dp = nullptr;
   if ((e = cudaHostGetDevicePointer(&dp, c->h_idx_orig, 0)) != cudaSuccess)
     return bail(cuda_fail(e, "cudaHostGetDevicePointer"));
@@ -1285,9 +1306,12 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   out->gather_launches = ws->acc_gather_launches;
   out->rows_read = h.acc_rows_read;
   out->gather_bytes = h.acc_gather_bytes;
+  out->host_rows_read = h.acc_host_rows;
+  out->host_adj_lines = h.acc_host_lines;
   if (reset) {
     h.acc_batches = h.acc_seeds = h.acc_rows = 0;
     h.acc_rows_read = h.acc_gather_bytes = 0;
+    h.acc_host_rows = h.acc_host_lines = 0;
     for (int c = 0; c < 4; ++c) h.acc_counters[c] = 0;
     DCI_CUDA(cudaMemcpy(ws->scal, &h, sizeof(h), cudaMemcpyHostToDevice));
     ws->acc_timed = ws->acc_gather_launches = 0;

@@ -52,6 +52,11 @@ struct BatchScalars {
   // its batches) and the gather's algorithmic bytes; launch_reads is the running
   // count of the current launch (group launches accumulate on their first batch's scalars)
   unsigned long long acc_rows_read, acc_gather_bytes, launch_reads;
+  // host-link traffic (bench roofline): 128-byte host lines read by adjacency misses (sampling
+  // kernels), feature rows read from pinned host memory (gathers); booked on a launch's first batch
+  unsigned long long acc_host_lines, acc_host_rows;
+  // node-sweep gather: next 32-node group to take (dynamic schedule; reset by the launch's last block)
+  unsigned long long sweep_ticket;
 };
 
 struct dci_ctx_impl;
@@ -69,6 +74,7 @@ struct dci_ctx {
   int32_t* h_idx_orig = nullptr;     // pinned+mapped, original CSC order
   int32_t* h_idx_cur = nullptr;      // pinned+mapped, current order (== orig before fill)
   float* h_feats = nullptr;          // pinned+mapped, [N][pitch]
+  bool adopted_idx = false, adopted_feats = false;  // DCI_ADOPT_HOST: caller memory registered in place
   // device aliases of the mapped host buffers (UVA)
   const int32_t* u_idx_cur = nullptr;
   const int32_t* u_idx_orig = nullptr;

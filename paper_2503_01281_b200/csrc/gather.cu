@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
     if (MODE != 0) {
       sc->acc_rows_read += rows;
       sc->acc_gather_bytes += rows * (8ull * (unsigned long long)a.D + 4ull);
+      sc->acc_host_rows += a.out_counters[3];  // every miss row is read from the host once
     }
     for (int c = 0; c < 4; ++c) sc->acc_counters[c] += a.out_counters[c];
     sc->status = 0;
@@ -306,9 +307,10 @@ struct TmaBatches {
 //  rows:  sum_b |F_L(b)| x (row read 4D + row write 4D + 4 B slot lookup)
 //  sweep: N x (8 B tag probe per batch + 4 B slot lookup) + |union| x 4D + sum_b |F_L(b)| x 4D
 __device__ __forceinline__ void group_epilogue(const TmaBatches& a, const unsigned (*s_cnt)[2], unsigned s_reads,
-                                               long long tot_rows, bool sweep) {
+                                               unsigned s_host_rows, long long tot_rows, bool sweep) {
   const int nb = a.n;
   if (threadIdx.x == 0 && s_reads) atomicAdd(&a.b[0].sc->launch_reads, (unsigned long long)s_reads);
+  if (threadIdx.x == 0 && s_host_rows) atomicAdd(&a.b[0].sc->acc_host_rows, (unsigned long long)s_host_rows);
   if (threadIdx.x < nb) {
     const int i = threadIdx.x;
     if (s_cnt[i][0]) atomicAdd(&a.b[i].sc->counters[2], (unsigned long long)s_cnt[i][0]);
@@ -331,6 +333,7 @@ __device__ __forceinline__ void group_epilogue(const TmaBatches& a, const unsign
     sc0->acc_gather_bytes += sweep ? (unsigned long long)a.N * (8ull * nb + 4ull) + reads * rowb + tot * rowb
                                    : tot * (2ull * rowb + 4ull);
     sc0->launch_reads = 0;
+    sc0->sweep_ticket = 0;
   }
   __syncthreads();
   if (s_last && threadIdx.x < nb) {
@@ -460,13 +463,14 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ uint32_t s_ep[kSweepMax];
   __shared__ unsigned s_cnt[kSweepMax][2];
-  __shared__ unsigned s_reads;
+  __shared__ unsigned s_reads, s_host;
   __shared__ long long s_tot;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nb = a.n;
   if (threadIdx.x < nb) s_ep[threadIdx.x] = __ldcg(&a.b[threadIdx.x].sc->hdr.epoch);
   if (threadIdx.x < 2 * kSweepMax) (&s_cnt[0][0])[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
     s_reads = 0u;
+    s_host = 0u;
     long long acc = 0;
     for (int i = 0; i < nb; ++i) acc += __ldcg(&a.b[i].sc->sizes[a.L]);
     s_tot = acc;
@@ -478,8 +482,15 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
   int* rt = sslot + 32;                                                     // [nb][32]
   const uint64_t pol = hint ? policy_evict_first() : policy_evict_normal();
   const int row16 = a.pitch >> 2;
-  const int64_t nw = (int64_t)gridDim.x * kSweepWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kSweepWarps + wib;
+  // dynamic schedule: a warp takes the next 32-node group from a ticket counter (in the first
+  // batch's scalars), so blocks that start late (SMs held by kernels running beside the gather)
+  // take fewer groups instead of running as a tail wave
+  unsigned long long* ticket = &a.b[0].sc->sweep_ticket;
+  auto take = [&]() -> int64_t {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1ull);
+    return 32 * (int64_t)__shfl_sync(0xffffffffu, t, 0);
+  };
   // probes of the group starting at node g: lane j copies node g + j's tag in every batch table
   // and its directory slot into the stage (zeros past N)
   auto prefetch = [&](int64_t g) {
@@ -490,11 +501,11 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
     for (int b = 0; b < nb; ++b) cp_async8(stag + b * 32 + lane, a.b[b].pos_of + vv, in ? 8 : 0);
     cp_async4(sslot + lane, &a.dir[vv].slot, in ? 4 : 0);
   };
-  unsigned reads = 0, hits = 0, misses = 0;  // lane b counts batch b's feature hits / misses
-  int64_t g = gw * 32;
+  unsigned reads = 0, host_reads = 0, hits = 0, misses = 0;  // lane b: batch b's feature hits / misses
+  int64_t g = take();
   prefetch(g);
   cp_async_commit();
-  for (; g < a.N; g += nw * 32) {
+  while (g < a.N) {
     cp_async_wait_all();
     __syncwarp();
     const int64_t v = g + lane;
@@ -508,7 +519,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
       }
     }
     __syncwarp();  // the stage is consumed: the next group's probes may overwrite it
-    prefetch(g + nw * 32);
+    const int64_t g_next = take();
+    prefetch(g_next);
     cp_async_commit();
     const char* src = nullptr;
     if (mask) {
@@ -531,6 +543,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
     }
     unsigned m = __ballot_sync(0xffffffffu, mask != 0);
     reads += __popc(m);
+    host_reads += __popc(m & ~hitm);
     while (m) {
       const int j1 = __ffs(m) - 1;
       m &= m - 1;
@@ -544,6 +557,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
       sweep_copy<VPL>(a, rt, row16, s1, m1, j1, two ? s2 : nullptr, two ? m2 : 0u, j2, lane, out16max, pol);
     }
     __syncwarp();  // every lane is done with the row table before the next group rewrites it
+    g = g_next;
   }
   cp_async_wait_all();
   if (lane < nb) {
@@ -551,8 +565,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
     if (misses) atomicAdd(&s_cnt[lane][1], misses);
   }
   if (lane == 0 && reads) atomicAdd(&s_reads, reads);
+  if (lane == 0 && host_reads) atomicAdd(&s_host, host_reads);
   __syncthreads();
-  group_epilogue(a, s_cnt, s_reads, s_tot, true);
+  group_epilogue(a, s_cnt, s_reads, s_host, s_tot, true);
 }
 
 __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_constant__ TmaBatches a, TmaArgs t) {
@@ -698,7 +713,9 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
   }
   bulk_wait_all();
   __syncthreads();
-  group_epilogue(a, s_cnt, s_reads, s_pre[nb], false);
+  unsigned host_rows = 0;  // row mode reads every miss row once per batch
+  for (int i = 0; i < nb; ++i) host_rows += s_cnt[i][1];
+  group_epilogue(a, s_cnt, s_reads, host_rows, s_pre[nb], false);
 }
 
 int env_int(const char* name, int dflt) {
@@ -854,7 +871,10 @@ static dci_status sweep_launch_v(dci_ctx* ctx, const TmaBatches& tb, int32_t out
   DCI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kSweepWarps, smem));
   static const int cap = env_int("DCI_SWEEP_BPS", 0);
   const int bps = std::max(1, cap > 0 ? std::min(cap, occ) : occ);
-  k_gather_sweep<VPL><<<ctx->num_sms * bps, 32 * kSweepWarps, smem, s>>>(tb, out16max, hint);
+  // DCI_SWEEP_SMS: SMs' worth of blocks (default all; leaves the rest to sampling running beside it)
+  static const int sms = env_int("DCI_SWEEP_SMS", 0);
+  const int nsm = (sms > 0 && sms < ctx->num_sms) ? sms : ctx->num_sms;
+  k_gather_sweep<VPL><<<nsm * bps, 32 * kSweepWarps, smem, s>>>(tb, out16max, hint);
   ++ctx->launches;
   return DCI_OK;
 }

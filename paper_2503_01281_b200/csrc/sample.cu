@@ -106,6 +106,7 @@ struct HopShared {
   unsigned long long seed[DCI_MAX_GROUP];
   const int32_t* Fin[DCI_MAX_GROUP];
   unsigned cnt[DCI_MAX_GROUP][2];     // adjacency hits / misses of this block, per batch
+  unsigned host_lines;                // distinct 128-byte host lines its adjacency misses read
   int all_ok;                         // no batch has a seed error (status set by hop 0)
 };
 
@@ -135,7 +136,21 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
     S.all_ok = ok;
   }
   if (threadIdx.x < 2 * DCI_MAX_GROUP) (&S.cnt[0][0])[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) S.host_lines = 0u;
   __syncthreads();
+}
+
+// Host-link requests of the adjacency miss path (bench roofline): a sampled element
+// that misses is a 4-byte zero-copy read of pinned host memory; misses of one (dst, hop) that fall
+// in the same 128-byte line are served together.  Ranks are sorted within a G-lane group, so the
+// misses are its last lanes in address order: a miss lane opens a new line unless the lane before
+// it missed in the same line.  Returns the lines the warp's groups open (warp-uniform).
+template <int G>
+__device__ __forceinline__ unsigned host_lines_opened(bool miss, int64_t elem, int gl) {
+  const long long line = elem >> 5;  // 32 int32 per 128-byte line
+  const long long pl = __shfl_up_sync(0xffffffffu, line, 1, G);
+  const bool pmiss = __shfl_up_sync(0xffffffffu, (int)miss, 1, G) != 0;
+  return __popc(__ballot_sync(0xffffffffu, miss && (gl == 0 || !pmiss || pl != line)));
 }
 
 // batch of item q in a prefix table (n <= 16: a short linear scan over shared memory)
@@ -152,6 +167,7 @@ __device__ __forceinline__ void hop_shared_flush(const HopLaunch& a, HopShared& 
     if (S.cnt[threadIdx.x][0]) atomicAdd(&sc->counters[0], (unsigned long long)S.cnt[threadIdx.x][0]);
     if (S.cnt[threadIdx.x][1]) atomicAdd(&sc->counters[1], (unsigned long long)S.cnt[threadIdx.x][1]);
   }
+  if (threadIdx.x == 0 && S.host_lines) atomicAdd(&a.b[0].sc->acc_host_lines, (unsigned long long)S.host_lines);
 }
 
 // Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
@@ -348,6 +364,10 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       hit = rank < cached_len;
       x = hit ? ld_keep_i32(a.acache + cache_off + rank, epol) : ld_host_i32(a.uidx + host_off + rank);
     }
+    {  // read once for every batch holding v: its host lines count once
+      const unsigned nl = host_lines_opened<G>(valid && !hit, host_off + rank, gl);
+      if (lane == 0 && nl) atomicAdd(&S.host_lines, nl);
+    }
     // write the sample into every batch holding v (local id shuffled from the probing lane)
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
@@ -466,6 +486,10 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     const int32_t rank = select_rank<G>(gl, lane, gmask, f, deg, floyd, S.seed[b], a.pass, (uint32_t)h, (uint32_t)v);
     const int pos = gl;
     const bool valid = active && gl < k;
+    {
+      const unsigned nl = host_lines_opened<G>(valid && rank >= cached_len, host_off + rank, gl);
+      if (lane == 0 && nl) atomicAdd(&S.host_lines, nl);
+    }
     int32_t x = -1;
     if (valid) {
       const bool hit = rank < cached_len;
@@ -574,8 +598,28 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
         }
       }
     }
-    // element reads in sorted-rank order: pos -> rank
-    for (int pos = lane; pos < f; pos += 32) {
+    // element reads in sorted-rank order: pos -> rank (all lanes run every pass: the host-line
+    // count shuffles across the warp, carrying the previous pass's last miss line)
+    long long carry_line = -1;
+    for (int base = 0; base < f; base += 32) {
+      const int pos = base + lane;
+      {
+        const int32_t rk = pos < k ? (deg > f ? chosen[pos] : pos) : 0;
+        const bool miss = pos < k && rk >= cached_len;
+        const long long line = (host_off + rk) >> 5;
+        long long pl = __shfl_up_sync(0xffffffffu, line, 1);
+        bool pmiss = __shfl_up_sync(0xffffffffu, (int)miss, 1) != 0;
+        if (lane == 0) {
+          pl = carry_line;
+          pmiss = carry_line >= 0;
+        }
+        const unsigned opened = __ballot_sync(0xffffffffu, miss && (!pmiss || pl != line));
+        const unsigned missm = __ballot_sync(0xffffffffu, miss);
+        const long long last = __shfl_sync(0xffffffffu, line, 31);
+        carry_line = (missm >> 31) & 1u ? last : -1;
+        if (lane == 0 && opened) atomicAdd(&S.host_lines, (unsigned)__popc(opened));
+      }
+      if (pos >= f) continue;
       int32_t x = -1;
       if (pos < k) {
         const int32_t rank = deg > f ? chosen[pos] : pos;
@@ -851,13 +895,14 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
 
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
   const HopLaunch a = hop_launch(ctx, ws, p, n);
-  // resident blocks per SM of the sampling grids: 8 (the whole GPU); 2 when a group's sampling
-  // overlaps the previous group's gather (DCI_PHASED=0; measured)
+  // resident blocks per SM of the sampling grids: 8 (the whole GPU).  (Round 1 used 2 when a group's
+  // sampling overlapped the previous group's 1-block-per-SM gather; the round-2 node-sweep gather
+  // fills the SMs itself, and 8 measured best both alone and overlapped: DESIGN.md §9.)
   static const int forced = [] {
     const char* e = getenv("DCI_SAMPLE_BPS");
     return e ? atoi(e) : 0;
   }();
-  const int bps = forced > 0 ? forced : (ws[0]->in_group && !group_phased() ? 2 : 8);
+  const int bps = forced > 0 ? forced : 8;
   // Grid: persistent (SM count x resident blocks), but no larger than the worst-case frontier of
   // this hop needs (small frontiers would otherwise start hundreds of idle blocks); the fused
   // relabel of hop h-1 (|F_{h-1}| * f_{h-1} items) is covered by the grid-stride loops either way.

@@ -105,6 +105,100 @@ def gather_clocks(local: dict, group=None) -> dict:
             "samples": sum(c.get("samples", 0) for c in allc), "per_rank": allc}
 
 
+def _shm_tag() -> str:
+    """A name shared by the ranks of one launch on this node (torchrun's run id / master port)."""
+    run = os.environ.get("TORCHELASTIC_RUN_ID") or os.environ.get("DCI_SHM_TAG") or "x"
+    return f"{run}_{os.environ.get('MASTER_PORT', '0')}".replace("/", "_")[:40]
+
+
+class SharedGraph:
+    """One host copy of a graph per node (DCI_ADOPT_HOST, round-1 VERDICT missing #2): the node's
+    local rank 0 generates indptr / indices / pitch-padded features into POSIX shared-memory
+    segments, every local rank maps them, and each rank's context registers them in place
+    (dci.load_graph(..., adopt=True)), so an 8-GPU papers100M-shaped run pins one 63 GB graph,
+    not eight.  The segments are unlinked once every rank has mapped them (the memory lives until
+    the last mapping goes).  Keep this object alive as long as the contexts."""
+
+    def __init__(self, N: int, E: int, D: int, generate, group=None, tag: str | None = None):
+        """generate() -> (indptr int64[N+1], indices int32[E], feats fp32[N, D]) as numpy or torch
+        (CPU or CUDA) arrays; called on local rank 0 only."""
+        from multiprocessing import shared_memory
+        import torch
+        import torch.distributed as dist
+        self.N, self.E, self.D = N, E, D
+        pitch = (D + 3) // 4 * 4
+        rank, world, local = dist_env()
+        dist_on = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        tag = tag or _shm_tag()
+        names = [f"dci_{tag}_{k}" for k in ("indptr", "indices", "feats")]
+        sizes = [8 * (N + 1), max(4 * E, 4), 4 * N * pitch]
+        self._shm = []
+        if local == 0:
+            for nm, sz in zip(names, sizes):
+                try:
+                    old = shared_memory.SharedMemory(name=nm)
+                    old.close()
+                    old.unlink()
+                except FileNotFoundError:
+                    pass
+                self._shm.append(shared_memory.SharedMemory(name=nm, create=True, size=sz))
+            ip, ix, ft = generate()
+            self._views()
+            _copy_into(self.indptr, ip)
+            _copy_into(self.indices[:E], ix)
+            fv = torch.from_numpy(self.feats)
+            fv[:, :D].copy_(torch.as_tensor(ft).reshape(N, D))
+            if pitch > D:
+                fv[:, D:].zero_()
+            del ip, ix, ft
+        if dist_on:
+            dist.barrier(group=group)
+        if local != 0:
+            self._shm = [shared_memory.SharedMemory(name=nm) for nm in names]
+            self._views()
+        if dist_on:
+            dist.barrier(group=group)
+        if local == 0:
+            for sm in self._shm:
+                sm.unlink()  # every rank has it mapped; the memory goes with the last mapping
+        self.names = names
+
+    def _views(self):
+        N, E, D = self.N, self.E, self.D
+        pitch = (D + 3) // 4 * 4
+        self.indptr = np.ndarray((N + 1,), np.int64, buffer=self._shm[0].buf)
+        self.indices = np.ndarray((max(E, 1),), np.int32, buffer=self._shm[1].buf)
+        self.feats = np.ndarray((N, pitch), np.float32, buffer=self._shm[2].buf)
+
+    @staticmethod
+    def fits(N: int, E: int, D: int) -> bool:
+        """Whether /dev/shm can hold the graph (containers often cap it)."""
+        import shutil
+        need = 8 * (N + 1) + 4 * E + 4 * N * ((D + 3) // 4 * 4)
+        try:
+            return shutil.disk_usage("/dev/shm").free > need * 1.05
+        except OSError:
+            return False
+
+    def load(self, device: int):
+        """This rank's context over the node-shared graph (registered in place, no copy)."""
+        import paper_2503_01281_b200 as dci
+        return dci.load_graph(self.indptr, self.indices[: self.E], self.feats, device=device, adopt=True, D=self.D)
+
+    def close(self):
+        for sm in self._shm:
+            try:
+                sm.close()
+            except BufferError:
+                pass  # a view is still alive; the mapping goes with the process
+        self._shm = []
+
+
+def _copy_into(dst: np.ndarray, src):
+    import torch
+    torch.from_numpy(dst).copy_(torch.as_tensor(src).reshape(dst.shape))
+
+
 def _ndev():
     import torch
     return torch.cuda.device_count()

@@ -95,3 +95,53 @@ def test_cap_split_to_data():
     assert parallel.cap_split_to_data(10, 20, 1000, 1000) == (10, 20)  # nothing to move
     a, f = parallel.cap_split_to_data(1_159_508_631, 14_671_851_609, 4 * 1_615_685_872, 512 * 111_059_956, 8)
     assert a == 4 * 1_615_685_872 and a + f == 1_159_508_631 + 14_671_851_609 and f * 8 >= 512 * 111_059_956
+
+
+def _shm_worker(rank, world, port, q, tag):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    try:
+        import synth
+        parallel.init("gloo")
+        N, E, D = 1200, 9000, 13
+        calls = []
+
+        def gen():
+            calls.append(rank)
+            ip, ix = synth.rmat_csc(N, E, seed=9)
+            return ip, ix, synth.features(N, D)
+
+        g = parallel.SharedGraph(N, E, D, gen, tag=tag)
+        ip, ix = synth.rmat_csc(N, E, seed=9)
+        ft = synth.features(N, D).numpy()
+        ok = (np.array_equal(g.indptr, ip.numpy()) and np.array_equal(g.indices[:E], ix.numpy())
+              and np.array_equal(g.feats[:, :D], ft) and not g.feats[:, D:].any())
+        q.put((rank, bool(ok), calls, g.feats.shape, g.names[2]))
+        dist.barrier()
+        g.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+        raise
+
+
+def test_shared_graph_generated_once_per_node():
+    """parallel.SharedGraph (DCI_ADOPT_HOST's host side): local rank 0 alone generates the graph
+    into shm segments; rank 1 maps the same bytes; features are pitch-padded with zeros."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    tag = f"test{port}"
+    procs = [ctx.Process(target=_shm_worker, args=(r, 2, port, q, tag)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert len(r) == 5, r
+    (_, ok0, calls0, shape0, name0), (_, ok1, calls1, shape1, name1) = res
+    assert ok0 and ok1
+    assert calls0 == [0] and calls1 == []  # generated once, by local rank 0
+    assert shape0 == shape1 == (1200, 16) and name0 == name1
+    assert not os.path.exists("/dev/shm/" + name0)  # unlinked once both ranks mapped it
