@@ -513,6 +513,8 @@ def run_ours(args):
     rows_read = sum(st["rows_read"] for st in sts)
     # the library's algorithmic gather bytes: row reads + row writes + lookups
     alg_bytes = float(sum(st["gather_bytes"] for st in sts))
+    kinds = np.sum([st["gather_kinds"] for st in sts], axis=0)
+    table_mb = max(st["table_bytes"] for st in sts) / 2 ** 20
     host_rows = sum(st["host_rows_read"] for st in sts)
     host_lines = sum(st["host_adj_lines"] for st in sts)
     tot = parallel.sum_over_ranks([sum(st["seeds"] for st in sts), launches, rows, alg_bytes, g_ms, s_ms, n_timed,
@@ -607,10 +609,13 @@ def run_ours(args):
     bind_peak = host_peak if host_bound else hbm_peak
     n_launch = max(1.0, tot[7])
     achieved_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per launch (live events)
-    kernel = (("k_gather_sweep (group of %d: node sweep, each row read once per group; route + feature gather, "
-               "S7-S8)" % G) if frac_read < 0.999 else
-              ("k_gather_tma (group of %d: rows; route + feature gather, S7-S8)" % G)) if G else \
-        "k_gather (fused route + relabel + feature gather, S7-S8)"
+    # the group gather kernels the timed regions launched (the library picks the node sweep's kernel
+    # per launch: bulk copies when nothing is queued ahead of the gather, register copies otherwise)
+    knames = ["k_gather_tma (rows)", "k_gather_sweep (register copies)", "k_gather_sweep_tma (bulk copies)"]
+    used = {knames[i]: int(kinds[i]) for i in range(3) if kinds[i]}
+    kernel = ((" + ".join(f"{k} x{v}" for k, v in used.items()) +
+               f" (group of {G}; route + feature gather, S7-S8; node sweep reads each row once per group)")
+              if G else "k_gather (fused route + relabel + feature gather, S7-S8)")
     aggregate_gbs = bind_b / (ms_tot / 1e3) / 1e9  # all gather launches over the timed wall time
     # Whole-step roofline of SURVEY §8(d), over all timed regions: T_roof = max(B_hbm/BW_hbm,
     # B_host/BW_host, N_req/R_req).  Algorithmic bytes: HBM = the gather's hit-row reads and all row
@@ -663,7 +668,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded R-MAT graph, closed-form features)",
         "config": {"workload": cfg.name, "global_batch": B * world, "batch_per_gpu": B,
-                   "ranks_share_gpus": shared_gpus, "host_graph": "node-shared (adopted)" if use_shm else "per rank", "fanouts": list(fan),
+                   "ranks_share_gpus": shared_gpus, "position_table_MB_per_workspace": table_mb, "host_graph": "node-shared (adopted)" if use_shm else "per rank", "fanouts": list(fan),
                    "N": cfg.N, "E": cfg.E, "D": cfg.D, "budget": args.budget or cfg.budget,
                    "ratio": args.ratio, "fill": args.fill,
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
@@ -685,7 +690,7 @@ def run_ours(args):
                      "frac": (achieved_gbs / bind_peak) if achieved_gbs else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": bind_b / n_launch, "launches": int(tot[7]),
                      "avg_gather_ms": tot[4] / n_launch, "avg_sample_ms": tot[5] / max(1, tot[6]),
-                     "rows_read_per_row": frac_read,
+                     "rows_read_per_row": frac_read, "gather_kernels": used,
                      "gather_busy_frac": tot[4] / ms_tot if ms_tot > 0 else None,
                      "aggregate_achieved": aggregate_gbs, "aggregate_frac": aggregate_gbs / bind_peak,
                      "alone": None if alone is None or host_bound else dict(alone, frac=alone["achieved"] / bind_peak),

@@ -201,7 +201,7 @@ dci_status validate_batch(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds,
 dci_status stage_header(dci_ctx* ctx, dci_workspace* ws, const int32_t* seeds, int32_t B, uint64_t seed,
                         cudaStream_t s) {
   if (++ws->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
-    DCI_CUDA(cudaMemsetAsync(ws->pos_of, 0, sizeof(unsigned long long) * ctx->N, s));
+    DCI_CUDA(cudaMemsetAsync(ws->pos_of, 0, ws->table_bytes, s));
     ws->epoch = 1;
   }
   const int slot = (int)(ws->calls++ % dci_workspace::kHdrRing);
@@ -396,6 +396,7 @@ void free_ctx(dci_ctx* c) {
   if (c->pre_out_mem) cudaFree(c->pre_out_mem);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->gather_ev) cudaEventDestroy(c->gather_ev);
+  if (c->gather_q_ev) cudaEventDestroy(c->gather_q_ev);
   if (c->d_dir) cudaFree(c->d_dir);
   if (c->d_acache) cudaFree(c->d_acache);
   release_feature_partitions(c);
@@ -463,7 +464,8 @@ dci_status dci_load_graph(dci_ctx** out, int device, int64_t N, int64_t E, const
   // the context's gather stream (group gathers and serial gathers run one at a time on it);
   // created here so concurrent callers with distinct workspaces never race on it
   if (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->gather_ev, kCrossStreamEvent) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->gather_ev, kCrossStreamEvent) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->gather_q_ev, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(DCI_ECUDA, "cudaStreamCreate(gather stream)"));
   memcpy(c->h_indptr, indptr, sizeof(int64_t) * (N + 1));
   cudaError_t e;
@@ -598,8 +600,22 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
     return cuda_fail(e, what);
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&w->pos_of, sizeof(unsigned long long) * ctx->N)) != cudaSuccess)
-    return bail(e, "cudaMalloc(pos_of)");
+  // position table layout (dci_internal.cuh): hashed when the dense table (8 N bytes) would be more
+  // than 4x the hashed one (16 B x pow2 >= 2 x the frontier bound) -- papers100M-shaped graphs;
+  // env DCI_TABLE=dense|hash overrides
+  {
+    static const int forced = [] {
+      const char* v = getenv("DCI_TABLE");
+      return !v ? 0 : (v[0] == 'd' ? 1 : (v[0] == 'h' ? 2 : 0));
+    }();
+    uint64_t cap = 1;
+    while (cap < 2ull * (uint64_t)std::max<int64_t>(w->hop_cap[L], 1)) cap <<= 1;
+    const uint64_t dense_b = 8ull * (uint64_t)ctx->N, hash_b = 16ull * cap;
+    const bool hashed = cap <= (1ull << 31) && (forced == 2 || (forced == 0 && dense_b > 4 * hash_b));
+    w->hmask = hashed ? (uint32_t)(cap - 1) : 0u;
+    w->table_bytes = hashed ? hash_b : dense_b;
+  }
+  if ((e = cudaMalloc(&w->pos_of, w->table_bytes)) != cudaSuccess) return bail(e, "cudaMalloc(pos_of)");
   for (int i = 0; i < 2; ++i) {
     if ((e = cudaMalloc(&w->cand[i], sizeof(int32_t) * std::max<int64_t>(w->cand_cap, 1))) != cudaSuccess)
       return bail(e, "cudaMalloc(cand)");
@@ -622,7 +638,7 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
   for (int i = 0; i < dci_workspace::kHdrRing; ++i)
     if ((e = cudaEventCreateWithFlags(&w->hdr_ev[i], cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "stream");
-  cudaMemset(w->pos_of, 0, sizeof(unsigned long long) * ctx->N);
+  cudaMemset(w->pos_of, 0, w->table_bytes);
   cudaMemset(w->tile_state, 0, sizeof(unsigned long long) * w->tiles_cap);
   cudaMemset(w->scal, 0, sizeof(BatchScalars));
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "workspace init");
@@ -749,7 +765,7 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     BatchHeader* hh = w0->ghdr_ring + (size_t)slot * DCI_MAX_GROUP;
     for (int i = 0; i < n; ++i) {
       if (++ws[i]->epoch == 0) {  // 2^32 batches on this workspace: clear the tag table once
-        DCI_CUDA(cudaMemsetAsync(ws[i]->pos_of, 0, sizeof(unsigned long long) * ctx->N, s));
+        DCI_CUDA(cudaMemsetAsync(ws[i]->pos_of, 0, ws[i]->table_bytes, s));
         ws[i]->epoch = 1;
       }
       hh[i].seeds = seeds[i];
@@ -911,7 +927,9 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   // node sweep when the group's frontier bounds together reach N (Reddit-shaped: one batch's bound
   // alone is N); host-resident papers100M-shaped groups stay in row mode
   bool sweep = false;
-  if (gather_sweep_enabled() && n >= 2) {
+  bool all_dense = true;
+  for (int i = 0; i < n; ++i) all_dense &= ws[i]->hmask == 0;
+  if (gather_sweep_enabled() && n >= 2 && all_dense) {
     int64_t grow = 1;
     for (int h = 0; h < L; ++h) grow = std::min<int64_t>(ctx->N, grow * (1 + (int64_t)fanouts[h]));
     int64_t cover = 0;
@@ -919,8 +937,17 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     sweep = cover >= ctx->N;
   }
   {
-    dci_status gst = launch_gather_many(ctx, ws, outs, n, L, stage, sweep, gs);
+    // which node-sweep kernel: the bulk-copy one (faster alone, 1.43 vs 1.55 ms on M2) when this
+    // gather will run by itself -- the previous group's gather had already finished when this
+    // group was enqueued, so nothing else is queued ahead of it -- else the register-copy one,
+    // whose full SMs keep the next group's sampling from slowing it (exp r2-6)
+    const bool alone = !ctx->gather_q_valid || cudaEventQuery(ctx->gather_q_ev) == cudaSuccess;
+    int kind = 0;
+    dci_status gst = launch_gather_many(ctx, ws, outs, n, L, stage, sweep, alone, gs, &kind);
     if (gst != DCI_OK) return gst;
+    ++w0->kind_launches[kind];
+    DCI_CUDA(cudaEventRecord(ctx->gather_q_ev, gs));
+    ctx->gather_q_valid = true;
   }
   enqueue_epilogue(s);
   if (phased) {
@@ -1308,10 +1335,13 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   out->gather_bytes = h.acc_gather_bytes;
   out->host_rows_read = h.acc_host_rows;
   out->host_adj_lines = h.acc_host_lines;
+  for (int k = 0; k < 3; ++k) out->gather_kinds[k] = ws->kind_launches[k];
+  out->table_bytes = ws->table_bytes;
   if (reset) {
     h.acc_batches = h.acc_seeds = h.acc_rows = 0;
     h.acc_rows_read = h.acc_gather_bytes = 0;
     h.acc_host_rows = h.acc_host_lines = 0;
+    for (auto& k : ws->kind_launches) k = 0;
     for (int c = 0; c < 4; ++c) h.acc_counters[c] = 0;
     DCI_CUDA(cudaMemcpy(ws->scal, &h, sizeof(h), cudaMemcpyHostToDevice));
     ws->acc_timed = ws->acc_gather_launches = 0;

@@ -28,6 +28,66 @@ static_assert(sizeof(DirEntry) == 32, "directory entry must be one 32-byte secto
 
 constexpr int kScanTile = 256;             // dst nodes per tile of the per-hop scan
 
+// ---- node -> position tag table of a batch (S6 dedup + relabel) ----
+// A tag is epoch << 32 | ~position: the batch's epoch marks it current, so the table is never
+// cleared between batches, and atomicMax keeps the first occurrence (smallest position).
+//  dense  (hmask == 0): tag[v] at pos_of + v, N entries (8 N bytes) -- small graphs, and the only
+//         layout the node-sweep modes (probe every node id in every batch) can use
+//  hashed (hmask = capacity - 1): open addressing with linear probing over 16-byte entries
+//         {key word = epoch << 32 | v, tag}, capacity = pow2 >= 2 x the workspace's frontier bound,
+//         so a batch's distinct nodes fill it at most half; an entry whose key word carries an older
+//         epoch is free for this batch (claimed with atomicCAS).  Papers100M-shaped: 64 MB instead of
+//         888 MB per workspace, L2-resident instead of DRAM (round-1 VERDICT missing #3)
+__device__ __forceinline__ uint32_t pt_hash(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+// the tag word of node x in this batch, claiming an entry for it if needed (hashed)
+__device__ __forceinline__ unsigned long long* pt_insert(unsigned long long* t, uint32_t hmask, int32_t x,
+                                                         uint32_t epoch) {
+  if (!hmask) return t + x;
+  const unsigned long long want = ((unsigned long long)epoch << 32) | (uint32_t)x;
+  uint32_t h = pt_hash((uint32_t)x) & hmask;
+  for (;;) {
+    unsigned long long* e = t + 2ull * h;
+    unsigned long long kw = __ldcg(e);
+    if (kw == want) return e + 1;
+    if ((uint32_t)(kw >> 32) != epoch) {
+      const unsigned long long old = atomicCAS(e, kw, want);
+      if (old == kw || old == want) return e + 1;
+      if ((uint32_t)(old >> 32) != epoch) continue;  // changed under us by an older-epoch writer: retry
+    }
+    h = (h + 1) & hmask;
+  }
+}
+
+// the tag word of node x in this batch, or null if x was never inserted (hashed)
+__device__ __forceinline__ unsigned long long* pt_find(unsigned long long* t, uint32_t hmask, int32_t x,
+                                                       uint32_t epoch) {
+  if (!hmask) return t + x;
+  const unsigned long long want = ((unsigned long long)epoch << 32) | (uint32_t)x;
+  uint32_t h = pt_hash((uint32_t)x) & hmask;
+  for (;;) {
+    unsigned long long* e = t + 2ull * h;
+    const unsigned long long kw = __ldcg(e);
+    if (kw == want) return e + 1;
+    if ((uint32_t)(kw >> 32) != epoch) return nullptr;
+    h = (h + 1) & hmask;
+  }
+}
+
+// tag of node x in this batch (0 = absent)
+__device__ __forceinline__ unsigned long long pt_tag(unsigned long long* t, uint32_t hmask, int32_t x,
+                                                     uint32_t epoch) {
+  const unsigned long long* p = pt_find(t, hmask, x, epoch);
+  return p ? __ldcg(p) : 0ull;
+}
+
 // Per-batch values that change every call; written by one host->device copy before the
 // batch's kernels (or CUDA graph) run, so a captured graph never needs re-capturing for them.
 struct BatchHeader {
@@ -104,6 +164,9 @@ struct dci_ctx {
   cudaStream_t gstream = nullptr;  // shared gather stream (serial-gather mode)
   cudaEvent_t gather_ev = nullptr;  // end of the last group gather (DCI_PHASED experiments)
   bool gather_ev_valid = false;
+  // end of the last group gather, only queried by the host (picks the node-sweep kernel)
+  cudaEvent_t gather_q_ev = nullptr;
+  bool gather_q_valid = false;
   // live user workspaces (= batches the caller keeps in flight); shared with the workspaces so
   // either may be destroyed first
   std::shared_ptr<std::atomic<int>> live_ws = std::make_shared<std::atomic<int>>(0);
@@ -129,9 +192,12 @@ struct dci_workspace {
   int64_t tiles_cap = 0;    // sum over hops of ceil(hop_cap[h] / kScanTile)
   int64_t tile_off[DCI_MAX_LAYERS + 1] = {0};
   // device buffers
-  // [N] node -> position tag of the current batch: epoch << 32 | ~position (entries with an
-  // older epoch read as absent, so the table is never cleared between batches)
+  // node -> position tag of the current batch: epoch << 32 | ~position (entries with an
+  // older epoch read as absent, so the table is never cleared between batches).  Dense [N]
+  // (hmask 0) or hashed [2 x (hmask + 1)] (see pt_insert)
   unsigned long long* pos_of = nullptr;
+  uint32_t hmask = 0;
+  size_t table_bytes = 0;
   uint32_t epoch = 0;
   int32_t* cand[2] = {nullptr, nullptr};  // ping-pong [cand_cap] padded candidates
   int32_t* kcnt[2] = {nullptr, nullptr};  // ping-pong [max hop_cap] samples per dst
@@ -191,6 +257,9 @@ struct dci_workspace {
   int32_t* gseeds_dev = nullptr;
   int64_t gseeds_cap = 0;
   cudaEvent_t gseeds_ev = nullptr;
+  // group gather launches by kernel (this workspace first in the group): row mode, register-copy
+  // node sweep, bulk-copy node sweep (dci_ws_stats.gather_kinds)
+  uint64_t kind_launches[3] = {0, 0, 0};
   // host-side running totals of the event-timed stages (profiling on)
   uint64_t acc_timed = 0, acc_gather_launches = 0;
   double acc_sample_ms = 0.0, acc_gather_ms = 0.0;
@@ -260,8 +329,11 @@ bool gather_uses_tma(const dci_ctx* ctx, const dci_batch_out* out);
 bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t n);
 // sweep: the group's frontiers may together cover the node set (sum of their bounds >= N), so the
 // node-sweep gather (each feature row read once for all batches) is used; else row mode.
+// alone: nothing is queued ahead of this gather (the bulk-copy sweep is then used, DCI_SWEEP_KIND=auto)
+// *kind: 0 row mode, 1 register-copy node sweep, 2 bulk-copy node sweep (the kernel launched)
 dci_status launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n,
-                              int32_t L, dci_batch_result* stage, bool sweep, cudaStream_t s);
+                              int32_t L, dci_batch_result* stage, bool sweep, bool alone, cudaStream_t s,
+                              int* kind);
 bool gather_sweep_enabled();  // env DCI_SWEEP (default 1)
 // Gather blocks per SM: the HBM-bound gather is given a small share of each SM when many
 // batches are in flight (their sampling kernels must co-reside), the whole SM when one is.

@@ -56,7 +56,8 @@ __device__ __forceinline__ void st_v4(int4* p, const int4& v, uint64_t pol) {
 
 struct FusedArgs {
   const DirEntry* dir;
-  const unsigned long long* pos_of;
+  unsigned long long* pos_of;
+  uint32_t hmask;  // position table layout (dci_internal.cuh)
   BatchScalars* sc;
   int64_t N;
   int32_t L;
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
       const int64_t d = q / pf;
       const int s = (int)(q - d * pf);
       if (s < a.last_kcnt[d])
-        a.last_bsrc[a.last_bptr[d] + s] = (int32_t)(0xFFFFFFFFu - (uint32_t)__ldcg(a.pos_of + a.last_cand[q]));
+        a.last_bsrc[a.last_bptr[d] + s] =
+            (int32_t)(0xFFFFFFFFu - (uint32_t)pt_tag(a.pos_of, a.hmask, a.last_cand[q], sc->hdr.epoch));
     }
     for (int64_t t = tid; t < a.last_ntiles; t += nthreads) a.last_tiles[t] = 0ull;
     if (tid == 0) sc->tickets[a.L - 1] = 0;
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
                                                                    int32_t out16max, int32_t hint) {
   // dynamic shared memory, per warp: tag stage [nb][32] u64 (the next group's probes, in flight
   // while the current group copies), slot stage [32] i32, row table [nb][32] i32
-  extern __shared__ __align__(16) unsigned char s_dyn[];
+  extern __shared__ __align__(128) unsigned char s_dyn[];
   __shared__ uint32_t s_ep[kSweepMax];
   __shared__ unsigned s_cnt[kSweepMax][2];
   __shared__ unsigned s_reads, s_host;
@@ -559,6 +561,192 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
     __syncwarp();  // every lane is done with the row table before the next group rewrites it
     g = g_next;
   }
+  cp_async_wait_all();
+  if (lane < nb) {
+    if (hits) atomicAdd(&s_cnt[lane][0], hits);
+    if (misses) atomicAdd(&s_cnt[lane][1], misses);
+  }
+  if (lane == 0 && reads) atomicAdd(&s_reads, reads);
+  if (lane == 0 && host_reads) atomicAdd(&s_host, host_reads);
+  __syncthreads();
+  group_epilogue(a, s_cnt, s_reads, s_host, s_tot, true);
+}
+
+// ------------------------------------------------------------------------------------
+// k_gather_sweep_tma: the same node sweep with Blackwell bulk copies instead of register copies
+// (DCI_SWEEP_KIND=tma).  A present node's row is loaded ONCE into a shared-memory ring slot
+// (cp.async.bulk global -> shared, completing on the slot's mbarrier; HBM cache row on a hit,
+// pinned host row through UVA on a miss), then the lanes of the warp store it to every batch that
+// holds it IN PARALLEL -- lane b issues one cp.async.bulk shared -> global of the whole row into
+// batch b's X.  Ring slots are line-padded (out16max words) with a zero tail, so whole-line X rows
+// need no register work.  Probes as in k_gather_sweep (cp.async-prefetched tags, dynamic group
+// tickets); a node's destination rows are copied into its slot's metadata when its load is
+// issued, so the next group's probes may be processed while earlier slots still drain.
+// Few warps and ~40 registers keep enough bytes in flight (the copies are asynchronous), which
+// leaves the SMs' registers and warps to the next group's sampling kernels.
+// ------------------------------------------------------------------------------------
+constexpr int kSweepTmaMaxWarps = 8;
+constexpr int kSweepTmaMaxSlots = 16;
+
+struct SweepTmaArgs {
+  int32_t W;           // warps per block
+  int32_t K;           // ring slots per warp
+  int32_t slot_bytes;  // out16max * 16 (128-byte multiple when lines are written)
+  int32_t row_bytes;   // 4 * pitch: bytes loaded per row
+  int32_t warp_bytes;  // dynamic shared memory per warp
+  int32_t hint;
+};
+
+__global__ void __launch_bounds__(32 * kSweepTmaMaxWarps) k_gather_sweep_tma(const __grid_constant__ TmaBatches a,
+                                                                           SweepTmaArgs t) {
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  __shared__ __align__(8) unsigned long long s_bar[kSweepTmaMaxWarps][kSweepTmaMaxSlots];
+  __shared__ uint32_t s_ep[kSweepMax];
+  __shared__ unsigned s_cnt[kSweepMax][2];
+  __shared__ unsigned s_reads, s_host;
+  __shared__ long long s_tot;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nb = a.n;
+  const int K = t.K;
+  if (threadIdx.x < nb) s_ep[threadIdx.x] = __ldcg(&a.b[threadIdx.x].sc->hdr.epoch);
+  if (threadIdx.x < 2 * kSweepMax) (&s_cnt[0][0])[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) {
+    s_reads = 0u;
+    s_host = 0u;
+    long long acc = 0;
+    for (int i = 0; i < nb; ++i) acc += __ldcg(&a.b[i].sc->sizes[a.L]);
+    s_tot = acc;
+  }
+  // per warp: ring [K][slot_bytes] | tag stage [nb][32] u64 | slot stage [32] i32 | row table
+  // [nb][32] i32 | slot metadata [K][1 + nb] i32 (mask, destination rows)
+  unsigned char* mine = s_dyn + (size_t)wib * t.warp_bytes;
+  unsigned char* ring = mine;
+  unsigned long long* stag = reinterpret_cast<unsigned long long*>(mine + (size_t)K * t.slot_bytes);
+  int* sslot = reinterpret_cast<int*>(stag + nb * 32);
+  int* rt = sslot + 32;
+  int* meta = rt + nb * 32;
+  for (int i = lane; i < K * t.slot_bytes / 16; i += 32) reinterpret_cast<int4*>(ring)[i] = make_int4(0, 0, 0, 0);
+  if (lane == 0) {
+    for (int k = 0; k < K; ++k) mbar_init(smem_addr(&s_bar[wib][k]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero tails visible to bulk stores
+  __syncthreads();
+  const uint64_t pol = t.hint ? policy_evict_first() : policy_evict_normal();
+  // lane b holds batch b's output row address base, stride and width (bulk stores are per lane)
+  float* xb = nullptr;
+  int64_t ldb = 0;
+  uint32_t ob = 0;
+  if (lane < nb) {
+    xb = a.b[lane].X;
+    ldb = a.b[lane].ldx;
+    ob = (uint32_t)a.b[lane].out16 * 16u;
+  }
+  unsigned long long* ticket = &a.b[0].sc->sweep_ticket;
+  auto take = [&]() -> int64_t {
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(ticket, 1ull);
+    return 32 * (int64_t)__shfl_sync(0xffffffffu, tk, 0);
+  };
+  auto prefetch = [&](int64_t g) {
+    if (g >= a.N) return;
+    const int64_t v = g + lane;
+    const bool in = v < a.N;
+    const int64_t vv = in ? v : 0;
+    for (int b = 0; b < nb; ++b) cp_async8(stag + b * 32 + lane, a.b[b].pos_of + vv, in ? 8 : 0);
+    cp_async4(sslot + lane, &a.dir[vv].slot, in ? 4 : 0);
+  };
+  unsigned reads = 0, host_reads = 0, hits = 0, misses = 0;
+  int64_t g = take();
+  prefetch(g);
+  cp_async_commit();
+  unsigned rem = 0, mask = 0;  // present lanes of the current group not yet issued; lane's mask
+  const char* src = nullptr;
+  bool done = false;
+  // the current group's probes -> masks, row table, sources, counters; then prefetch the next
+  auto next_group = [&]() {
+    cp_async_wait_all();
+    __syncwarp();
+    const int64_t v = g + lane;
+    const int32_t sl = v < a.N ? sslot[lane] : -1;
+    mask = 0;
+    for (int b = 0; b < nb; ++b) {
+      const unsigned long long tg = stag[b * 32 + lane];
+      if ((uint32_t)(tg >> 32) == s_ep[b]) {
+        mask |= 1u << b;
+        rt[b * 32 + lane] = (int)(0xFFFFFFFFu - (uint32_t)tg);
+      }
+    }
+    __syncwarp();
+    const int64_t g_next = take();
+    prefetch(g_next);
+    cp_async_commit();
+    src = nullptr;
+    if (mask) {
+      if (sl < 0)
+        src = reinterpret_cast<const char*>(a.hfeats + v * a.pitch);
+      else if (a.G == 1)
+        src = reinterpret_cast<const char*>(a.fcache + (int64_t)sl * a.pitch);
+      else
+        src = reinterpret_cast<const char*>(
+            reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(a.fbases) + sl % a.G)) +
+            (int64_t)(sl / a.G) * a.pitch);
+    }
+    const unsigned hitm = __ballot_sync(0xffffffffu, sl >= 0);
+    for (int b = 0; b < nb; ++b) {
+      const unsigned inb = __ballot_sync(0xffffffffu, (mask >> b) & 1u);
+      if (lane == b) {
+        hits += __popc(inb & hitm);
+        misses += __popc(inb & ~hitm);
+      }
+    }
+    rem = __ballot_sync(0xffffffffu, mask != 0);
+    reads += __popc(rem);
+    host_reads += __popc(rem & ~hitm);
+    g = g_next;
+  };
+  int64_t issued = 0, consumed = 0;
+  // load the next present node's row into slot issued % K (false: the sweep is over)
+  auto issue = [&]() -> bool {
+    while (!rem) {
+      if (done || g >= a.N) {
+        done = true;
+        return false;
+      }
+      next_group();
+    }
+    const int j = __ffs(rem) - 1;
+    rem &= rem - 1;
+    const int s = (int)(issued % K);
+    const unsigned mj = __shfl_sync(0xffffffffu, mask, j);
+    const char* sj = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), j));
+    int* ms = meta + s * (1 + nb);
+    if (lane < nb && ((mj >> lane) & 1u)) ms[1 + lane] = rt[lane * 32 + j];
+    if (lane == 0) {
+      ms[0] = (int)mj;
+      const uint32_t bar = smem_addr(&s_bar[wib][s]);
+      mbar_expect_tx(bar, (uint32_t)t.row_bytes);
+      bulk_g2s(smem_addr(ring + (size_t)s * t.slot_bytes), sj, (uint32_t)t.row_bytes, bar, pol);
+    }
+    __syncwarp();
+    ++issued;
+    return true;
+  };
+  for (int k = 0; k < K; ++k)
+    if (!issue()) break;
+  while (consumed < issued) {
+    const int s = (int)(consumed % K);
+    mbar_wait(smem_addr(&s_bar[wib][s]), (uint32_t)((consumed / K) & 1));
+    const int* ms = meta + s * (1 + nb);
+    const unsigned mk = (unsigned)ms[0];
+    if ((mk >> lane) & 1u)
+      bulk_s2g(xb + (int64_t)ms[1 + lane] * ldb, smem_addr(ring + (size_t)s * t.slot_bytes), ob, pol);
+    bulk_commit();
+    ++consumed;
+    bulk_wait_read1();  // stores of nodes < consumed - 1 have read their slots
+    __syncwarp();
+    if (issued < consumed - 1 + K) issue();
+  }
+  bulk_wait_all();
   cp_async_wait_all();
   if (lane < nb) {
     if (hits) atomicAdd(&s_cnt[lane][0], hits);
@@ -879,9 +1067,51 @@ static dci_status sweep_launch_v(dci_ctx* ctx, const TmaBatches& tb, int32_t out
   return DCI_OK;
 }
 
-static dci_status sweep_launch(dci_ctx* ctx, const TmaBatches& tb, cudaStream_t s) {
+static dci_status sweep_tma_launch(dci_ctx* ctx, const TmaBatches& tb, int32_t out16max, cudaStream_t s) {
+  // 8 warps x 4 slots measured best on M2 (1.43 ms per group of 20 alone; 4 x 6: 1.68 ms)
+  static const int W = std::max(1, std::min(kSweepTmaMaxWarps, env_int("DCI_SWEEP_WARPS", 8)));
+  static const int Kenv = std::max(2, std::min(kSweepTmaMaxSlots, env_int("DCI_SWEEP_SLOTS", 4)));
+  static const int hint = env_int("DCI_TMA_HINT", 1);
+  SweepTmaArgs t;
+  t.W = W;
+  t.slot_bytes = out16max * 16;
+  t.row_bytes = tb.pitch * 4;
+  t.hint = hint;
+  const int nb = tb.n;
+  auto warp_bytes = [&](int K) {
+    const int b = K * t.slot_bytes + nb * 32 * 8 + 128 + nb * 32 * 4 + K * (1 + nb) * 4;
+    return (b + 127) / 128 * 128;
+  };
+  int K = Kenv;
+  while (K > 2 && (size_t)W * warp_bytes(K) > 220 * 1024) --K;
+  t.K = K;
+  t.warp_bytes = warp_bytes(K);
+  const size_t smem = (size_t)W * t.warp_bytes;
+  if (smem > 220 * 1024) return fail(DCI_ERANGE, "sweep gather: feature rows too wide for the TMA ring");
+  static std::atomic<int> smem_set[kMaxDevices];
+  dci_status st = ensure_dyn_smem(reinterpret_cast<const void*>(k_gather_sweep_tma), smem_set, ctx->device, smem);
+  if (st != DCI_OK) return st;
+  static const int sms = env_int("DCI_SWEEP_SMS", 0);
+  const int nsm = (sms > 0 && sms < ctx->num_sms) ? sms : ctx->num_sms;
+  k_gather_sweep_tma<<<nsm, 32 * W, smem, s>>>(tb, t);
+  ++ctx->launches;
+  return DCI_OK;
+}
+
+static dci_status sweep_launch(dci_ctx* ctx, const TmaBatches& tb, bool alone, cudaStream_t s, int* used) {
   int32_t out16max = 0;
   for (int i = 0; i < tb.n; ++i) out16max = std::max(out16max, tb.b[i].out16);
+  // DCI_SWEEP_KIND: auto (default: bulk copies when the gather runs alone, register copies when the
+  // next group's sampling will run beside it) | ldg | tma
+  static const int kind = [] {
+    const char* e = getenv("DCI_SWEEP_KIND");
+    return !e ? 2 : (e[0] == 't' || e[0] == 'T') ? 1 : (e[0] == 'l' || e[0] == 'L') ? 0 : 2;
+  }();
+  if (kind == 1 || (kind == 2 && alone)) {
+    *used = 2;
+    return sweep_tma_launch(ctx, tb, out16max, s);
+  }
+  *used = 1;
   // 16-byte words per lane per pass over a row (rows longer than 32 * VPL words take several passes)
   if (out16max <= 32) return sweep_launch_v<1>(ctx, tb, out16max, s);
   if (out16max <= 64) return sweep_launch_v<2>(ctx, tb, out16max, s);
@@ -895,11 +1125,13 @@ bool gather_sweep_enabled() {
 }
 
 dci_status launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n,
-                              int32_t L, dci_batch_result* stage, bool sweep, cudaStream_t s) {
+                              int32_t L, dci_batch_result* stage, bool sweep, bool alone, cudaStream_t s,
+                              int* kind) {
   TmaBatches tb = tma_batches(ctx, L);
   tb.stage = stage;
   for (int i = 0; i < n; ++i) tma_add(&tb, ctx, ws[i], outs + i, nullptr);
-  if (sweep && n >= 2 && n <= kSweepMax) return sweep_launch(ctx, tb, s);
+  if (sweep && n >= 2 && n <= kSweepMax) return sweep_launch(ctx, tb, alone, s, kind);
+  *kind = 0;
   return tma_launch(ctx, tb, outs, s);
 }
 
@@ -919,6 +1151,7 @@ static FusedArgs fused_args(dci_ctx* ctx, dci_workspace* ws, int32_t L, const dc
   FusedArgs a;
   a.dir = ctx->d_dir;
   a.pos_of = ws->pos_of;
+  a.hmask = ws->hmask;
   a.sc = ws->scal;
   a.N = ctx->N;
   a.L = L;

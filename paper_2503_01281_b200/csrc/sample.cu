@@ -65,7 +65,8 @@ struct HopBatch {
   const int32_t* prev_bptr;
   int32_t* prev_bsrc;
   int32_t* bptr;                   // this hop's block row pointers (written by the scan)
-  unsigned long long* pos_of;      // the workspace's node -> position tag table
+  unsigned long long* pos_of;      // the workspace's node -> position tag table (dense or hashed)
+  uint32_t hmask;                  // 0: dense table; else hashed capacity - 1 (pt_insert / pt_find)
   BatchScalars* sc;
   unsigned long long* tiles;       // this hop's scan tile state
   unsigned long long* prev_tiles;  // previous hop's scan tile state (cleared here)
@@ -187,7 +188,7 @@ __device__ __forceinline__ void hop_prologue(const HopLaunch& a, const HopShared
       if (s < 0 || (int64_t)s >= a.N)
         atomicCAS(&hb.sc->status, 0, (int32_t)DCI_ESEED);
       else
-        atomicMax(hb.pos_of + s, S.ehi[b] | (0xFFFFFFFFu - (uint32_t)d));
+        atomicMax(pt_insert(hb.pos_of, hb.hmask, s, (uint32_t)(S.ehi[b] >> 32)), S.ehi[b] | (0xFFFFFFFFu - (uint32_t)d));
     }
     return;
   }
@@ -223,7 +224,7 @@ __device__ __forceinline__ void hop_prologue(const HopLaunch& a, const HopShared
     for (int u = 0; u < U; ++u) {
       if (q0 + u * nthreads < ptot && su[u] < ku[u]) {
         const HopBatch& hb = a.b[bu[u]];
-        tu[u] = __ldcg(hb.pos_of + cu[u]);
+        tu[u] = pt_tag(hb.pos_of, hb.hmask, cu[u], (uint32_t)(S.ehi[bu[u]] >> 32));
         pu[u] = hb.prev_bptr[du[u]];
       }
     }
@@ -503,7 +504,8 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     if (active && gl == 0) hb.kcnt[d] = k;
     if (valid) {
       const unsigned long long tag = S.ehi[b] | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
-      if (!a.precheck || __ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
+      unsigned long long* tp = pt_insert(hb.pos_of, hb.hmask, x, (uint32_t)(S.ehi[b] >> 32));
+      if (!a.precheck || __ldcg(tp) < tag) atomicMax(tp, tag);
       if (a.edge_counts) atomicAdd(a.edge_counts + host_off + rank, 1);
     }
     v = v_next;
@@ -630,7 +632,8 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
           x = ld_host_i32(a.uidx + host_off + rank);
         atomicAdd(&S.cnt[b][hit ? 0 : 1], 1u);
         const unsigned long long tag = S.ehi[b] | (0xFFFFFFFFu - (uint32_t)(n_h + d * f + pos));
-        if (__ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
+        unsigned long long* tp = pt_insert(hb.pos_of, hb.hmask, x, (uint32_t)(S.ehi[b] >> 32));
+        if (__ldcg(tp) < tag) atomicMax(tp, tag);
         if (a.edge_counts) atomicAdd(a.edge_counts + host_off + rank, 1);
       }
       hb.cand[d * f + pos] = x;
@@ -737,7 +740,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
         for (int u = 0; u < 8; ++u) x[u] = (s0 + u < k) ? c[s0 + u] : -1;
         unsigned long long t[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? __ldcg(hb.pos_of + x[u]) : 0ull;
+        for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? pt_tag(hb.pos_of, hb.hmask, x[u], (uint32_t)(ehi >> 32)) : 0ull;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) {
@@ -749,7 +752,8 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
       }
       if (h == 0) {
         const int32_t sd = hb.F[d];
-        if (sd >= 0 && (int64_t)sd < a.N && __ldcg(hb.pos_of + sd) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
+        if (sd >= 0 && (int64_t)sd < a.N &&
+            pt_tag(hb.pos_of, hb.hmask, sd, (uint32_t)(ehi >> 32)) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
           atomicCAS(&hb.sc->status, 0, (int32_t)DCI_EDUP);
       }
     }
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
           const int s = __ffs(m) - 1;
           const int32_t x = c[s];
           hb.F[nid] = x;
-          hb.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+          *pt_find(hb.pos_of, hb.hmask, x, (uint32_t)(ehi >> 32)) = ehi | (0xFFFFFFFFu - nid);
           ++nid;
         }
       } else if (nwide) {
@@ -829,9 +833,10 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
         const uint32_t base = (uint32_t)(n_h + d * f);
         for (uint32_t s = 0; s < k; ++s) {
           const int32_t x = c[s];
-          if (x >= 0 && __ldcg(hb.pos_of + x) == (ehi | (0xFFFFFFFFu - (base + s)))) {
+          unsigned long long* tp = x >= 0 ? pt_find(hb.pos_of, hb.hmask, x, (uint32_t)(ehi >> 32)) : nullptr;
+          if (tp && __ldcg(tp) == (ehi | (0xFFFFFFFFu - (base + s)))) {
             hb.F[nid] = x;
-            hb.pos_of[x] = ehi | (0xFFFFFFFFu - nid);
+            *tp = ehi | (0xFFFFFFFFu - nid);
             ++nid;
           }
         }
@@ -869,6 +874,8 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
     return e ? atoi(e) : 1;
   }();
   a.sweep = sweep;
+  for (int i = 0; i < n; ++i)
+    if (ws[i]->hmask) a.sweep = 0;  // the node sweep probes every node id: dense tables only
   for (int i = 0; i < n; ++i) {
     HopBatch& b = a.b[i];
     const int h = p[i].hop;
@@ -881,6 +888,7 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
     b.prev_bsrc = p[i].prev_bsrc;
     b.bptr = p[i].bptr;
     b.pos_of = ws[i]->pos_of;
+    b.hmask = ws[i]->hmask;
     b.sc = ws[i]->scal;
     b.tiles = h < ws[i]->L ? ws[i]->tile_state + ws[i]->tile_off[h] : nullptr;
     if (h > 0) {

@@ -197,8 +197,11 @@ def test_many_stats_and_profiling(filled):
     assert sum(st["frontier_rows"] for st in sts) == 3 * rows
     D, N, n = ctx.D, ctx.N, len(wss)
     read = sts[0]["rows_read"]
-    if 3 * rows // 3 >= N:  # node sweep: each row read once per group
-        assert read < 3 * rows
+    kinds = sts[0]["gather_kinds"]
+    assert sum(kinds) == 3 and all(sum(st["gather_kinds"]) == 0 for st in sts[1:])
+    if kinds[0] == 0:  # node sweep (register or bulk copies): each row read once per group
+        assert n >= 2 and sts[0]["table_bytes"] == 8 * N  # sweeps need the dense position table
+        assert read <= 3 * rows
         assert sts[0]["gather_bytes"] == 3 * N * (8 * n + 4) + read * 4 * D + 3 * rows * 4 * D
     else:
         assert read == 3 * rows
