@@ -381,8 +381,8 @@ def sample_gather(ctx: Context, ws: Workspace, seeds, fanouts, seed: int, out: B
 
 
 def sample_gather_many(ctx: Context, wss, seeds_list, fanouts, seed: int, outs, stream=None):
-    """dci_sample_gather_many: n <= 16 batches (one workspace and one BatchOut each) sampled
-    concurrently and gathered by ONE TMA gather launch; asynchronous on `stream`."""
+    """dci_sample_gather_many: n <= 32 (DCI_MAX_GROUP) batches (one workspace and one BatchOut each) sampled
+    concurrently and gathered by ONE group gather launch (row mode or node sweep); asynchronous on `stream`."""
     import torch
     n = len(wss)
     if not n == len(seeds_list) == len(outs):

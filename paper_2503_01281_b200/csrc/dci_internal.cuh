@@ -278,8 +278,8 @@ dci_status cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::dci::cuda_fail(_e, #expr);          \
   } while (0)
 
-// dci_sample_gather_many schedule: sampling of a group waits for the previous group's gather
-// (default) or overlaps it (DCI_PHASED=0)
+// dci_sample_gather_many schedule (DCI_PHASED): unset or 0 (default) = a group's sampling overlaps
+// the previous group's gather; 1 = it waits for that gather (phased); 2 = only its last hop waits
 // Flags of the events that order work ACROSS streams (sampling -> gather -> caller, and the
 // phased schedule's gather -> next group).  Timing-enabled on purpose: measured on B200 (driver
 // 580), a stream waiting on a cudaEventDisableTiming event started its next work later, which cost
