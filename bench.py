@@ -168,6 +168,33 @@ def host_link_peaks(region_bytes: float = 0.0):
     return 51.5, 90.0, "assumed"
 
 
+def host_read_peak(region_bytes: float):
+    """Best random-read PAYLOAD rate of the host link (GB/s) for a pinned region of this size:
+    the max over request sizes (32 B .. 2 KB) of tools/probe/hostreq_probe.cu's rates
+    (profiles/hostreq_probe.jsonl, interpolated in log2 of the region), i.e. no random read
+    pattern over that region moves payload faster.  Falls back to host_link_peaks()."""
+    p = os.path.join(ROOT, "profiles", "hostreq_probe.jsonl")
+    if not os.path.exists(p):
+        peak, _, kind = host_link_peaks(region_bytes)
+        return peak, kind
+    best = {}
+    for ln in open(p):
+        try:
+            d = json.loads(ln)
+        except ValueError:
+            continue
+        if d.get("probe") == "host_random_read" and d["bytes"] >= 32:
+            best[d["region_GB"]] = max(best.get(d["region_GB"], 0.0), float(d["GBps"]))
+    pts = sorted(best.items())
+    gb = max(region_bytes / 2 ** 30, 1e-9)
+    peak = pts[0][1] if gb <= pts[0][0] else pts[-1][1]
+    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+        if x0 <= gb <= x1:
+            w = (np.log2(gb) - np.log2(x0)) / (np.log2(x1) - np.log2(x0))
+            peak = y0 + (y1 - y0) * w
+    return peak, f"best random-read payload rate for a {gb:.2f} GB pinned region (tools/probe/hostreq_probe.cu)"
+
+
 def _cfg(args):
     import dataclasses
     cfg = synth.CONFIGS[args.config]
@@ -516,9 +543,9 @@ def run_ours(args):
     kinds = np.sum([st["gather_kinds"] for st in sts], axis=0)
     table_mb = max(st["table_bytes"] for st in sts) / 2 ** 20
     host_rows = sum(st["host_rows_read"] for st in sts)
-    host_lines = sum(st["host_adj_lines"] for st in sts)
+    host_sectors = sum(st["host_adj_sectors"] for st in sts)
     tot = parallel.sum_over_ranks([sum(st["seeds"] for st in sts), launches, rows, alg_bytes, g_ms, s_ms, n_timed,
-                                   n_glaunch, rows_read, *cn.tolist(), host_rows, host_lines], device=dev)
+                                   n_glaunch, rows_read, *cn.tolist(), host_rows, host_sectors], device=dev)
     seeds_all = tot[0] / R  # per timed region
     value = seeds_all / (ms / 1e3)
     rep_values = [seeds_all / (m / 1e3) for m in ms_list]
@@ -597,7 +624,7 @@ def run_ours(args):
     hbm_peak, peak_kind = measured_peaks()
     # Binding resource of the gather kernel: HBM (hit rows read + every row written + 4 B
     # slot lookup) vs the host link (miss rows read through UVA).
-    host_peak, host_req_peak, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats())
+    host_peak, _, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats())
     hits_rows, miss_rows = cn[2], cn[3]
     # rows actually read: a node-sweep group reads each row once for all its batches; misses
     # among them are apportioned by the batches' miss fraction
@@ -618,31 +645,32 @@ def run_ours(args):
               if G else "k_gather (fused route + relabel + feature gather, S7-S8)")
     aggregate_gbs = bind_b / (ms_tot / 1e3) / 1e9  # all gather launches over the timed wall time
     # Whole-step roofline of SURVEY §8(d), over all timed regions: T_roof = max(B_hbm/BW_hbm,
-    # B_host/BW_host, N_req/R_req).  Algorithmic bytes: HBM = the gather's hit-row reads and all row
-    # writes (+ lookups) + the sampler's cached element reads and candidate writes (4 B each); host =
-    # miss rows + 4 B per adjacency miss.  Requests: host feature rows + distinct 128-byte host lines
-    # of the adjacency misses (the library counts both).  R_req = the probe's random-read rate for a
-    # pinned region of the graph's size (tools/probe, profiles/hostlink_peaks.json).
-    host_rows_read, host_adj_lines = tot[13], tot[14]
+    # B_host/BW_host).  Algorithmic bytes: HBM = the gather's hit-row reads and all row writes
+    # (+ lookups) + the sampler's cached element reads and candidate writes (4 B each); host = the
+    # miss rows the gathers read (4 * pitch bytes each) + the distinct 32-byte sectors the
+    # adjacency misses read (the unit the GPU fetches from system memory; the library counts both).
+    # BW_host = the best random-read payload rate measured for a pinned region of the graph's size
+    # (profiles/hostreq_probe.jsonl), so T_host is a lower bound on the link time of that traffic.
+    host_rows_read, host_adj_sectors = tot[13], tot[14]
     samples = cn[0] + cn[1]
     B_hbm = hbm_b + 4.0 * cn[0] + 4.0 * samples
-    B_host = host_rows_read * 4.0 * D + 4.0 * cn[1]
-    N_req = host_rows_read + host_adj_lines
+    B_host = host_rows_read * 4.0 * cfg.pitch_floats() + 32.0 * host_adj_sectors
     region = cfg.N * 4.0 * cfg.pitch_floats() + 4.0 * cfg.E
-    req_rate = min(host_req_peak, host_link_peaks(region)[0] * 1e9 / 512.0 / 1e6)  # M requests/s
-    T_terms = {"hbm_ms": B_hbm / (hbm_peak * 1e9) * 1e3, "host_bytes_ms": B_host / (host_link_peaks()[0] * 1e9) * 1e3,
-               "host_requests_ms": N_req / (req_rate * 1e6) * 1e3}
+    bw_host, bw_host_kind = host_read_peak(region)
+    T_terms = {"hbm_ms": B_hbm / (hbm_peak * 1e9) * 1e3, "host_ms": B_host / (bw_host * 1e9) * 1e3}
     T_roof = max(T_terms.values())
     host_link = {"feature_miss_GBps": host_b / (ms_tot / 1e3) / 1e9, "peak_GBps": host_peak,
-                 "feature_frac": host_b / (ms_tot / 1e3) / 1e9 / host_peak,
-                 "adj_miss_Mreads_per_s": cn[1] / (ms_tot / 1e3) / 1e6, "random_read_peak_Mreq_per_s": host_req_peak,
-                 "peak_kind": host_kind,
-                 "requests_M_per_s": N_req / (ms_tot / 1e3) / 1e6, "request_peak_M_per_s": req_rate,
-                 "host_rows_read": host_rows_read, "host_adj_lines": host_adj_lines,
+                 "feature_frac": host_b / (ms_tot / 1e3) / 1e9 / host_peak, "peak_kind": host_kind,
+                 "adj_miss_Mreads_per_s": cn[1] / (ms_tot / 1e3) / 1e6,
+                 "host_rows_read": host_rows_read, "host_adj_sectors": host_adj_sectors,
+                 "host_payload_GBps": B_host / (ms_tot / 1e3) / 1e9, "host_read_peak_GBps": bw_host,
+                 "host_read_peak_kind": bw_host_kind,
                  "step_roofline": {"T_roof_ms": T_roof, "T_measured_ms": ms_tot, "frac": T_roof / ms_tot,
                                    "binding": max(T_terms, key=T_terms.get), **T_terms,
+                                   "B_hbm_bytes": B_hbm, "B_host_bytes": B_host,
                                    "note": "whole timed regions (all steps); T_roof = max(B_hbm/BW_hbm, "
-                                           "B_host/BW_host, N_req/R_req), SURVEY §8(d)"}}
+                                           "B_host/BW_host), SURVEY §8(d); BW_host = best measured random-read "
+                                           "payload rate for the graph's pinned region"}}
     steps_total = steps_eff * world if args.scaling == "weak" else steps_eff
     avg_fl = tot[2] / max(1, steps_total * R)
     traffic = None

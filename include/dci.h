@@ -328,10 +328,11 @@ dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* ga
  * for all its batches); gather_bytes: the gather's algorithmic bytes (row
  * reads + row writes + lookups), also booked on a group's first workspace.
  * host_rows_read: feature rows read from pinned host memory (misses; once per row in a node
- * sweep); host_adj_lines: distinct 128-byte host lines read by adjacency misses (per dst node and
- * hop; a node-sweep hop reads a node's elements once for all batches) -- the host-link request
- * count of the bench roofline (T_roof = max(B_hbm/BW_hbm, B_host/BW_host,
- * N_req/R_req)).  Both are booked on the first workspace of a launch.
+ * sweep); host_adj_sectors: distinct 32-byte host sectors (the unit the GPU fetches from system
+ * memory) read by adjacency misses (per dst node and hop; a node-sweep hop reads a node's
+ * elements once for all batches).  Together they give the host-link bytes of the bench roofline
+ * (T_roof = max(B_hbm/BW_hbm, B_host/BW_host, ...)).  Both are booked on the first
+ * workspace of a launch.
  * reset != 0 zeroes the totals after reading them. */
 typedef struct dci_ws_stats {
   uint64_t batches;
@@ -345,7 +346,7 @@ typedef struct dci_ws_stats {
   uint64_t rows_read;
   uint64_t gather_bytes;
   uint64_t host_rows_read;
-  uint64_t host_adj_lines;
+  uint64_t host_adj_sectors;
   uint64_t gather_kinds[3]; /* group gathers this workspace led: row mode, node sweep with register
                                copies, node sweep with bulk copies */
   uint64_t table_bytes;     /* device bytes of the workspace's position table (dense 8 N, or hashed) */

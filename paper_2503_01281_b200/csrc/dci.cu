@@ -141,9 +141,17 @@ dci_status trec_fold(dci_workspace* ws, dci_workspace::TimeRec& r) {
   if (r.state & 2) {
     float ms = 0.f;
     DCI_CUDA(cudaEventSynchronize(r.e[3]));
-    DCI_CUDA(cudaEventElapsedTime(&ms, r.e[2], r.e[3]));
+    if (r.state & 4) {  // split gather: the two launches, without the wait between them
+      float ms2 = 0.f;
+      DCI_CUDA(cudaEventElapsedTime(&ms, r.e[2], r.e[4]));
+      DCI_CUDA(cudaEventElapsedTime(&ms2, r.e[5], r.e[3]));
+      ms += ms2;
+      ws->acc_gather_launches += 2;
+    } else {
+      DCI_CUDA(cudaEventElapsedTime(&ms, r.e[2], r.e[3]));
+      ws->acc_gather_launches += 1;
+    }
     ws->acc_gather_ms += ms;
-    ws->acc_gather_launches += 1;
   }
   r.state = 0;
   return DCI_OK;
@@ -622,14 +630,17 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
     if ((e = cudaMalloc(&w->kcnt[i], sizeof(int32_t) * std::max<int64_t>(max_front, 1))) != cudaSuccess)
       return bail(e, "cudaMalloc(kcnt)");
   }
+  if ((e = cudaMalloc(&w->nmask, sizeof(uint32_t) * std::max<int64_t>(max_front, 1))) != cudaSuccess)
+    return bail(e, "cudaMalloc(nmask)");
   if ((e = cudaMalloc(&w->tile_state, sizeof(unsigned long long) * w->tiles_cap)) != cudaSuccess)
     return bail(e, "cudaMalloc(tile_state)");
   if ((e = cudaMalloc(&w->scal, sizeof(BatchScalars))) != cudaSuccess) return bail(e, "cudaMalloc(scal)");
   if ((e = cudaMalloc(&w->seeds_stage, sizeof(int32_t) * max_batch)) != cudaSuccess) return bail(e, "cudaMalloc");
   for (auto& r : w->trec)
-    for (int i = 0; i < 4; ++i)
-      if ((e = cudaEventCreate(&r.e[i])) != cudaSuccess) return bail(e, "event");
+    for (auto& ev : r.e)
+      if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_mid, kCrossStreamEvent)) != cudaSuccess) return bail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&w->ev_pre, kCrossStreamEvent)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->ev_done, kCrossStreamEvent)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaEventCreateWithFlags(&w->gseeds_ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "event");
   if ((e = cudaHostAlloc(reinterpret_cast<void**>(&w->hdr_ring), sizeof(BatchHeader) * dci_workspace::kHdrRing,
@@ -659,15 +670,17 @@ dci_status dci_workspace_destroy(dci_workspace* w) {
     cudaFree(w->cand[i]);
     cudaFree(w->kcnt[i]);
   }
+  cudaFree(w->nmask);
   cudaFree(w->tile_state);
   cudaFree(w->scal);
   cudaFree(w->seeds_stage);
   for (auto& r : w->trec)
-    for (int i = 0; i < 4; ++i)
-      if (r.e[i]) cudaEventDestroy(r.e[i]);
+    for (auto& ev : r.e)
+      if (ev) cudaEventDestroy(ev);
   for (int i = 0; i < dci_workspace::kHdrRing; ++i)
     if (w->hdr_ev[i]) cudaEventDestroy(w->hdr_ev[i]);
   if (w->ev_mid) cudaEventDestroy(w->ev_mid);
+  if (w->ev_pre) cudaEventDestroy(w->ev_pre);
   if (w->ev_done) cudaEventDestroy(w->ev_done);
 
   if (w->hdr_ring) cudaFreeHost(w->hdr_ring);
@@ -780,7 +793,7 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   // a CUDA graph on the first workspace, re-captured when the group (workspaces, outputs,
   // fan-outs, caches) changes; the last hop's relabel follows the gather launch ----
   struct GroupSig {
-    int32_t n, L;
+    int32_t n, L, hs;
     int32_t fan[DCI_MAX_LAYERS];
     uint64_t ws[DCI_MAX_GROUP];  // workspace uids (a freed workspace's address may be reused)
     dci_batch_out out[DCI_MAX_GROUP];
@@ -824,14 +837,40 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
       }
       if (h >= h0) {
         launch_sample_hop(ctx, ws, p, n, es);
+        launch_newmask_sweep(ctx, ws, p, n, es);
         launch_scan_hop(ctx, ws, p, n, es);
       }
       for (int i = 0; i < n; ++i) prev[i] = p[i];
     }
   };
+  // node sweep when the group's frontier bounds together reach N (Reddit-shaped: one batch's bound
+  // alone is N); host-resident papers100M-shaped groups stay in row mode
+  bool sweep = false;
+  bool all_dense = true;
+  for (int i = 0; i < n; ++i) all_dense &= ws[i]->hmask == 0;
+  if (gather_sweep_enabled() && n >= 2 && all_dense) {
+    int64_t grow = 1;
+    for (int h = 0; h < L; ++h) grow = std::min<int64_t>(ctx->N, grow * (1 + (int64_t)fanouts[h]));
+    int64_t cover = 0;
+    for (int i = 0; i < n && cover < ctx->N; ++i) cover += std::min<int64_t>(ctx->N, (int64_t)B[i] * grow);
+    sweep = cover >= ctx->N;
+  }
+  // alone: the previous group's gather had already finished when this group was enqueued, so
+  // nothing is queued ahead of this group's gather
+  const bool alone = !ctx->gather_q_valid || cudaEventQuery(ctx->gather_q_ev) == cudaSuccess;
+  // Split gather (DCI_SPLIT_GATHER=1; off by default): when nothing else would run beside this
+  // group's sampling (alone), its node-sweep gather is two launches -- the rows of F_{L-1} right
+  // after hop L-2's scan, beside hop L-1's sampling and scan, then the rows added by hop L-1 -- to
+  // hide the last hop's sampling.  Measured on M2 (groups of 20, one group per timed region): no
+  // gain (10.72 vs 10.74 M seeds/s): the two launches take 1.71 ms against 1.44 ms for one (each
+  // reads the shared rows, and the first shares the GPU with the sampler), which cancels the
+  // ~0.3 ms of hidden sampling.  Pipelined groups (not alone) never split.
+  const bool split = sweep && alone && L >= 2 && gather_split_enabled() && !gather_concurrent();
   // split schedule: hops [0, hs) before the wait for the previous group's gather, [hs, L) after
   const bool phased = group_phased();
-  const int hs = (phased && group_split() && L >= 2) ? L - 1 : 0;
+  const bool split_sched = phased && group_split() && L >= 2;
+  const int hs = (split || split_sched) ? L - 1 : 0;
+  sig->hs = hs;
   // the relabel of every batch's last hop: needed by the caller, not by the gather, so it runs
   // on `stream` while the gather runs on the gather stream
   auto enqueue_epilogue = [&](cudaStream_t es) {
@@ -888,7 +927,7 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   // launch runs ~3 % slower beside the sampler, exp60).  DCI_PHASED=1: a group
   // samples only after the previous group's gather has finished; DCI_PHASED=2: only its last hop
   // waits for it.
-  if (hs == 0 && phased && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
+  if (phased && !split_sched && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
   if (tr) DCI_CUDA(cudaEventRecord(tr->e[0], s));
   if (use_graph) {
     ctx->launches += gg->kernels;
@@ -896,8 +935,34 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   } else {
     enqueue(s, 0, hs > 0 ? hs : L);
   }
+  // ---- the group's gather, on the context's gather stream (group gathers run one at a time;
+  // DCI_GATHER_SERIAL=0 puts it on `stream` instead).  Node-sweep kernel: the bulk-copy one
+  // (faster alone, 1.43 vs 1.55 ms on M2) when the gather runs by itself, else the register-copy
+  // one, whose full SMs keep the next group's sampling from slowing it (exp r2-6) ----
+  cudaStream_t gs = gather_concurrent() ? s : ctx->gstream;
+  dci_batch_result* stage = nullptr;
+  if (w0->want_stage) {
+    if (!w0->stage) DCI_CUDA(cudaMalloc(&w0->stage, sizeof(dci_batch_result) * DCI_MAX_GROUP));
+    stage = w0->stage;
+    w0->staged = true;
+  }
+  auto gather_launch = [&](int32_t phase) -> dci_status {
+    int kind = 0;
+    dci_status gst = launch_gather_many(ctx, ws, outs, n, L, stage, sweep, alone, phase, gs, &kind);
+    if (gst != DCI_OK) return gst;
+    ++w0->kind_launches[kind];
+    return DCI_OK;
+  };
+  if (split) {  // first launch: the rows of F_{L-1}, beside hop L-1's sampling and scan
+    DCI_CUDA(cudaEventRecord(w0->ev_pre, s));
+    DCI_CUDA(cudaStreamWaitEvent(gs, w0->ev_pre, 0));
+    if (tr) DCI_CUDA(cudaEventRecord(tr->e[2], gs));
+    dci_status gst = gather_launch(1);
+    if (gst != DCI_OK) return gst;
+    if (tr) DCI_CUDA(cudaEventRecord(tr->e[4], gs));
+  }
   if (hs > 0) {
-    if (ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
+    if (split_sched && ctx->gather_ev_valid) DCI_CUDA(cudaStreamWaitEvent(s, ctx->gather_ev, 0));
     if (use_graph) {
       ctx->launches += gg->kernels2;
       DCI_CUDA(cudaGraphLaunch(gg->exec2, s));
@@ -909,43 +974,14 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     DCI_CUDA(cudaEventRecord(tr->e[1], s));
     tr->state |= 1;
   }
-  // ---- one TMA gather over the whole group, on the context's gather stream (group gathers run
-  // one at a time; DCI_GATHER_SERIAL=0 puts it on `stream` instead) ----
-  cudaStream_t gs = s;
-  if (!gather_concurrent()) {
-    gs = ctx->gstream;
+  if (gs != s) {
     DCI_CUDA(cudaEventRecord(w0->ev_mid, s));
     DCI_CUDA(cudaStreamWaitEvent(gs, w0->ev_mid, 0));
   }
-  if (tr) DCI_CUDA(cudaEventRecord(tr->e[2], gs));
-  dci_batch_result* stage = nullptr;
-  if (w0->want_stage) {
-    if (!w0->stage) DCI_CUDA(cudaMalloc(&w0->stage, sizeof(dci_batch_result) * DCI_MAX_GROUP));
-    stage = w0->stage;
-    w0->staged = true;
-  }
-  // node sweep when the group's frontier bounds together reach N (Reddit-shaped: one batch's bound
-  // alone is N); host-resident papers100M-shaped groups stay in row mode
-  bool sweep = false;
-  bool all_dense = true;
-  for (int i = 0; i < n; ++i) all_dense &= ws[i]->hmask == 0;
-  if (gather_sweep_enabled() && n >= 2 && all_dense) {
-    int64_t grow = 1;
-    for (int h = 0; h < L; ++h) grow = std::min<int64_t>(ctx->N, grow * (1 + (int64_t)fanouts[h]));
-    int64_t cover = 0;
-    for (int i = 0; i < n && cover < ctx->N; ++i) cover += std::min<int64_t>(ctx->N, (int64_t)B[i] * grow);
-    sweep = cover >= ctx->N;
-  }
+  if (tr) DCI_CUDA(cudaEventRecord(tr->e[split ? 5 : 2], gs));
   {
-    // which node-sweep kernel: the bulk-copy one (faster alone, 1.43 vs 1.55 ms on M2) when this
-    // gather will run by itself -- the previous group's gather had already finished when this
-    // group was enqueued, so nothing else is queued ahead of it -- else the register-copy one,
-    // whose full SMs keep the next group's sampling from slowing it (exp r2-6)
-    const bool alone = !ctx->gather_q_valid || cudaEventQuery(ctx->gather_q_ev) == cudaSuccess;
-    int kind = 0;
-    dci_status gst = launch_gather_many(ctx, ws, outs, n, L, stage, sweep, alone, gs, &kind);
+    dci_status gst = gather_launch(split ? 2 : 0);
     if (gst != DCI_OK) return gst;
-    ++w0->kind_launches[kind];
     DCI_CUDA(cudaEventRecord(ctx->gather_q_ev, gs));
     ctx->gather_q_valid = true;
   }
@@ -956,7 +992,7 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
   }
   if (tr) {
     DCI_CUDA(cudaEventRecord(tr->e[3], gs));
-    tr->state |= 2;
+    tr->state |= split ? 6 : 2;
   }
   if (gs != s) {
     DCI_CUDA(cudaEventRecord(w0->ev_done, gs));
@@ -1305,11 +1341,20 @@ dci_status dci_workspace_set_profiling(dci_workspace* ws, int32_t on) {
 dci_status dci_workspace_stage_ms(dci_workspace* ws, float* sample_ms, float* gather_ms) {
   if (!ws) return fail(DCI_EINVAL, "null workspace");
   const dci_workspace::TimeRec& r = ws->trec[ws->trec_cur];
-  if (r.state != 3) return fail(DCI_ESTATE, "no profiled batch recorded");
+  if ((r.state & 3) != 3) return fail(DCI_ESTATE, "no profiled batch recorded");
   DeviceGuard g(ws->device);
   DCI_CUDA(cudaEventSynchronize(r.e[3]));
   if (sample_ms) DCI_CUDA(cudaEventElapsedTime(sample_ms, r.e[0], r.e[1]));
-  if (gather_ms) DCI_CUDA(cudaEventElapsedTime(gather_ms, r.e[2], r.e[3]));
+  if (gather_ms) {
+    if (r.state & 4) {  // split gather: both launches, without the wait between them
+      float a = 0.f, b = 0.f;
+      DCI_CUDA(cudaEventElapsedTime(&a, r.e[2], r.e[4]));
+      DCI_CUDA(cudaEventElapsedTime(&b, r.e[5], r.e[3]));
+      *gather_ms = a + b;
+    } else {
+      DCI_CUDA(cudaEventElapsedTime(gather_ms, r.e[2], r.e[3]));
+    }
+  }
   return DCI_OK;
 }
 
@@ -1334,13 +1379,13 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   out->rows_read = h.acc_rows_read;
   out->gather_bytes = h.acc_gather_bytes;
   out->host_rows_read = h.acc_host_rows;
-  out->host_adj_lines = h.acc_host_lines;
+  out->host_adj_sectors = h.acc_host_sectors;
   for (int k = 0; k < 3; ++k) out->gather_kinds[k] = ws->kind_launches[k];
   out->table_bytes = ws->table_bytes;
   if (reset) {
     h.acc_batches = h.acc_seeds = h.acc_rows = 0;
     h.acc_rows_read = h.acc_gather_bytes = 0;
-    h.acc_host_rows = h.acc_host_lines = 0;
+    h.acc_host_rows = h.acc_host_sectors = 0;
     for (auto& k : ws->kind_launches) k = 0;
     for (int c = 0; c < 4; ++c) h.acc_counters[c] = 0;
     DCI_CUDA(cudaMemcpy(ws->scal, &h, sizeof(h), cudaMemcpyHostToDevice));

@@ -112,9 +112,9 @@ struct BatchScalars {
   // its batches) and the gather's algorithmic bytes; launch_reads is the running
   // count of the current launch (group launches accumulate on their first batch's scalars)
   unsigned long long acc_rows_read, acc_gather_bytes, launch_reads;
-  // host-link traffic (bench roofline): 128-byte host lines read by adjacency misses (sampling
+  // host-link traffic (bench roofline): 32-byte host sectors read by adjacency misses (sampling
   // kernels), feature rows read from pinned host memory (gathers); booked on a launch's first batch
-  unsigned long long acc_host_lines, acc_host_rows;
+  unsigned long long acc_host_sectors, acc_host_rows;
   // node-sweep gather: next 32-node group to take (dynamic schedule; reset by the launch's last block)
   unsigned long long sweep_ticket;
 };
@@ -201,6 +201,7 @@ struct dci_workspace {
   uint32_t epoch = 0;
   int32_t* cand[2] = {nullptr, nullptr};  // ping-pong [cand_cap] padded candidates
   int32_t* kcnt[2] = {nullptr, nullptr};  // ping-pong [max hop_cap] samples per dst
+  uint32_t* nmask = nullptr;  // [max hop_cap] new-candidate slot masks of a node-sweep hop (k_newmask_sweep)
   unsigned long long* tile_state = nullptr;  // [tiles_cap]
   dci::BatchScalars* scal = nullptr;
   int32_t* seeds_stage = nullptr;     // [max_batch] device copy for the host-seed variant
@@ -218,13 +219,17 @@ struct dci_workspace {
   unsigned char graph_sig[512] = {0};
   size_t graph_sig_len = 0;
   uint64_t graph_kernels[3] = {0, 0, 0};
-  // stage events; ev_mid / ev_done hand the gather to and from the shared gather stream
-  cudaEvent_t ev_mid = nullptr, ev_done = nullptr;
+  // stage events; ev_mid / ev_done hand the gather to and from the shared gather stream; ev_pre
+  // hands a split group gather its first phase (the rows of F_{L-1}) after hop L-2's scan
+  cudaEvent_t ev_mid = nullptr, ev_done = nullptr, ev_pre = nullptr;
   // stage timing (profiling on): a ring of event records, so timing never blocks the host on the
   // batch just issued; a record is folded into the totals when it is reused (or on stats)
   struct TimeRec {
-    cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};  // sample start/end, gather start/end
-    int32_t state = 0;  // bit 0: sampling times recorded, bit 1: gather launch times recorded
+    // sample start/end, gather start/end; a split group gather (two launches) also records the end
+    // of its first launch (e[4]) and the start of its second (e[5])
+    cudaEvent_t e[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int32_t state = 0;  // bit 0: sampling times recorded, bit 1: gather launch times recorded,
+                        // bit 2: the gather was split (two launches: e[2]..e[4] and e[5]..e[3])
     int32_t nb = 1;     // batches whose sampling the record covers (a group's sampling is one graph)
   };
   static constexpr int kTimeRing = 8;
@@ -241,7 +246,7 @@ struct dci_workspace {
     uint64_t kernels = 0, kernels2 = 0;
     uint64_t last_use = 0;
   };
-  GroupGraph gg[2];
+  GroupGraph gg[4];
   uint64_t gg_clock = 0;
   // the group's headers: a pinned ring of host blocks -> one copy into ghdr_dev per call
   static constexpr int kGroupHdrRing = 8;
@@ -312,6 +317,11 @@ struct HopParams {
 // per kernel; a single call is n = 1.
 void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
+// Between a multi-batch hop and its scan: when the hop sampled by node sweep (decided on the device),
+// find every batch's new candidates node-major (one coalesced tag probe per node and batch) instead of
+// one random tag read per candidate in the scan.  Launched only when the host-side conditions allow
+// a node sweep (n >= 2, 3 <= f <= 32, hop >= 1, dense tables).
+void launch_newmask_sweep(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s);
 // A group's headers: src = device staging block of n headers -> ws[i]->scal->hdr.
 void launch_scatter_headers(dci_ctx* ctx, dci_workspace* const* ws, const BatchHeader* src, int32_t n,
                             cudaStream_t s);
@@ -330,10 +340,13 @@ bool gather_many_uses_tma(const dci_ctx* ctx, const dci_batch_out* outs, int32_t
 // sweep: the group's frontiers may together cover the node set (sum of their bounds >= N), so the
 // node-sweep gather (each feature row read once for all batches) is used; else row mode.
 // alone: nothing is queued ahead of this gather (the bulk-copy sweep is then used, DCI_SWEEP_KIND=auto)
+// phase (node sweep only): 0 = all rows; a split gather is two launches, 1 = the rows of F_{L-1}
+// (enqueued after hop L-2's scan, beside hop L-1's sampling) and 2 = the rest (after hop L-1's scan)
 // *kind: 0 row mode, 1 register-copy node sweep, 2 bulk-copy node sweep (the kernel launched)
 dci_status launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n,
-                              int32_t L, dci_batch_result* stage, bool sweep, bool alone, cudaStream_t s,
-                              int* kind);
+                              int32_t L, dci_batch_result* stage, bool sweep, bool alone, int32_t phase,
+                              cudaStream_t s, int* kind);
+bool gather_split_enabled();  // env DCI_SPLIT_GATHER (default 0: measured no gain)
 bool gather_sweep_enabled();  // env DCI_SWEEP (default 1)
 // Gather blocks per SM: the HBM-bound gather is given a small share of each SM when many
 // batches are in flight (their sampling kernels must co-reside), the whole SM when one is.

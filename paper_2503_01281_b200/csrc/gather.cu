@@ -48,6 +48,21 @@ __device__ __forceinline__ int4 ld_stream_v4(const int4* p, uint64_t pol) {
   return r;
 }
 
+// Pinned-host (UVA) row reads on a miss: a plain (L1-allocating) load.  Random host-row reads with
+// L1::no_allocate loads stop at ~25.7 GB/s on this B200 whatever the row size, plain loads reach
+// ~49.7 GB/s (tools/probe/hostreq_probe.cu, profiles/hostreq_probe.jsonl); host rows are
+// read-only while kernels run, so L1 allocation is safe.
+__device__ __forceinline__ int4 ld_host_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// a feature row's 16-byte word from the HBM cache (hit) or from pinned host memory (miss)
+__device__ __forceinline__ int4 ld_row_v4(const int4* p, bool host, uint64_t pol) {
+  return host ? ld_host_v4(p) : ld_stream_v4(p, pol);
+}
+
 __device__ __forceinline__ void st_v4(int4* p, const int4& v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
@@ -144,7 +159,7 @@ __global__ void __launch_bounds__(256) k_gather(FusedArgs a) {
 #pragma unroll
           for (int j = 0; j < VPL; ++j) {
             const int idx = c0 + lane + 32 * j;
-            if (idx < row16) buf[j] = ld_stream_v4(s4 + idx, pol);
+            if (idx < row16) buf[j] = ld_row_v4(s4 + idx, slot < 0, pol);
           }
 #pragma unroll
           for (int j = 0; j < VPL; ++j) {
@@ -289,6 +304,10 @@ struct TmaBatch {
 struct TmaBatches {
   int32_t n;  // batches in this launch (<= kTmaMaxBatches)
   int32_t L;
+  // node sweep only: 0 = every row of F_L; split group gather: 1 = the rows of F_{L-1} (local ids
+  // < |F_{L-1}|, final once hop L-2's scan is done, so this launch runs beside hop L-1's sampling),
+  // 2 = the rest (ids >= |F_{L-1}|, after hop L-1's scan)
+  int32_t phase;
   int64_t N;
   const DirEntry* dir;
   const float* fcache;
@@ -310,6 +329,8 @@ struct TmaBatches {
 //  sweep: N x (8 B tag probe per batch + 4 B slot lookup) + |union| x 4D + sum_b |F_L(b)| x 4D
 __device__ __forceinline__ void group_epilogue(const TmaBatches& a, const unsigned (*s_cnt)[2], unsigned s_reads,
                                                unsigned s_host_rows, long long tot_rows, bool sweep) {
+  // (a split gather's first launch books its bytes and folds its feature counts into the
+  // scalars, but publishes nothing: the second launch publishes the batches' results)
   const int nb = a.n;
   if (threadIdx.x == 0 && s_reads) atomicAdd(&a.b[0].sc->launch_reads, (unsigned long long)s_reads);
   if (threadIdx.x == 0 && s_host_rows) atomicAdd(&a.b[0].sc->acc_host_rows, (unsigned long long)s_host_rows);
@@ -336,9 +357,10 @@ __device__ __forceinline__ void group_epilogue(const TmaBatches& a, const unsign
                                    : tot * (2ull * rowb + 4ull);
     sc0->launch_reads = 0;
     sc0->sweep_ticket = 0;
+    if (a.phase == 1) sc0->done = 0;
   }
   __syncthreads();
-  if (s_last && threadIdx.x < nb) {
+  if (s_last && a.phase != 1 && threadIdx.x < nb) {
     __threadfence();
     const TmaBatch& tb = a.b[threadIdx.x];
     BatchScalars* sc = tb.sc;
@@ -389,6 +411,34 @@ __device__ __forceinline__ void group_epilogue(const TmaBatches& a, const unsign
 constexpr int kSweepWarps = 8;
 constexpr int kSweepMax = DCI_MAX_GROUP;  // 32-bit presence masks
 
+// Per-launch batch table of a node sweep (shared memory): each batch's epoch and the local-id range
+// [lo, hi) this launch writes (phase 0: all of F_L; split gather: 1 = F_{L-1}, 2 = the rest), and the
+// rows the launch writes in all (for its algorithmic bytes).  |F_{L-1}| is final once hop L-2's
+// scan has run: the hop L-1 sampling running beside a phase-1 launch only raises the tags of nodes
+// outside F_{L-1} (candidate positions >= |F_{L-1}|), and its scan gives new nodes ids >= |F_{L-1}|.
+// Ends with a block barrier.
+__device__ __forceinline__ void sweep_init(const TmaBatches& a, uint32_t* s_ep, uint32_t* s_lo, uint32_t* s_hi,
+                                           long long* s_tot) {
+  const int nb = a.n;
+  if (threadIdx.x < nb) {
+    const BatchScalars* sc = a.b[threadIdx.x].sc;
+    s_ep[threadIdx.x] = __ldcg(&sc->hdr.epoch);
+    const uint32_t nprev = a.L >= 2 ? (uint32_t)__ldcg(&sc->sizes[a.L - 1]) : (uint32_t)__ldcg(&sc->hdr.B);
+    s_lo[threadIdx.x] = a.phase == 2 ? nprev : 0u;
+    s_hi[threadIdx.x] = a.phase == 1 ? nprev : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int i = 0; i < nb; ++i) {
+      const long long nl = a.phase == 1 ? 0 : __ldcg(&a.b[i].sc->sizes[a.L]);
+      acc += a.phase == 0 ? nl : a.phase == 1 ? (long long)s_hi[i] : nl - (long long)s_lo[i];
+    }
+    *s_tot = acc;
+  }
+  __syncthreads();
+}
+
 // X row address of node j (lane index in the warp's group) in batch b
 __device__ __forceinline__ int4* sweep_dst(const TmaBatches& a, const int* rt, int b, int j) {
   const TmaBatch& tb = a.b[b];
@@ -428,16 +478,16 @@ __device__ __forceinline__ void sweep_store(const TmaBatches& a, const int* rt, 
 // Two nodes (rows s1 -> mask m1, s2 -> m2; s2 may be null): both rows' loads are issued before
 // any store.
 template <int VPL>
-__device__ __forceinline__ void sweep_copy(const TmaBatches& a, const int* rt, int row16, const char* s1,
-                                           unsigned m1, int j1, const char* s2, unsigned m2, int j2, int lane,
-                                           int out16max, uint64_t pol) {
+__device__ __forceinline__ void sweep_copy(const TmaBatches& a, const int* rt, int row16, const char* s1, bool h1,
+                                           unsigned m1, int j1, const char* s2, bool h2, unsigned m2, int j2,
+                                           int lane, int out16max, uint64_t pol) {
   for (int c0 = 0; c0 < out16max; c0 += 32 * VPL) {
     int4 b1[VPL], b2[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int idx = c0 + lane + 32 * k;
-      b1[k] = idx < row16 ? ld_stream_v4(reinterpret_cast<const int4*>(s1) + idx, pol) : make_int4(0, 0, 0, 0);
-      b2[k] = (s2 && idx < row16) ? ld_stream_v4(reinterpret_cast<const int4*>(s2) + idx, pol)
+      b1[k] = idx < row16 ? ld_row_v4(reinterpret_cast<const int4*>(s1) + idx, h1, pol) : make_int4(0, 0, 0, 0);
+      b2[k] = (s2 && idx < row16) ? ld_row_v4(reinterpret_cast<const int4*>(s2) + idx, h2, pol)
                                   : make_int4(0, 0, 0, 0);
     }
     sweep_store<VPL>(a, rt, j1, m1, b1, c0, lane, pol);
@@ -464,19 +514,17 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
   // while the current group copies), slot stage [32] i32, row table [nb][32] i32
   extern __shared__ __align__(128) unsigned char s_dyn[];
   __shared__ uint32_t s_ep[kSweepMax];
+  __shared__ uint32_t s_lo[kSweepMax], s_hi[kSweepMax];  // local-id range this launch writes
   __shared__ unsigned s_cnt[kSweepMax][2];
   __shared__ unsigned s_reads, s_host;
   __shared__ long long s_tot;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nb = a.n;
-  if (threadIdx.x < nb) s_ep[threadIdx.x] = __ldcg(&a.b[threadIdx.x].sc->hdr.epoch);
   if (threadIdx.x < 2 * kSweepMax) (&s_cnt[0][0])[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
     s_reads = 0u;
     s_host = 0u;
-    long long acc = 0;
-    for (int i = 0; i < nb; ++i) acc += __ldcg(&a.b[i].sc->sizes[a.L]);
-    s_tot = acc;
   }
+  sweep_init(a, s_ep, s_lo, s_hi, &s_tot);
   __syncthreads();
   unsigned char* mine = s_dyn + (size_t)wib * (nb * 32 * 12 + 128);
   unsigned long long* stag = reinterpret_cast<unsigned long long*>(mine);  // [nb][32]
@@ -515,9 +563,10 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
     unsigned mask = 0;
     for (int b = 0; b < nb; ++b) {
       const unsigned long long tg = stag[b * 32 + lane];
-      if ((uint32_t)(tg >> 32) == s_ep[b]) {
+      const uint32_t row = 0xFFFFFFFFu - (uint32_t)tg;
+      if ((uint32_t)(tg >> 32) == s_ep[b] && row >= s_lo[b] && row < s_hi[b]) {
         mask |= 1u << b;
-        rt[b * 32 + lane] = (int)(0xFFFFFFFFu - (uint32_t)tg);
+        rt[b * 32 + lane] = (int)row;
       }
     }
     __syncwarp();  // the stage is consumed: the next group's probes may overwrite it
@@ -556,7 +605,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_gather_sweep(const __grid_
       const unsigned m1 = __shfl_sync(0xffffffffu, mask, j1);
       const char* s2 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), j2));
       const unsigned m2 = __shfl_sync(0xffffffffu, mask, j2);
-      sweep_copy<VPL>(a, rt, row16, s1, m1, j1, two ? s2 : nullptr, two ? m2 : 0u, j2, lane, out16max, pol);
+      const bool h1 = (hitm >> j1 & 1u) == 0, h2 = (hitm >> j2 & 1u) == 0;  // host rows (misses)
+      sweep_copy<VPL>(a, rt, row16, s1, h1, m1, j1, two ? s2 : nullptr, h2, two ? m2 : 0u, j2, lane, out16max, pol);
     }
     __syncwarp();  // every lane is done with the row table before the next group rewrites it
     g = g_next;
@@ -602,20 +652,18 @@ __global__ void __launch_bounds__(32 * kSweepTmaMaxWarps) k_gather_sweep_tma(con
   extern __shared__ __align__(128) unsigned char s_dyn[];
   __shared__ __align__(8) unsigned long long s_bar[kSweepTmaMaxWarps][kSweepTmaMaxSlots];
   __shared__ uint32_t s_ep[kSweepMax];
+  __shared__ uint32_t s_lo[kSweepMax], s_hi[kSweepMax];  // local-id range this launch writes
   __shared__ unsigned s_cnt[kSweepMax][2];
   __shared__ unsigned s_reads, s_host;
   __shared__ long long s_tot;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nb = a.n;
   const int K = t.K;
-  if (threadIdx.x < nb) s_ep[threadIdx.x] = __ldcg(&a.b[threadIdx.x].sc->hdr.epoch);
   if (threadIdx.x < 2 * kSweepMax) (&s_cnt[0][0])[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
     s_reads = 0u;
     s_host = 0u;
-    long long acc = 0;
-    for (int i = 0; i < nb; ++i) acc += __ldcg(&a.b[i].sc->sizes[a.L]);
-    s_tot = acc;
   }
+  sweep_init(a, s_ep, s_lo, s_hi, &s_tot);
   // per warp: ring [K][slot_bytes] | tag stage [nb][32] u64 | slot stage [32] i32 | row table
   // [nb][32] i32 | slot metadata [K][1 + nb] i32 (mask, destination rows)
   unsigned char* mine = s_dyn + (size_t)wib * t.warp_bytes;
@@ -671,9 +719,10 @@ __global__ void __launch_bounds__(32 * kSweepTmaMaxWarps) k_gather_sweep_tma(con
     mask = 0;
     for (int b = 0; b < nb; ++b) {
       const unsigned long long tg = stag[b * 32 + lane];
-      if ((uint32_t)(tg >> 32) == s_ep[b]) {
+      const uint32_t row = 0xFFFFFFFFu - (uint32_t)tg;
+      if ((uint32_t)(tg >> 32) == s_ep[b] && row >= s_lo[b] && row < s_hi[b]) {
         mask |= 1u << b;
-        rt[b * 32 + lane] = (int)(0xFFFFFFFFu - (uint32_t)tg);
+        rt[b * 32 + lane] = (int)row;
       }
     }
     __syncwarp();
@@ -1124,11 +1173,18 @@ bool gather_sweep_enabled() {
   return sweep != 0;
 }
 
+bool gather_split_enabled() {
+  static const int split = env_int("DCI_SPLIT_GATHER", 0);
+  return split != 0;
+}
+
 dci_status launch_gather_many(dci_ctx* ctx, dci_workspace* const* ws, const dci_batch_out* outs, int32_t n,
-                              int32_t L, dci_batch_result* stage, bool sweep, bool alone, cudaStream_t s,
-                              int* kind) {
+                              int32_t L, dci_batch_result* stage, bool sweep, bool alone, int32_t phase,
+                              cudaStream_t s, int* kind) {
   TmaBatches tb = tma_batches(ctx, L);
   tb.stage = stage;
+  tb.phase = sweep ? phase : 0;
+  if (phase != 0 && !(sweep && n >= 2 && n <= kSweepMax)) return fail(DCI_EINVAL, "split gather needs a node sweep");
   for (int i = 0; i < n; ++i) tma_add(&tb, ctx, ws[i], outs + i, nullptr);
   if (sweep && n >= 2 && n <= kSweepMax) return sweep_launch(ctx, tb, alone, s, kind);
   *kind = 0;

@@ -27,10 +27,12 @@ __device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned 
 }
 
 // Host-mapped (UVA) neighbour read: a plain global load that the GPU turns into a PCIe
-// read request.
+// read request.  L1-allocating: random host reads through L1::no_allocate loads
+// run at up to ~1.75x lower rates on this B200 (tools/probe/hostreq_probe.cu: 64 B requests 11.2
+// vs 19.4 GB/s, 128 B 23 vs 42 GB/s); the host CSC is read-only while kernels run.
 __device__ __forceinline__ int32_t ld_host_i32(const int32_t* p) {
   int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 
@@ -66,6 +68,7 @@ struct HopBatch {
   int32_t* prev_bsrc;
   int32_t* bptr;                   // this hop's block row pointers (written by the scan)
   unsigned long long* pos_of;      // the workspace's node -> position tag table (dense or hashed)
+  uint32_t* nmask;                 // [n_h] new-candidate slot masks of a node-sweep hop
   uint32_t hmask;                  // 0: dense table; else hashed capacity - 1 (pt_insert / pt_find)
   BatchScalars* sc;
   unsigned long long* tiles;       // this hop's scan tile state
@@ -84,6 +87,7 @@ struct HopLaunch {
   int32_t* edge_counts; // presample only (nullable, n = 1)
   int32_t precheck;     // read the tag before the atomicMax (DCI_PRECHECK=1; measured slower on M2)
   int32_t sweep;        // node-sweep sampling allowed (multi-batch hops covering >= N nodes)
+  int32_t nmask_on;     // a sweeping hop's new-candidate masks come from k_newmask_sweep (DCI_NMASK_SWEEP)
   HopBatch b[DCI_MAX_GROUP];
 };
 
@@ -107,7 +111,7 @@ struct HopShared {
   unsigned long long seed[DCI_MAX_GROUP];
   const int32_t* Fin[DCI_MAX_GROUP];
   unsigned cnt[DCI_MAX_GROUP][2];     // adjacency hits / misses of this block, per batch
-  unsigned host_lines;                // distinct 128-byte host lines its adjacency misses read
+  unsigned host_sectors;              // distinct 32-byte host sectors its adjacency misses read
   int all_ok;                         // no batch has a seed error (status set by hop 0)
 };
 
@@ -137,18 +141,19 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
     S.all_ok = ok;
   }
   if (threadIdx.x < 2 * DCI_MAX_GROUP) (&S.cnt[0][0])[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) S.host_lines = 0u;
+  if (threadIdx.x == 0) S.host_sectors = 0u;
   __syncthreads();
 }
 
-// Host-link requests of the adjacency miss path (bench roofline): a sampled element
-// that misses is a 4-byte zero-copy read of pinned host memory; misses of one (dst, hop) that fall
-// in the same 128-byte line are served together.  Ranks are sorted within a G-lane group, so the
-// misses are its last lanes in address order: a miss lane opens a new line unless the lane before
-// it missed in the same line.  Returns the lines the warp's groups open (warp-uniform).
+// Host-link traffic of the adjacency miss path (bench roofline): a sampled element
+// that misses is a 4-byte zero-copy read of pinned host memory, and the GPU fetches system memory
+// in 32-byte sectors, so misses of one (dst, hop) that fall in the same sector are served together.
+// Ranks are sorted within a G-lane group, so the misses are its last lanes in address order: a miss
+// lane opens a new sector unless the lane before it missed in the same sector.  Returns the
+// sectors the warp's groups open (warp-uniform).
 template <int G>
-__device__ __forceinline__ unsigned host_lines_opened(bool miss, int64_t elem, int gl) {
-  const long long line = elem >> 5;  // 32 int32 per 128-byte line
+__device__ __forceinline__ unsigned host_sectors_opened(bool miss, int64_t elem, int gl) {
+  const long long line = elem >> 3;  // 8 int32 per 32-byte sector
   const long long pl = __shfl_up_sync(0xffffffffu, line, 1, G);
   const bool pmiss = __shfl_up_sync(0xffffffffu, (int)miss, 1, G) != 0;
   return __popc(__ballot_sync(0xffffffffu, miss && (gl == 0 || !pmiss || pl != line)));
@@ -168,7 +173,7 @@ __device__ __forceinline__ void hop_shared_flush(const HopLaunch& a, HopShared& 
     if (S.cnt[threadIdx.x][0]) atomicAdd(&sc->counters[0], (unsigned long long)S.cnt[threadIdx.x][0]);
     if (S.cnt[threadIdx.x][1]) atomicAdd(&sc->counters[1], (unsigned long long)S.cnt[threadIdx.x][1]);
   }
-  if (threadIdx.x == 0 && S.host_lines) atomicAdd(&a.b[0].sc->acc_host_lines, (unsigned long long)S.host_lines);
+  if (threadIdx.x == 0 && S.host_sectors) atomicAdd(&a.b[0].sc->acc_host_sectors, (unsigned long long)S.host_sectors);
 }
 
 // Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
@@ -286,6 +291,14 @@ __device__ __forceinline__ int32_t select_rank(int gl, int lane, unsigned gmask,
   return rank;
 }
 
+// Whether a hop samples by node sweep (decided on the device: the frontier sizes are device data).
+// k_sample_hop, k_newmask_sweep and k_scan_hop take the same decision from the same inputs (for
+// h >= 1 the batches' status words and frontier sizes no longer change within the hop).
+__device__ __forceinline__ bool hop_sweeps(const HopLaunch& a, long long total, int all_ok) {
+  return a.f >= 3 && a.f <= 32 && a.hop >= 1 && all_ok && a.sweep && a.n >= 2 && total >= a.N &&
+         a.edge_counts == nullptr;
+}
+
 // ------------------------------------------------------------------------------------
 // Node-sweep sampling of a multi-batch hop (2+ batches whose frontiers together hold >= N nodes):
 // the draws of (node v, hop h) do not depend on the batch (C4), so each node is sampled ONCE
@@ -324,6 +337,9 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
     }
   };
   unsigned long long tc[CH], tn[CH];
+  unsigned acc_h[CH], acc_m[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc_h[c] = acc_m[c] = 0u;
   int4 e0, e1, e0n, e1n;
   probe(warp_id * GPW, tc, e0, e1);
   for (int64_t vbase = warp_id * GPW; vbase < a.N; vbase += vstride) {
@@ -365,33 +381,58 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       hit = rank < cached_len;
       x = hit ? ld_keep_i32(a.acache + cache_off + rank, epol) : ld_host_i32(a.uidx + host_off + rank);
     }
-    {  // read once for every batch holding v: its host lines count once
-      const unsigned nl = host_lines_opened<G>(valid && !hit, host_off + rank, gl);
-      if (lane == 0 && nl) atomicAdd(&S.host_lines, nl);
+    {  // read once for every batch holding v: its host sectors count once
+      const unsigned nl = host_sectors_opened<G>(valid && !hit, host_off + rank, gl);
+      if (lane == 0 && nl) atomicAdd(&S.host_sectors, nl);
     }
-    // write the sample into every batch holding v (local id shuffled from the probing lane)
+    // v's hits / misses, counted once per node and added to every batch holding v: lane gl keeps
+    // the running counts of batches gl, gl + G, ... in registers (no per-sample shared atomics)
+    {
+      const unsigned vm = __ballot_sync(0xffffffffu, valid) & gmask;
+      const unsigned hm = __ballot_sync(0xffffffffu, valid && hit) & gmask;
+      const unsigned nh = __popc(hm), nm = __popc(vm) - nh;
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if (c * G >= n) break;
-      for (int r = 0; r < G && c * G + r < n; ++r) {
-        const int bb = c * G + r;
-        const uint32_t d = __shfl_sync(0xffffffffu, dd[c], gbase + r);
-        if (!((pm >> bb) & 1u)) continue;
-        const HopBatch& hb = a.b[bb];
-        if (gl < f) hb.cand[(int64_t)d * f + gl] = x;
-        if (gl == 0) hb.kcnt[d] = k;
-        if (valid) {
-          const uint32_t n_h = (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
-          const unsigned long long tag = S.ehi[bb] | (0xFFFFFFFFu - (n_h + d * (uint32_t)f + (uint32_t)gl));
-          if (!a.precheck || __ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
-          atomicAdd(&S.cnt[bb][hit ? 0 : 1], 1u);
+      for (int c = 0; c < CH; ++c)
+        if ((pm >> (c * G + gl)) & 1u) {
+          acc_h[c] += nh;
+          acc_m[c] += nm;
         }
+    }
+    // write the sample into every batch holding v (local id shuffled from the probing lane); the
+    // loop runs over the batches holding ANY of the warp's nodes, not over all n
+    for (unsigned um = __reduce_or_sync(0xffffffffu, pm); um; um &= um - 1) {
+      const int bb = __ffs(um) - 1;
+      const int cb = bb / G;
+      uint32_t dsel = dd[0];
+#pragma unroll
+      for (int c = 1; c < CH; ++c)
+        if (cb == c) dsel = dd[c];
+      const uint32_t d = __shfl_sync(0xffffffffu, dsel, gbase + (bb & (G - 1)));
+      if (!((pm >> bb) & 1u)) continue;
+      const HopBatch& hb = a.b[bb];
+      if (gl < f) hb.cand[(int64_t)d * f + gl] = x;
+      if (gl == 0) {
+        hb.kcnt[d] = k;
+        hb.nmask[d] = 0u;  // filled by k_newmask_sweep
+      }
+      if (valid) {
+        const uint32_t n_h = (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
+        const unsigned long long tag = S.ehi[bb] | (0xFFFFFFFFu - (n_h + d * (uint32_t)f + (uint32_t)gl));
+        if (!a.precheck || __ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
       }
     }
 #pragma unroll
     for (int c = 0; c < CH; ++c) tc[c] = tn[c];
     e0 = e0n;
     e1 = e1n;
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int bb = c * G + gl;
+    if (bb < n) {
+      if (acc_h[c]) atomicAdd(&S.cnt[bb][0], acc_h[c]);
+      if (acc_m[c]) atomicAdd(&S.cnt[bb][1], acc_m[c]);
+    }
   }
 }
 
@@ -436,7 +477,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   // not final until the kernel ends; from hop 1 on, F_h's tags were finalised by the last scan)
   // (and not when a batch has a seed error: a bad or repeated seed has no table slot of its own,
   // so the sweep would leave its candidate slots unwritten; frontier order fills them)
-  if (G >= 4 && h >= 1 && S.all_ok && a.sweep && a.n >= 2 && total >= a.N && a.edge_counts == nullptr) {
+  if (G >= 4 && hop_sweeps(a, total, S.all_ok)) {
     sample_sweep<(G >= 4 ? G : 4)>(a, S, warp_id, nwarps, keep, epol);
     hop_shared_flush(a, S);
     return;
@@ -488,17 +529,24 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     const int pos = gl;
     const bool valid = active && gl < k;
     {
-      const unsigned nl = host_lines_opened<G>(valid && rank >= cached_len, host_off + rank, gl);
-      if (lane == 0 && nl) atomicAdd(&S.host_lines, nl);
+      const unsigned nl = host_sectors_opened<G>(valid && rank >= cached_len, host_off + rank, gl);
+      if (lane == 0 && nl) atomicAdd(&S.host_sectors, nl);
     }
     int32_t x = -1;
+    const bool hit = valid && rank < cached_len;
     if (valid) {
-      const bool hit = rank < cached_len;
       if (hit)
         x = ld_keep_i32(a.acache + cache_off + rank, epol);
       else
         x = ld_host_i32(a.uidx + host_off + rank);
-      atomicAdd(&S.cnt[b][hit ? 0 : 1], 1u);
+    }
+    {  // the group's hits / misses in one pair of shared atomics (its dst belongs to one batch)
+      const unsigned vm = __ballot_sync(0xffffffffu, valid) & gmask;
+      const unsigned hm = __ballot_sync(0xffffffffu, hit) & gmask;
+      if (gl == 0 && vm) {
+        if (hm) atomicAdd(&S.cnt[b][0], (unsigned)__popc(hm));
+        if (vm != hm) atomicAdd(&S.cnt[b][1], (unsigned)__popc(vm & ~hm));
+      }
     }
     if (active && gl < f) hb.cand[d * f + (valid ? pos : gl)] = x;
     if (active && gl == 0) hb.kcnt[d] = k;
@@ -600,15 +648,15 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
         }
       }
     }
-    // element reads in sorted-rank order: pos -> rank (all lanes run every pass: the host-line
-    // count shuffles across the warp, carrying the previous pass's last miss line)
+    // element reads in sorted-rank order: pos -> rank (all lanes run every pass: the host-sector
+    // count shuffles across the warp, carrying the previous pass's last miss sector)
     long long carry_line = -1;
     for (int base = 0; base < f; base += 32) {
       const int pos = base + lane;
       {
         const int32_t rk = pos < k ? (deg > f ? chosen[pos] : pos) : 0;
         const bool miss = pos < k && rk >= cached_len;
-        const long long line = (host_off + rk) >> 5;
+        const long long line = (host_off + rk) >> 3;  // 32-byte sector
         long long pl = __shfl_up_sync(0xffffffffu, line, 1);
         bool pmiss = __shfl_up_sync(0xffffffffu, (int)miss, 1) != 0;
         if (lane == 0) {
@@ -619,7 +667,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
         const unsigned missm = __ballot_sync(0xffffffffu, miss);
         const long long last = __shfl_sync(0xffffffffu, line, 31);
         carry_line = (missm >> 31) & 1u ? last : -1;
-        if (lane == 0 && opened) atomicAdd(&S.host_lines, (unsigned)__popc(opened));
+        if (lane == 0 && opened) atomicAdd(&S.host_sectors, (unsigned)__popc(opened));
       }
       if (pos >= f) continue;
       int32_t x = -1;
@@ -667,6 +715,42 @@ __global__ void __launch_bounds__(256) k_hop_epilogue(const __grid_constant__ Ho
 }
 
 // ------------------------------------------------------------------------------------
+// k_newmask_sweep: the new-candidate masks of a node-sweep hop, node-major.  After the hop's
+// atomicMax insertions, a node v is NEW in batch b iff its tag carries b's epoch and a position
+// p >= n_h (a candidate position of this hop: F_h's own entries hold final ids < n_h), and p is its
+// FIRST occurrence, i.e. the candidate (d, s) = ((p - n_h) / f, (p - n_h) % f) that owns it -- the
+// same test the scan otherwise makes per candidate (tag == own position).  Sweeping node ids reads
+// every table once, coalesced (N x n x 8 B), instead of one random tag read per candidate
+// (sum_b |F_h(b)| x f: 12 M per group of 20 on M2's last hop), and sets bit s of nmask_b[d].
+// The sampler zeroed nmask_b[d] for every dst it wrote.  Exits at once unless the hop swept.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_newmask_sweep(const __grid_constant__ HopLaunch a) {
+  __shared__ HopShared S;
+  hop_shared_init(a, S);
+  if (!a.nmask_on || !hop_sweeps(a, S.pre[a.n], S.all_ok)) return;
+  const int n = a.n, f = a.f;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = tid; v < a.N; v += nthreads) {
+    for (int b0 = 0; b0 < n; b0 += 8) {
+      unsigned long long t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = b0 + u < n ? __ldcg(a.b[b0 + u].pos_of + v) : 0ull;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + u;
+        if (b >= n || (t[u] >> 32) != (S.ehi[b] >> 32)) continue;
+        const uint32_t p = 0xFFFFFFFFu - (uint32_t)t[u];
+        const uint32_t n_h = (uint32_t)(S.pre[b + 1] - S.pre[b]);
+        if (p < n_h) continue;
+        const uint32_t q = p - n_h;
+        atomicOr(a.b[b].nmask + q / (uint32_t)f, 1u << (q % (uint32_t)f));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // k_scan_hop: one thread per dst of F_h, kScanTile dsts per tile, tiles taken by dynamic
 // tickets (in-order => deadlock-free look-back); a multi-batch launch numbers the tiles of all its
 // batches consecutively (one ticket counter) and each batch's tiles look back only within it.
@@ -692,8 +776,11 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
   __shared__ uint32_t s_ticket;
   __shared__ unsigned long long s_warp[kScanTile / 32];
   __shared__ unsigned long long s_prefix;
+  __shared__ int s_nmask;  // the hop swept: new-candidate masks come from k_newmask_sweep
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
+    int ok = 1;
+    for (int b = 0; b < n; ++b) ok &= __ldcg(&a.b[b].sc->status) == 0;
     long long acc = 0, tacc = 0;
     for (int b = 0; b < n; ++b) {
       const BatchScalars* sc = a.b[b].sc;
@@ -706,8 +793,10 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
     }
     s_pre[n] = acc;
     s_tpre[n] = tacc;
+    s_nmask = a.nmask_on && hop_sweeps(a, acc, ok) ? 1 : 0;
   }
   __syncthreads();
+  const bool use_nmask = s_nmask != 0;
   // empty batches: no tiles; their block CSR and size are written here
   if (blockIdx.x == 0 && threadIdx.x < n && s_pre[threadIdx.x + 1] == s_pre[threadIdx.x]) {
     a.b[threadIdx.x].bptr[0] = 0;
@@ -728,7 +817,10 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
     const unsigned long long ehi = s_ehi[b];
     const int64_t d = tile * kScanTile + threadIdx.x;
     uint32_t k = 0, newmask = 0, nwide = 0;
-    if (d < n_h) {
+    if (d < n_h && use_nmask) {  // (f <= 32, h >= 1)
+      k = (uint32_t)hb.kcnt[d];
+      newmask = hb.nmask[d];
+    } else if (d < n_h) {
       k = (uint32_t)hb.kcnt[d];
       const int32_t* c = hb.cand + d * f;
       const uint32_t base = (uint32_t)(n_h + d * f);
@@ -876,6 +968,11 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
   a.sweep = sweep;
   for (int i = 0; i < n; ++i)
     if (ws[i]->hmask) a.sweep = 0;  // the node sweep probes every node id: dense tables only
+  static const int nmask_on = [] {
+    const char* e = getenv("DCI_NMASK_SWEEP");
+    return e ? atoi(e) : 1;
+  }();
+  a.nmask_on = nmask_on;
   for (int i = 0; i < n; ++i) {
     HopBatch& b = a.b[i];
     const int h = p[i].hop;
@@ -888,6 +985,7 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
     b.prev_bsrc = p[i].prev_bsrc;
     b.bptr = p[i].bptr;
     b.pos_of = ws[i]->pos_of;
+    b.nmask = ws[i]->nmask;
     b.hmask = ws[i]->hmask;
     b.sc = ws[i]->scal;
     b.tiles = h < ws[i]->L ? ws[i]->tile_state + ws[i]->tile_off[h] : nullptr;
@@ -955,6 +1053,15 @@ void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p,
   int64_t grid = persistent_grid(ctx, k_scan_hop, kScanTile, 8);
   if (tiles < grid) grid = tiles > 0 ? tiles : 1;
   k_scan_hop<<<(unsigned)grid, kScanTile, 0, s>>>(a);
+  ++ctx->launches;
+}
+
+void launch_newmask_sweep(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
+  const HopLaunch a = hop_launch(ctx, ws, p, n);
+  if (!(a.nmask_on && n >= 2 && a.f >= 3 && a.f <= 32 && a.hop >= 1 && a.sweep && a.edge_counts == nullptr))
+    return;
+  const int64_t grid = std::min<int64_t>(persistent_grid(ctx, k_newmask_sweep, 256, 8), (ctx->N + 255) / 256);
+  k_newmask_sweep<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, s>>>(a);
   ++ctx->launches;
 }
 

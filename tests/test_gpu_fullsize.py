@@ -154,13 +154,17 @@ def test_workspace_stats_and_graph_recapture():
                                  {"DCI_TMA_SMS": "37"}, {"DCI_PHASED": "2"}, {"DCI_PHASED": "2", "DCI_GRAPH": "0"},
                                  {"DCI_TABLE": "hash"}, {"DCI_TABLE": "hash", "DCI_GRAPH": "0"},
                                  {"DCI_SWEEP_KIND": "tma"}, {"DCI_SWEEP_KIND": "tma", "DCI_SWEEP_WARPS": "2"},
-                                 {"DCI_SWEEP_BPS": "1", "DCI_SWEEP_SMS": "20"}])
+                                 {"DCI_SWEEP_BPS": "1", "DCI_SWEEP_SMS": "20"}, {"DCI_SPLIT_GATHER": "0"},
+                                 {"DCI_SPLIT_GATHER": "1", "DCI_GRAPH": "0"}, {"DCI_SPLIT_GATHER": "1", "DCI_PHASED": "2"},
+                                 {"DCI_SPLIT_GATHER": "1", "DCI_SWEEP_KIND": "ldg"}, {"DCI_NMASK_SWEEP": "0"}])
 def test_gather_variants_subprocess(env):
     """Process-wide switches (read once per process): the TMA gather for single-batch
     calls, row mode for groups, group gathers on the caller's stream, a small TMA ring, phased
     (not overlapped) groups, frontier-order sampling only, the tag pre-read before atomicMax, one
     sampling block per SM, a gather grid on a quarter of the SMs, the split schedule (graphs and
-    direct launches), hashed position tables, the bulk-copy node sweep, a small sweep grid."""
+    direct launches), hashed position tables, the bulk-copy node sweep, a small sweep grid, and the
+    split group gather (off; without graphs; with the split schedule; register-copy sweeps), and the
+    scan's per-candidate tag reads instead of the node-major new-candidate masks."""
     r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=ROOT,
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

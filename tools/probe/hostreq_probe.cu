@@ -1,0 +1,200 @@
+// Probe: the host link's random-read REQUEST rate (zero-copy UVA reads of pinned host memory) by
+// access size and by pinned-region size, with enough reads in flight to saturate the link.
+// Round 1's uva_rand4 probe kept one 4-byte read in flight per thread and measured 94 M reads/s;
+// the sampler's adjacency misses reach far more (ncu: ~0.5 G sysmem requests/s on M4s's last hop),
+// so that figure was a latency bound, not the link's.  Here every thread (S <= 32) or every group
+// of S/16 lanes (S >= 64) keeps U = 8 independent reads in flight.
+//
+//   hostreq_probe [max_region_GB=64] > profiles/hostreq_probe.jsonl
+//
+// Every request of a launch goes to a DISTINCT S-byte slot (a bijective hash of its index over the
+// power-of-two slot count, with at most half the slots touched), so no read is served by L2, and
+// loads are the library's miss-path loads (ld.global.nc.L1::no_allocate).
+// Output: one JSON line per (region, size): Mreq_per_s and payload GB/s (req x size / time).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include <algorithm>
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e = (x);                                                                  \
+    if (e != cudaSuccess) {                                                               \
+      fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+      exit(1);                                                                            \
+    }                                                                                     \
+  } while (0)
+
+// bijection of [0, 2^bits): odd multiplies and xorshifts, masked
+__device__ __forceinline__ uint64_t perm(uint64_t x, int bits) {
+  const uint64_t m = (bits >= 64) ? ~0ull : ((1ull << bits) - 1);
+  x = (x * 0x9E3779B97F4A7C15ull) & m;
+  x ^= x >> (bits / 2 + 1);
+  x = (x * 0xBF58476D1CE4E5B9ull) & m;
+  x ^= x >> (bits / 2 + 1);
+  return x & m;
+}
+
+// load kinds: 0 = ld.global.nc.L1::no_allocate (round 1's miss-path load), 1 = plain ld.global
+// (L1-allocating; the library's miss-path load since round 2), 2 = ld.global.L1::no_allocate
+// (coherent), 3 = ld.global.nc (read-only path, L1-allocating)
+__device__ int g_kind_dummy;
+template <int KIND>
+__device__ __forceinline__ int ld32(const int* p) {
+  int v;
+  if (KIND == 0)
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  else if (KIND == 1)
+    asm volatile("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  else if (KIND == 3)
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+template <int KIND>
+__device__ __forceinline__ int4 ld128(const int4* p) {
+  int4 v;
+  if (KIND == 0)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else if (KIND == 1)
+    asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else if (KIND == 3)
+    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+// S-byte random reads (S in {4, 16, 32}), one thread per read, U reads in flight per thread
+template <int S, int U, int KIND>
+__global__ void rand_small(const char* __restrict__ src, int bits, int iters, int* sink) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  int acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    int v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t slot = perm(((uint64_t)(it * U + u)) * nthr + t, bits);
+      const char* p = src + slot * S;
+      if (S == 4) {
+        v[u] = ld32<KIND>(reinterpret_cast<const int*>(p));
+      } else if (S == 16) {
+        const int4 x = ld128<KIND>(reinterpret_cast<const int4*>(p));
+        v[u] = x.x ^ x.w;
+      } else {  // 32: two 16-byte halves of one sector
+        const int4 x = ld128<KIND>(reinterpret_cast<const int4*>(p));
+        const int4 y = ld128<KIND>(reinterpret_cast<const int4*>(p) + 1);
+        v[u] = x.x ^ y.w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u];
+  }
+  if (acc == 0x12345678) sink[0] = acc;
+}
+
+// S-byte random reads (S >= 64, multiple of 16) by groups of L = min(32, S/16) lanes, each lane
+// reading S/(16 L) int4 of the request; U requests in flight per group
+template <int S, int U, int KIND>
+__global__ void rand_wide(const char* __restrict__ src, int bits, int iters, int* sink) {
+  constexpr int L = (S / 16) < 32 ? (S / 16) : 32;
+  constexpr int PER = S / 16 / L;
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t ngrp = (uint64_t)gridDim.x * blockDim.x / L;
+  const uint64_t grp = t / L;
+  const int gl = (int)(t % L);
+  int acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    int v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t slot = perm(((uint64_t)(it * U + u)) * ngrp + grp, bits);
+      const int4* p = reinterpret_cast<const int4*>(src + slot * S) + gl;
+      v[u] = 0;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int4 x = ld128<KIND>(p + k * L);
+        v[u] ^= x.x ^ x.w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u];
+  }
+  if (acc == 0x12345678) sink[0] = acc;
+}
+
+template <int S, int KIND>
+static double run(const char* src, size_t region, int* sink, int sms, double* mreq) {
+  int bits = 0;
+  while ((2ull << bits) <= region / S) ++bits;  // 2^bits slots of S bytes
+  const int threads = 256;
+  const int grid = sms * 8;
+  constexpr int U = 8;
+  const int per_group = S <= 32 ? 1 : ((S / 16) < 32 ? (S / 16) : 32);
+  const double per_iter = (double)grid * threads / per_group * U;
+  // at most half of the slots and ~16 M requests per launch
+  int iters = (int)std::min(16.0, std::max(1.0, std::min((double)(1ull << bits) / 2, 16.0e6) / per_iter));
+  const double nreq = per_iter * iters;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  auto launch = [&]() {
+    if constexpr (S <= 32)
+      rand_small<S, U, KIND><<<grid, threads>>>(src, bits, iters, sink);
+    else
+      rand_wide<S, U, KIND><<<grid, threads>>>(src, bits, iters, sink);
+  };
+  launch();  // warm-up (page-table walks of a fresh region)
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    CK(cudaEventRecord(a));
+    launch();
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (ms < best) best = ms;
+  }
+  CK(cudaGetLastError());
+  *mreq = nreq / best / 1e3;
+  return nreq * S / best / 1e6;  // payload GB/s
+}
+
+int main(int argc, char** argv) {
+  const double max_gb = argc > 1 ? atof(argv[1]) : 64.0;
+  int sms;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t bytes = (size_t)(max_gb * (1ull << 30));
+  void* h;
+  CK(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  for (size_t i = 0; i < bytes; i += 4096) static_cast<char*>(h)[i] = (char)i;
+  void* hd;
+  CK(cudaHostGetDevicePointer(&hd, h, 0));
+  int* sink;
+  CK(cudaMalloc(&sink, 64));
+  const double regions[] = {0.5, 1, 2, 8, 32, 64};
+  for (double gb : regions) {
+    if (gb > max_gb) break;
+    const size_t region = (size_t)(gb * (1ull << 30));
+    const char* src = static_cast<const char*>(hd);
+    double m, g;
+#define ONEK(S, K)                                                                                          \
+  g = run<S, K>(src, region, sink, sms, &m);                                                               \
+  printf("{\"probe\":\"host_random_read\",\"region_GB\":%.1f,\"bytes\":%d,\"load\":\"%s\",\"Mreq_per_s\":%.1f," \
+         "\"GBps\":%.2f}\n",                                                                                    \
+         gb, S, K == 0 ? "nc.L1::no_allocate" : K == 1 ? "default" : K == 2 ? "L1::no_allocate" : "nc", m, g);                \
+  fflush(stdout);
+#define ONE(S) ONEK(S, 0) ONEK(S, 1) ONEK(S, 2) ONEK(S, 3)
+    ONE(4) ONE(32) ONE(64) ONE(128) ONE(256) ONE(512) ONE(2048)
+  }
+  CK(cudaFreeHost(h));
+  return 0;
+}
