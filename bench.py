@@ -147,10 +147,48 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def host_link_peaks(region_bytes: float = 0.0):
-    """Host-link peaks measured on the B200 box by tools/probe (profiles/hostlink_peaks.json):
-    the random-row read rate for a pinned region of this size (it falls from ~51 GB/s at 1 GB
-    to ~22 GB/s at 64 GB), else the streaming read rate."""
+def _hostreq_table(min_bytes: int = 32, exact_bytes: int | None = None):
+    """{region_GB: best GB/s over load kinds} from profiles/hostreq_probe.jsonl (tools/probe/
+    hostreq_probe.cu), over request sizes >= min_bytes (or exactly exact_bytes)."""
+    p = os.path.join(ROOT, "profiles", "hostreq_probe.jsonl")
+    if not os.path.exists(p):
+        return None
+    best = {}
+    for ln in open(p):
+        try:
+            d = json.loads(ln)
+        except ValueError:
+            continue
+        if d.get("probe") != "host_random_read":
+            continue
+        if (exact_bytes is not None and d["bytes"] != exact_bytes) or d["bytes"] < min_bytes:
+            continue
+        best[d["region_GB"]] = max(best.get(d["region_GB"], 0.0), float(d["GBps"]))
+    return sorted(best.items()) or None
+
+
+def _interp_log2(pts, gb):
+    gb = max(gb, 1e-9)
+    y = pts[0][1] if gb <= pts[0][0] else pts[-1][1]
+    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+        if x0 <= gb <= x1:
+            y = y0 + (y1 - y0) * (np.log2(gb) - np.log2(x0)) / (np.log2(x1) - np.log2(x0))
+    return y
+
+
+def host_link_peaks(region_bytes: float = 0.0, row_bytes: int = 512):
+    """Host-link peak for the gather's miss rows: the best measured random-read rate of requests of
+    the row's size (the probe's next size >= the row, e.g. 512 B for 400 B rows: an upper bound)
+    for a pinned region of this size, over the probe's load kinds (profiles/hostreq_probe.jsonl;
+    it falls from ~50 GB/s at 0.5-2 GB to ~35 GB/s at 64 GB for 512 B rows).  Falls back to round
+    1's profiles/hostlink_peaks.json.  Returns (GB/s, random 4 B reads M/s, description)."""
+    sizes = [32, 64, 128, 256, 512, 2048]
+    req = next((z for z in sizes if z >= row_bytes), sizes[-1])
+    tab = _hostreq_table(exact_bytes=req)
+    if tab and region_bytes > 0:
+        gb = region_bytes / 2 ** 30
+        return (_interp_log2(tab, gb), 0.0,
+                f"best measured random {req} B UVA read rate for a {gb:.1f} GB pinned region (tools/probe/hostreq_probe.cu)")
     p = os.path.join(ROOT, "profiles", "hostlink_peaks.json")
     if os.path.exists(p):
         d = json.load(open(p))
@@ -159,10 +197,7 @@ def host_link_peaks(region_bytes: float = 0.0):
         if tab and region_bytes > 0:
             pts = sorted((float(k), float(v)) for k, v in tab.items())
             gb = region_bytes / 2 ** 30
-            peak = pts[0][1] if gb <= pts[0][0] else pts[-1][1]
-            for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
-                if x0 <= gb <= x1:
-                    peak = y0 + (y1 - y0) * (gb - x0) / (x1 - x0)
+            peak = _interp_log2(pts, gb)
             kind = f"measured random-row UVA read for a {gb:.1f} GB pinned region (tools/probe)"
         return peak, float(d["uva_random4_Mreq_per_s"]), kind
     return 51.5, 90.0, "assumed"
@@ -170,29 +205,16 @@ def host_link_peaks(region_bytes: float = 0.0):
 
 def host_read_peak(region_bytes: float):
     """Best random-read PAYLOAD rate of the host link (GB/s) for a pinned region of this size:
-    the max over request sizes (32 B .. 2 KB) of tools/probe/hostreq_probe.cu's rates
-    (profiles/hostreq_probe.jsonl, interpolated in log2 of the region), i.e. no random read
+    the max over request sizes (32 B .. 2 KB) and load kinds of tools/probe/hostreq_probe.cu's
+    rates (profiles/hostreq_probe.jsonl, interpolated in log2 of the region), i.e. no random read
     pattern over that region moves payload faster.  Falls back to host_link_peaks()."""
-    p = os.path.join(ROOT, "profiles", "hostreq_probe.jsonl")
-    if not os.path.exists(p):
+    tab = _hostreq_table(min_bytes=32)
+    if not tab:
         peak, _, kind = host_link_peaks(region_bytes)
         return peak, kind
-    best = {}
-    for ln in open(p):
-        try:
-            d = json.loads(ln)
-        except ValueError:
-            continue
-        if d.get("probe") == "host_random_read" and d["bytes"] >= 32:
-            best[d["region_GB"]] = max(best.get(d["region_GB"], 0.0), float(d["GBps"]))
-    pts = sorted(best.items())
-    gb = max(region_bytes / 2 ** 30, 1e-9)
-    peak = pts[0][1] if gb <= pts[0][0] else pts[-1][1]
-    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
-        if x0 <= gb <= x1:
-            w = (np.log2(gb) - np.log2(x0)) / (np.log2(x1) - np.log2(x0))
-            peak = y0 + (y1 - y0) * w
-    return peak, f"best random-read payload rate for a {gb:.2f} GB pinned region (tools/probe/hostreq_probe.cu)"
+    gb = region_bytes / 2 ** 30
+    return (_interp_log2(tab, gb),
+            f"best random-read payload rate for a {gb:.2f} GB pinned region (tools/probe/hostreq_probe.cu)")
 
 
 def _cfg(args):
@@ -624,7 +646,7 @@ def run_ours(args):
     hbm_peak, peak_kind = measured_peaks()
     # Binding resource of the gather kernel: HBM (hit rows read + every row written + 4 B
     # slot lookup) vs the host link (miss rows read through UVA).
-    host_peak, _, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats())
+    host_peak, _, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats(), 4 * cfg.pitch_floats())
     hits_rows, miss_rows = cn[2], cn[3]
     # rows actually read: a node-sweep group reads each row once for all its batches; misses
     # among them are apportioned by the batches' miss fraction
@@ -691,6 +713,15 @@ def run_ours(args):
         if achieved_gbs:
             pattern = {"name": key.replace("_GBps", ""), "peak": pj[key], "frac": achieved_gbs / pj[key],
                        "writes_per_read": wpr, "source": "profiles/hbm_pattern_peaks.json"}
+    # L2 rule: no flush between timed steps; say whether the inputs exceed the L2 (126 MB on B200)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    fc_mb, ac_mb = info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6
+    x_mb = avg_fl * D * 4 / 1e6
+    big = max(fc_mb, ac_mb, x_mb * min(steps_eff, per)) * 1e6 > l2_bytes
+    l2_note = ("%s (L2 %.0f MB; feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
+               % ("inputs larger than L2, no flush" if big else
+                  "inputs SMALLER than L2, not flushed: this config is latency-bound, not a bandwidth line",
+                  l2_bytes / 1e6, fc_mb, ac_mb, x_mb))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps_eff,
         "warmup": args.warmup, "ms_per_step": ms / steps_eff, "higher_is_better": True, "scaling": args.scaling,
@@ -702,9 +733,7 @@ def run_ours(args):
                    "parallelism": f"dp{world} (" + ("feature cache partitioned over NVLink, adjacency replicated"
                                                     if args.partitioned and world > 1 else "replicated caches") + ")",
                    "inflight": nws, "group": G, "ldx": outs[0][0].ldx, "warmup_batches_run": int(sum(wsizes)),
-                   "l2": "inputs larger than L2 (feature cache %.0f MB, adjacency cache %.0f MB, X %.0f MB/step)"
-                         % (info["feat_rows"] * info["pitch"] * 4 / 1e6, info["adj_elems"] * 4 / 1e6,
-                            avg_fl * D * 4 / 1e6)},
+                   "l2": l2_note},
         "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * B,
                 "d2h_bytes_per_step": (8 * dci.RESULT_WORDS) if G else (8 * (L + 1) + 8 * 4 + 4),
                 "repeats": [seeds_all / (m / 1e3) for m in ems_list], "note": "median over the R timed regions"},
