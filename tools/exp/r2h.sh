@@ -7,3 +7,6 @@ done
 DCI_NMASK_SWEEP=0 timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2h/bench_M2_k20_nonmask.json 2> gpurun_out/r2h/bench_M2_k20_nonmask.log
 timeout 600 python bench.py --steps 300 --warmup 20 --no-cpu-baseline > gpurun_out/r2h/bench_M2_k300.json 2> gpurun_out/r2h/bench_M2_k300.log
 bash tools/exp/launches.sh r2h --steps 20 --warmup 5
+for g in 8 0; do
+timeout 900 python bench.py --config M4s --steps 40 --warmup 8 --group $g --no-cpu-baseline > gpurun_out/r2h/bench_M4s_g$g.json 2> gpurun_out/r2h/bench_M4s_g$g.log
+done
