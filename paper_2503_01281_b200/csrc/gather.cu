@@ -420,21 +420,20 @@ constexpr int kSweepMax = DCI_MAX_GROUP;  // 32-bit presence masks
 __device__ __forceinline__ void sweep_init(const TmaBatches& a, uint32_t* s_ep, uint32_t* s_lo, uint32_t* s_hi,
                                            long long* s_tot) {
   const int nb = a.n;
-  if (threadIdx.x < nb) {
-    const BatchScalars* sc = a.b[threadIdx.x].sc;
-    s_ep[threadIdx.x] = __ldcg(&sc->hdr.epoch);
-    const uint32_t nprev = a.L >= 2 ? (uint32_t)__ldcg(&sc->sizes[a.L - 1]) : (uint32_t)__ldcg(&sc->hdr.B);
-    s_lo[threadIdx.x] = a.phase == 2 ? nprev : 0u;
-    s_hi[threadIdx.x] = a.phase == 1 ? nprev : 0xFFFFFFFFu;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long acc = 0;
-    for (int i = 0; i < nb; ++i) {
-      const long long nl = a.phase == 1 ? 0 : __ldcg(&a.b[i].sc->sizes[a.L]);
-      acc += a.phase == 0 ? nl : a.phase == 1 ? (long long)s_hi[i] : nl - (long long)s_lo[i];
+  if (threadIdx.x < 32) {  // warp 0: lane b reads batch b; the rows written summed by shuffles
+    long long rows = 0;
+    if (threadIdx.x < nb) {
+      const BatchScalars* sc = a.b[threadIdx.x].sc;
+      s_ep[threadIdx.x] = __ldcg(&sc->hdr.epoch);
+      const uint32_t nprev = a.L >= 2 ? (uint32_t)__ldcg(&sc->sizes[a.L - 1]) : (uint32_t)__ldcg(&sc->hdr.B);
+      const long long nl = a.phase == 1 ? 0 : __ldcg(&sc->sizes[a.L]);
+      s_lo[threadIdx.x] = a.phase == 2 ? nprev : 0u;
+      s_hi[threadIdx.x] = a.phase == 1 ? nprev : 0xFFFFFFFFu;
+      rows = a.phase == 0 ? nl : a.phase == 1 ? (long long)nprev : nl - (long long)nprev;
     }
-    *s_tot = acc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, o);
+    if (threadIdx.x == 0) *s_tot = rows;
   }
   __syncthreads();
 }
@@ -819,13 +818,16 @@ __global__ void __launch_bounds__(32 * kTmaMaxWarps) k_gather_tma(const __grid_c
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int K = t.K, R = t.R, nb = a.n;
   const uint32_t ring = smem_addr(s_ring) + (uint32_t)(wib * K * t.slot_bytes);
-  if (threadIdx.x == 0) {
-    long long acc = 0;
-    for (int i = 0; i < nb; ++i) {
-      s_pre[i] = acc;
-      acc += __ldcg(&a.b[i].sc->sizes[a.L]);
+  if (threadIdx.x < 32) {  // warp 0: lane b reads batch b, shuffle prefix sum
+    const long long nl = threadIdx.x < nb ? __ldcg(&a.b[threadIdx.x].sc->sizes[a.L]) : 0;
+    long long x = nl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)threadIdx.x >= o) x += y;
     }
-    s_pre[nb] = acc;
+    if ((int)threadIdx.x < nb) s_pre[threadIdx.x] = x - nl;
+    if ((int)threadIdx.x == nb - 1) s_pre[nb] = x;
   }
   if (threadIdx.x < 2 * kTmaMaxBatches) (&s_cnt[0][0])[threadIdx.x] = 0u;
   if (threadIdx.x == 0) s_reads = 0u;

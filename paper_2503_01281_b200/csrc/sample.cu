@@ -115,33 +115,55 @@ struct HopShared {
   int all_ok;                         // no batch has a seed error (status set by hop 0)
 };
 
+// warp-inclusive prefix sum of 64-bit values (warp 0, all lanes)
+__device__ __forceinline__ long long warp_incl_scan(long long x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// The launch's batch table in shared memory, built by warp 0 with lane b reading batch b's
+// scalars (all batches' loads in flight at once; a serial loop in one thread cost ~2n dependent
+// L2 round trips before every block could start) and shuffle prefix sums.
 __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S) {
-  if (threadIdx.x == 0) {
-    long long acc = 0, pacc = 0, tacc = 0;
-    for (int b = 0; b < a.n; ++b) {
+  if (threadIdx.x < 32) {
+    const int b = threadIdx.x;
+    const bool in = b < a.n;
+    long long nh = 0, pw = 0, tw = 0;
+    int ok = 1;
+    if (in) {
       const BatchScalars* sc = a.b[b].sc;
       const long long B = sc->hdr.B;
-      const long long nh = a.hop == 0 ? B : sc->sizes[a.hop];
+      nh = a.hop == 0 ? B : sc->sizes[a.hop];
       const long long np = a.hop == 0 ? 0 : (a.hop == 1 ? B : sc->sizes[a.hop - 1]);
-      S.pre[b] = acc;
-      S.ppre[b] = pacc;
-      S.tpre[b] = tacc;
-      acc += nh;
-      pacc += np * a.prev_f;
-      tacc += a.b[b].prev_ntiles;
+      pw = np * a.prev_f;
+      tw = a.b[b].prev_ntiles;
       S.ehi[b] = (unsigned long long)sc->hdr.epoch << 32;
       S.seed[b] = sc->hdr.seed;
       S.Fin[b] = a.hop == 0 ? sc->hdr.seeds : a.b[b].F;
+      ok = __ldcg(&sc->status) == 0;
     }
-    S.pre[a.n] = acc;
-    S.ppre[a.n] = pacc;
-    S.tpre[a.n] = tacc;
-    int ok = 1;
-    for (int b = 0; b < a.n; ++b) ok &= __ldcg(&a.b[b].sc->status) == 0;
-    S.all_ok = ok;
+    const long long ia = warp_incl_scan(nh, b), ip = warp_incl_scan(pw, b), it = warp_incl_scan(tw, b);
+    if (in) {
+      S.pre[b] = ia - nh;
+      S.ppre[b] = ip - pw;
+      S.tpre[b] = it - tw;
+    }
+    if (b == a.n - 1) {
+      S.pre[a.n] = ia;
+      S.ppre[a.n] = ip;
+      S.tpre[a.n] = it;
+    }
+    const int all_ok = __all_sync(0xffffffffu, ok);
+    if (b == 0) {
+      S.all_ok = all_ok;
+      S.host_sectors = 0u;
+    }
   }
   if (threadIdx.x < 2 * DCI_MAX_GROUP) (&S.cnt[0][0])[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) S.host_sectors = 0u;
   __syncthreads();
 }
 
@@ -319,7 +341,10 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const int GPW = 32 / G;
   // the next node group's table probes and directory entry (contiguous: ids are consecutive)
-  // are loaded while the current group samples and writes
+  // are loaded while the current group samples and writes.  Static stride over the warps: a
+  // dynamic schedule (warps taking chunks of node groups from a ticket counter) measured slower
+  // at every chunk size (hop 2 of M2: 195 us static, 226 / 239 / 617 us for 8 / 32 / 128 nodes
+  // per ticket: ticket contention, and too few chunks for 4.7 K warps)
   const int64_t vstride = nwarps * GPW;
   auto probe = [&](int64_t vb, unsigned long long* t, int4& x0, int4& x1) {
     const int64_t vv = vb + lane / G;
@@ -341,9 +366,11 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc_h[c] = acc_m[c] = 0u;
   int4 e0, e1, e0n, e1n;
-  probe(warp_id * GPW, tc, e0, e1);
-  for (int64_t vbase = warp_id * GPW; vbase < a.N; vbase += vstride) {
-    probe(vbase + vstride, tn, e0n, e1n);
+  int64_t vbase = warp_id * GPW;
+  probe(vbase, tc, e0, e1);
+  while (vbase < a.N) {
+    const int64_t vn = vbase + vstride;
+    probe(vn, tn, e0n, e1n);
     const int64_t vv = vbase + lane / G;
     const bool in = vv < a.N;
     const int32_t v = (int32_t)vv;
@@ -425,6 +452,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
     for (int c = 0; c < CH; ++c) tc[c] = tn[c];
     e0 = e0n;
     e1 = e1n;
+    vbase = vn;
   }
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
@@ -778,22 +806,30 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
   __shared__ unsigned long long s_prefix;
   __shared__ int s_nmask;  // the hop swept: new-candidate masks come from k_newmask_sweep
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: lane b reads batch b (see hop_shared_init)
+    const int b = threadIdx.x;
+    const bool in = b < n;
+    long long nh = 0, nt = 0;
     int ok = 1;
-    for (int b = 0; b < n; ++b) ok &= __ldcg(&a.b[b].sc->status) == 0;
-    long long acc = 0, tacc = 0;
-    for (int b = 0; b < n; ++b) {
+    if (in) {
       const BatchScalars* sc = a.b[b].sc;
-      const long long nh = h == 0 ? (long long)sc->hdr.B : sc->sizes[h];
-      s_pre[b] = acc;
-      s_tpre[b] = tacc;
+      nh = h == 0 ? (long long)sc->hdr.B : sc->sizes[h];
+      nt = (nh + kScanTile - 1) / kScanTile;
       s_ehi[b] = (unsigned long long)sc->hdr.epoch << 32;
-      acc += nh;
-      tacc += (nh + kScanTile - 1) / kScanTile;
+      ok = __ldcg(&sc->status) == 0;
     }
-    s_pre[n] = acc;
-    s_tpre[n] = tacc;
-    s_nmask = a.nmask_on && hop_sweeps(a, acc, ok) ? 1 : 0;
+    const long long ia = warp_incl_scan(nh, b), it = warp_incl_scan(nt, b);
+    if (in) {
+      s_pre[b] = ia - nh;
+      s_tpre[b] = it - nt;
+    }
+    const int all_ok = __all_sync(0xffffffffu, ok);
+    const long long acc = __shfl_sync(0xffffffffu, ia, n - 1);
+    if (b == n - 1) {
+      s_pre[n] = ia;
+      s_tpre[n] = it;
+    }
+    if (b == 0) s_nmask = a.nmask_on && hop_sweeps(a, acc, all_ok) ? 1 : 0;
   }
   __syncthreads();
   const bool use_nmask = s_nmask != 0;
