@@ -600,7 +600,7 @@ static dci_status workspace_create(dci_ctx* ctx, int32_t max_batch, const int32_
   for (int h = 0; h < L; ++h) {
     w->cand_cap = std::max(w->cand_cap, w->hop_cap[h] * max_fanouts[L - 1 - h]);
     w->tile_off[h] = w->tiles_cap;
-    w->tiles_cap += (w->hop_cap[h] + kScanTile - 1) / kScanTile + 1;
+    w->tiles_cap += (w->hop_cap[h] + kScanDsts - 1) / kScanDsts + 1;
   }
   w->tile_off[L] = w->tiles_cap;
   auto bail = [&](cudaError_t e, const char* what) {

@@ -779,8 +779,10 @@ __global__ void __launch_bounds__(256) k_newmask_sweep(const __grid_constant__ H
 }
 
 // ------------------------------------------------------------------------------------
-// k_scan_hop: one thread per dst of F_h, kScanTile dsts per tile, tiles taken by dynamic
-// tickets (in-order => deadlock-free look-back); a multi-batch launch numbers the tiles of all its
+// k_scan_hop: kScanItems consecutive dsts of F_h per thread (1: four per thread, a quarter of the
+// look-back steps, measured slower -- fewer tiles leave the early hops' per-candidate tag reads
+// less parallelism), kScanDsts dsts per tile, tiles taken by dynamic tickets (in-order =>
+// deadlock-free look-back); a multi-batch launch numbers the tiles of all its
 // batches consecutively (one ticket counter) and each batch's tiles look back only within it.
 // Per dst: k (samples) and the bitmask of candidates that are the first occurrence of a node not
 // yet in F (table tag == tag(n_h + q)).  One block scan + warp-parallel decoupled look-back over
@@ -814,7 +816,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
     if (in) {
       const BatchScalars* sc = a.b[b].sc;
       nh = h == 0 ? (long long)sc->hdr.B : sc->sizes[h];
-      nt = (nh + kScanTile - 1) / kScanTile;
+      nt = (nh + kScanDsts - 1) / kScanDsts;
       s_ehi[b] = (unsigned long long)sc->hdr.epoch << 32;
       ok = __ldcg(&sc->status) == 0;
     }
@@ -849,45 +851,67 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
     const HopBatch& hb = a.b[b];
     const int64_t tile = gt - s_tpre[b];
     const int64_t n_h = s_pre[b + 1] - s_pre[b];
-    const int64_t ntiles = (n_h + kScanTile - 1) / kScanTile;
+    const int64_t ntiles = (n_h + kScanDsts - 1) / kScanDsts;
     const unsigned long long ehi = s_ehi[b];
-    const int64_t d = tile * kScanTile + threadIdx.x;
-    uint32_t k = 0, newmask = 0, nwide = 0;
-    if (d < n_h && use_nmask) {  // (f <= 32, h >= 1)
-      k = (uint32_t)hb.kcnt[d];
-      newmask = hb.nmask[d];
-    } else if (d < n_h) {
-      k = (uint32_t)hb.kcnt[d];
-      const int32_t* c = hb.cand + d * f;
-      const uint32_t base = (uint32_t)(n_h + d * f);
-      // which of my candidates own their node's first occurrence (8 loads in flight); a
-      // 32-bit mask for f <= 32, else counted here and re-checked when appending
-      for (uint32_t s0 = 0; s0 < k; s0 += 8) {
-        int32_t x[8];
+    // this thread's kScanItems consecutive dsts of the tile
+    const int64_t d0 = tile * kScanDsts + (int64_t)threadIdx.x * kScanItems;
+    uint32_t kk[kScanItems], newmask[kScanItems], nwide[kScanItems];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = (s0 + u < k) ? c[s0 + u] : -1;
-        unsigned long long t[8];
+    for (int it = 0; it < kScanItems; ++it) {
+      kk[it] = 0;
+      newmask[it] = 0;
+      nwide[it] = 0;
+    }
+    if (use_nmask) {  // (f <= 32, h >= 1)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = x[u] >= 0 ? pt_tag(hb.pos_of, hb.hmask, x[u], (uint32_t)(ehi >> 32)) : 0ull;
+      for (int it = 0; it < kScanItems; ++it)
+        if (d0 + it < n_h) {
+          kk[it] = (uint32_t)hb.kcnt[d0 + it];
+          newmask[it] = hb.nmask[d0 + it];
+        }
+    } else {
+      for (int it = 0; it < kScanItems; ++it) {
+        const int64_t d = d0 + it;
+        if (d >= n_h) break;
+        const uint32_t k = (uint32_t)hb.kcnt[d];
+        kk[it] = k;
+        const int32_t* c = hb.cand + d * f;
+        const uint32_t base = (uint32_t)(n_h + d * f);
+        // which of d's candidates own their node's first occurrence (8 loads in flight); a
+        // 32-bit mask for f <= 32, else counted here and re-checked when appending
+        uint32_t nm = 0, nw = 0;
+        for (uint32_t s0 = 0; s0 < k; s0 += 8) {
+          int32_t x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) {
-            if (f <= 32)
-              newmask |= 1u << (s0 + u);
-            else
-              ++nwide;
-          }
-      }
-      if (h == 0) {
-        const int32_t sd = hb.F[d];
-        if (sd >= 0 && (int64_t)sd < a.N &&
-            pt_tag(hb.pos_of, hb.hmask, sd, (uint32_t)(ehi >> 32)) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
-          atomicCAS(&hb.sc->status, 0, (int32_t)DCI_EDUP);
+          for (int u = 0; u < 8; ++u) x[u] = (s0 + u < k) ? c[s0 + u] : -1;
+          unsigned long long t[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            t[u] = x[u] >= 0 ? pt_tag(hb.pos_of, hb.hmask, x[u], (uint32_t)(ehi >> 32)) : 0ull;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (x[u] >= 0 && t[u] == (ehi | (0xFFFFFFFFu - (base + s0 + u)))) {
+              if (f <= 32)
+                nm |= 1u << (s0 + u);
+              else
+                ++nw;
+            }
+        }
+        newmask[it] = nm;
+        nwide[it] = nw;
+        if (h == 0) {
+          const int32_t sd = hb.F[d];
+          if (sd >= 0 && (int64_t)sd < a.N &&
+              pt_tag(hb.pos_of, hb.hmask, sd, (uint32_t)(ehi >> 32)) != (ehi | (0xFFFFFFFFu - (uint32_t)d)))
+            atomicCAS(&hb.sc->status, 0, (int32_t)DCI_EDUP);
+        }
       }
     }
-    const uint32_t nn = f <= 32 ? __popc(newmask) : nwide;
+    unsigned long long mine = 0;  // packed (k << 31 | nn) over the thread's dsts
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it)
+      mine += ((unsigned long long)kk[it] << 31) | (f <= 32 ? (uint32_t)__popc(newmask[it]) : nwide[it]);
     // block exclusive scan of packed (k << 31 | nn)
-    const unsigned long long mine = ((unsigned long long)k << 31) | nn;
     unsigned long long incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -943,31 +967,36 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
       }
     }
     __syncthreads();
-    if (d < n_h) {
-      const unsigned long long pre = s_prefix + excl;
-      hb.bptr[d] = (int32_t)(pre >> 31);
-      uint32_t nid = (uint32_t)(n_h + (int64_t)(pre & ((1ull << 31) - 1)));
-      const int32_t* c = hb.cand + d * f;
-      if (f <= 32) {
-        for (uint32_t m = newmask; m; m &= m - 1) {
-          const int s = __ffs(m) - 1;
-          const int32_t x = c[s];
-          hb.F[nid] = x;
-          *pt_find(hb.pos_of, hb.hmask, x, (uint32_t)(ehi >> 32)) = ehi | (0xFFFFFFFFu - nid);
-          ++nid;
-        }
-      } else if (nwide) {
-        // only this candidate's owner rewrites its tag, so the check is stable (see above)
-        const uint32_t base = (uint32_t)(n_h + d * f);
-        for (uint32_t s = 0; s < k; ++s) {
-          const int32_t x = c[s];
-          unsigned long long* tp = x >= 0 ? pt_find(hb.pos_of, hb.hmask, x, (uint32_t)(ehi >> 32)) : nullptr;
-          if (tp && __ldcg(tp) == (ehi | (0xFFFFFFFFu - (base + s)))) {
+    {
+      unsigned long long pre = s_prefix + excl;
+      for (int it = 0; it < kScanItems; ++it) {
+        const int64_t d = d0 + it;
+        if (d >= n_h) break;
+        hb.bptr[d] = (int32_t)(pre >> 31);
+        uint32_t nid = (uint32_t)(n_h + (int64_t)(pre & ((1ull << 31) - 1)));
+        const int32_t* c = hb.cand + d * f;
+        if (f <= 32) {
+          for (uint32_t m = newmask[it]; m; m &= m - 1) {
+            const int s = __ffs(m) - 1;
+            const int32_t x = c[s];
             hb.F[nid] = x;
-            *tp = ehi | (0xFFFFFFFFu - nid);
+            *pt_find(hb.pos_of, hb.hmask, x, (uint32_t)(ehi >> 32)) = ehi | (0xFFFFFFFFu - nid);
             ++nid;
           }
+        } else if (nwide[it]) {
+          // only this candidate's owner rewrites its tag, so the check is stable (see above)
+          const uint32_t base = (uint32_t)(n_h + d * f);
+          for (uint32_t s = 0; s < kk[it]; ++s) {
+            const int32_t x = c[s];
+            unsigned long long* tp = x >= 0 ? pt_find(hb.pos_of, hb.hmask, x, (uint32_t)(ehi >> 32)) : nullptr;
+            if (tp && __ldcg(tp) == (ehi | (0xFFFFFFFFu - (base + s)))) {
+              hb.F[nid] = x;
+              *tp = ehi | (0xFFFFFFFFu - nid);
+              ++nid;
+            }
+          }
         }
+        pre += ((unsigned long long)kk[it] << 31) | (f <= 32 ? (uint32_t)__popc(newmask[it]) : nwide[it]);
       }
     }
     __syncthreads();  // s_ticket / s_prefix reuse
@@ -1085,7 +1114,7 @@ void launch_sample_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* 
 void launch_scan_hop(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n, cudaStream_t s) {
   const HopLaunch a = hop_launch(ctx, ws, p, n);
   int64_t tiles = 0;
-  for (int i = 0; i < n; ++i) tiles += (ws[i]->hop_cap[p[0].hop] + kScanTile - 1) / kScanTile;
+  for (int i = 0; i < n; ++i) tiles += (ws[i]->hop_cap[p[0].hop] + kScanDsts - 1) / kScanDsts;
   int64_t grid = persistent_grid(ctx, k_scan_hop, kScanTile, 8);
   if (tiles < grid) grid = tiles > 0 ? tiles : 1;
   k_scan_hop<<<(unsigned)grid, kScanTile, 0, s>>>(a);

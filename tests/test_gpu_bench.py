@@ -79,3 +79,21 @@ def test_bench_spawns_ranks_for_gpus_n(scaling):
     seeds = B * steps * (2 if scaling == "weak" else 1)
     assert d["value"] == pytest.approx(seeds / (d["ms_per_step"] * steps / 1e3), rel=1e-6)
     assert len(d["clocks"]["per_rank"]) == 2
+
+
+def test_bench_m4s_hashed_tables_light_parity():
+    """Hashed position tables at scale (S6): the papers100M-shaped graph at 1/10
+    scale (11.1 M nodes, 161.6 M edges, 25 % budget, host-resident misses, groups of 8) with the
+    hashed layout forced, timed as the bench times it, then a whole group of full-size batches
+    checked bit-exact against the oracle (presample, fills and sampling on the full graph; X rows
+    against the closed-form features)."""
+    env = dict(os.environ, DCI_TABLE="hash")
+    r = subprocess.run([sys.executable, "bench.py", "--config", "M4s", "--steps", "8", "--warmup", "8",
+                        "--repeats", "1", "--check-light", "--no-cpu-baseline"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    check_common(d, 8, 8)
+    assert d["parity_check"]["bit_exact"] is True and d["parity_check"]["batches"] == 3
+    assert d["config"]["position_table_MB_per_workspace"] <= 64.0  # hashed, not 8 N = 89 MB
+    assert d["stats"]["adj_hit_rate"] < 1.0 and d["stats"]["feat_hit_rate"] < 1.0  # misses went through UVA

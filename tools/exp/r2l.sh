@@ -1,0 +1,7 @@
+# multi-item scan tiles (1024 dsts per tile)
+mkdir -p gpurun_out/r2l
+timeout 2000 python -m pytest tests -m gpu -q -x 2>&1 | tail -4 > gpurun_out/r2l/tests.txt
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/r2l/bench_M2_k20.json 2> gpurun_out/r2l/bench_M2_k20.log
+bash tools/exp/launches.sh r2l --steps 20 --warmup 5
+timeout 600 python bench.py --steps 300 --warmup 20 --no-cpu-baseline > gpurun_out/r2l/bench_M2_k300.json 2> gpurun_out/r2l/bench_M2_k300.log
+timeout 900 python bench.py --config M3 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2l/bench_M3.json 2> gpurun_out/r2l/bench_M3.log
