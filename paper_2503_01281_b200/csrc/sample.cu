@@ -112,6 +112,9 @@ struct HopShared {
   const int32_t* Fin[DCI_MAX_GROUP];
   unsigned cnt[DCI_MAX_GROUP][2];     // adjacency hits / misses of this block, per batch
   unsigned host_sectors;              // distinct 32-byte host sectors its adjacency misses read
+  unsigned long long tbase[DCI_MAX_GROUP];  // epoch << 32 | ~n_h: a candidate's tag = tbase - (d f + slot)
+  uint32_t nh[DCI_MAX_GROUP];         // n_h of each batch
+  unsigned sweep_next;                // node sweep: the block's next node group (shared ticket)
   int all_ok;                         // no batch has a seed error (status set by hop 0)
 };
 
@@ -151,6 +154,8 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
       S.pre[b] = ia - nh;
       S.ppre[b] = ip - pw;
       S.tpre[b] = it - tw;
+      S.nh[b] = (uint32_t)nh;
+      S.tbase[b] = S.ehi[b] | (0xFFFFFFFFu - (uint32_t)nh);
     }
     if (b == a.n - 1) {
       S.pre[a.n] = ia;
@@ -161,6 +166,7 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
     if (b == 0) {
       S.all_ok = all_ok;
       S.host_sectors = 0u;
+      S.sweep_next = 0u;
     }
   }
   if (threadIdx.x < 2 * DCI_MAX_GROUP) (&S.cnt[0][0])[threadIdx.x] = 0u;
@@ -341,11 +347,24 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const int GPW = 32 / G;
   // the next node group's table probes and directory entry (contiguous: ids are consecutive)
-  // are loaded while the current group samples and writes.  Static stride over the warps: a
-  // dynamic schedule (warps taking chunks of node groups from a ticket counter) measured slower
-  // at every chunk size (hop 2 of M2: 195 us static, 226 / 239 / 617 us for 8 / 32 / 128 nodes
-  // per ticket: ticket contention, and too few chunks for 4.7 K warps)
-  const int64_t vstride = nwarps * GPW;
+  // are loaded while the current group samples and writes.  Schedule: each block owns a static
+  // contiguous range of node groups and its warps take them one at a time from a shared-memory
+  // ticket (taken one ahead).  A static stride over all warps left a long tail (a warp's work is a
+  // sum of ~25 nodes present in 0..n batches: 12 % of the stall samples sat at the block barrier,
+  // ncu r2i), and one global ticket counter measured slower still (226-617 us: contention on one
+  // address, and too few chunks for 4.7 K warps); block ranges are sums of ~400 groups each.
+  const int64_t ngroups = (a.N + GPW - 1) / GPW;
+  const int64_t per_block = (ngroups + gridDim.x - 1) / gridDim.x;
+  const int64_t g0 = (int64_t)blockIdx.x * per_block;
+  const int64_t g1 = g0 + per_block < ngroups ? g0 + per_block : ngroups;
+  auto take = [&]() -> int64_t {  // -> first node id of the warp's next group, or N when done
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&S.sweep_next, 1u);
+    const int64_t g = g0 + (int64_t)__shfl_sync(0xffffffffu, t, 0);
+    return g < g1 ? g * GPW : a.N;
+  };
+  (void)warp_id;
+  (void)nwarps;
   auto probe = [&](int64_t vb, unsigned long long* t, int4& x0, int4& x1) {
     const int64_t vv = vb + lane / G;
     x0 = make_int4(0, 0, 0, 0);
@@ -366,10 +385,10 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc_h[c] = acc_m[c] = 0u;
   int4 e0, e1, e0n, e1n;
-  int64_t vbase = warp_id * GPW;
+  int64_t vbase = take();
   probe(vbase, tc, e0, e1);
   while (vbase < a.N) {
-    const int64_t vn = vbase + vstride;
+    const int64_t vn = take();
     probe(vn, tn, e0n, e1n);
     const int64_t vv = vbase + lane / G;
     const bool in = vv < a.N;
@@ -385,7 +404,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       dd[c] = 0xFFFFFFFFu - (uint32_t)tc[c];
       if (c * G < n) {
         if (in && bb < n)
-          pres = (tc[c] >> 32) == (S.ehi[bb] >> 32) && dd[c] < (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
+          pres = (tc[c] >> 32) == (S.ehi[bb] >> 32) && dd[c] < S.nh[bb];
         const unsigned bal = (__ballot_sync(0xffffffffu, pres) & gmask) >> gbase;
         pm |= bal << (c * G);
       }
@@ -438,13 +457,9 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       if (!((pm >> bb) & 1u)) continue;
       const HopBatch& hb = a.b[bb];
       if (gl < f) hb.cand[(int64_t)d * f + gl] = x;
-      if (gl == 0) {
-        hb.kcnt[d] = k;
-        hb.nmask[d] = 0u;  // filled by k_newmask_sweep
-      }
-      if (valid) {
-        const uint32_t n_h = (uint32_t)(S.pre[bb + 1] - S.pre[bb]);
-        const unsigned long long tag = S.ehi[bb] | (0xFFFFFFFFu - (n_h + d * (uint32_t)f + (uint32_t)gl));
+      if (gl == 0) hb.kcnt[d] = k;
+      if (valid) {  // tag(n_h + d f + gl) = epoch << 32 | ~(n_h + d f + gl); no borrow: < 2^31
+        const unsigned long long tag = S.tbase[bb] - (unsigned long long)(d * (uint32_t)f + (uint32_t)gl);
         if (!a.precheck || __ldcg(hb.pos_of + x) < tag) atomicMax(hb.pos_of + x, tag);
       }
     }
@@ -506,6 +521,11 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   // (and not when a batch has a seed error: a bad or repeated seed has no table slot of its own,
   // so the sweep would leave its candidate slots unwritten; frontier order fills them)
   if (G >= 4 && hop_sweeps(a, total, S.all_ok)) {
+    if (a.nmask_on)  // the new-mask pass (next kernel) ORs into zeroed masks: one coalesced pass here
+      for (long long q = tid, b = 0; q < total; q += nthreads) {
+        while (b + 1 < a.n && q >= S.pre[b + 1]) ++b;  // q only grows: the batch only advances
+        a.b[b].nmask[q - S.pre[b]] = 0u;
+      }
     sample_sweep<(G >= 4 ? G : 4)>(a, S, warp_id, nwarps, keep, epol);
     hop_shared_flush(a, S);
     return;
@@ -750,7 +770,7 @@ __global__ void __launch_bounds__(256) k_hop_epilogue(const __grid_constant__ Ho
 // same test the scan otherwise makes per candidate (tag == own position).  Sweeping node ids reads
 // every table once, coalesced (N x n x 8 B), instead of one random tag read per candidate
 // (sum_b |F_h(b)| x f: 12 M per group of 20 on M2's last hop), and sets bit s of nmask_b[d].
-// The sampler zeroed nmask_b[d] for every dst it wrote.  Exits at once unless the hop swept.
+// The hop kernel zeroed the masks (one coalesced pass).  Exits at once unless the hop swept.
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_newmask_sweep(const __grid_constant__ HopLaunch a) {
   __shared__ HopShared S;
