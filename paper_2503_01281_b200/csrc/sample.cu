@@ -802,7 +802,10 @@ __global__ void __launch_bounds__(256) k_newmask_sweep(const __grid_constant__ H
 // k_scan_hop: kScanItems consecutive dsts of F_h per thread (1: four per thread, a quarter of the
 // look-back steps, measured slower -- fewer tiles leave the early hops' per-candidate tag reads
 // less parallelism), kScanDsts dsts per tile, tiles taken by dynamic tickets (in-order =>
-// deadlock-free look-back); a multi-batch launch numbers the tiles of all its
+// deadlock-free look-back).  (Measured and not kept: a three-pass reduce-then-scan, 27 / 48 /
+// 70 us against 14 / 26 / 65 us per hop of M2 -- the last scan's cost is its 2 M new-node appends
+// (candidate read, F write, final-id tag write), not the look-back; and a warp-cooperative append,
+// no change); a multi-batch launch numbers the tiles of all its
 // batches consecutively (one ticket counter) and each batch's tiles look back only within it.
 // Per dst: k (samples) and the bitmask of candidates that are the first occurrence of a node not
 // yet in F (table tag == tag(n_h + q)).  One block scan + warp-parallel decoupled look-back over
@@ -867,7 +870,10 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
     __syncthreads();
     const long long gt = s_ticket;
     if (gt >= ntiles_all) break;
-    const int b = batch_of(s_tpre, n, gt);
+    int b = 0;  // batch of tile gt: binary search over the tile prefix (n <= 32)
+#pragma unroll
+    for (int step = 16; step; step >>= 1)
+      if (b + step < n && gt >= s_tpre[b + step]) b += step;
     const HopBatch& hb = a.b[b];
     const int64_t tile = gt - s_tpre[b];
     const int64_t n_h = s_pre[b + 1] - s_pre[b];
