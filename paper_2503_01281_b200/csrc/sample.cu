@@ -187,7 +187,8 @@ __device__ __forceinline__ unsigned host_sectors_opened(bool miss, int64_t elem,
   return __popc(__ballot_sync(0xffffffffu, miss && (gl == 0 || !pmiss || pl != line)));
 }
 
-// batch of item q in a prefix table (n <= 16: a short linear scan over shared memory)
+// batch of item q in a prefix table (n <= DCI_MAX_GROUP = 32: a linear scan over shared memory;
+// the hot loops advance a running batch index instead, since their items only grow)
 __device__ __forceinline__ int batch_of(const long long* pre, int n, long long q) {
   int b = 0;
   while (b + 1 < n && q >= pre[b + 1]) ++b;
