@@ -167,6 +167,26 @@ def _hostreq_table(min_bytes: int = 32, exact_bytes: int | None = None):
     return sorted(best.items()) or None
 
 
+def host_request_peak(region_bytes: float):
+    """Best random-REQUEST rate of the host link (M requests/s) for a pinned region of this size: the
+    max over request sizes (>= 32 B) and load kinds of profiles/hostreq_probe.jsonl's Mreq_per_s
+    (interpolated in log2 of the region).  For regions beyond a few GB it is set by address
+    translation (~70-80 M/s for 8-64 GB, whatever the size up to 512 B), not by bytes."""
+    p = os.path.join(ROOT, "profiles", "hostreq_probe.jsonl")
+    if not os.path.exists(p):
+        return None
+    best = {}
+    for ln in open(p):
+        try:
+            d = json.loads(ln)
+        except ValueError:
+            continue
+        if d.get("probe") == "host_random_read" and d["bytes"] >= 32:
+            best[d["region_GB"]] = max(best.get(d["region_GB"], 0.0), float(d["Mreq_per_s"]))
+    pts = sorted(best.items())
+    return _interp_log2(pts, region_bytes / 2 ** 30) if pts else None
+
+
 def _interp_log2(pts, gb):
     gb = max(gb, 1e-9)
     y = pts[0][1] if gb <= pts[0][0] else pts[-1][1]
@@ -566,8 +586,9 @@ def run_ours(args):
     table_mb = max(st["table_bytes"] for st in sts) / 2 ** 20
     host_rows = sum(st["host_rows_read"] for st in sts)
     host_sectors = sum(st["host_adj_sectors"] for st in sts)
+    host_runs = sum(st["host_adj_runs"] for st in sts)
     tot = parallel.sum_over_ranks([sum(st["seeds"] for st in sts), launches, rows, alg_bytes, g_ms, s_ms, n_timed,
-                                   n_glaunch, rows_read, *cn.tolist(), host_rows, host_sectors], device=dev)
+                                   n_glaunch, rows_read, *cn.tolist(), host_rows, host_sectors, host_runs], device=dev)
     seeds_all = tot[0] / R  # per timed region
     value = seeds_all / (ms / 1e3)
     rep_values = [seeds_all / (m / 1e3) for m in ms_list]
@@ -673,7 +694,7 @@ def run_ours(args):
     # adjacency misses read (the unit the GPU fetches from system memory; the library counts both).
     # BW_host = the best random-read payload rate measured for a pinned region of the graph's size
     # (profiles/hostreq_probe.jsonl), so T_host is a lower bound on the link time of that traffic.
-    host_rows_read, host_adj_sectors = tot[13], tot[14]
+    host_rows_read, host_adj_sectors, host_adj_runs = tot[13], tot[14], tot[15]
     samples = cn[0] + cn[1]
     B_hbm = hbm_b + 4.0 * cn[0] + 4.0 * samples
     B_host = host_rows_read * 4.0 * cfg.pitch_floats() + 32.0 * host_adj_sectors
@@ -681,12 +702,27 @@ def run_ours(args):
     bw_host, bw_host_kind = host_read_peak(region)
     T_terms = {"hbm_ms": B_hbm / (hbm_peak * 1e9) * 1e3, "host_ms": B_host / (bw_host * 1e9) * 1e3}
     T_roof = max(T_terms.values())
+    # Request view (SURVEY §8(d)'s N_req/R_req term, reported beside the byte roofline, not in it):
+    # random host requests = miss rows + adjacency-miss runs (a run's sectors are contiguous) against
+    # the best random-request rate the probe measured for a pinned region of the graph's size.  The
+    # probe's requests are uniformly random, so a workload with more page locality can exceed it.
+    R_req = host_request_peak(region)
+    N_req = host_rows_read + host_adj_runs
+    request_view = None
+    if R_req and N_req > 0:
+        T_req = N_req / (R_req * 1e6) * 1e3
+        request_view = {"requests": N_req, "host_rows": host_rows_read, "adj_runs": host_adj_runs,
+                        "M_requests_per_s": N_req / (ms_tot / 1e3) / 1e6, "peak_M_per_s": R_req,
+                        "T_req_ms": T_req, "frac": T_req / ms_tot,
+                        "note": "best random-request rate of tools/probe/hostreq_probe.cu for this pinned region "
+                                "(address-translation bound beyond a few GB); uniformly random requests"}
     host_link = {"feature_miss_GBps": host_b / (ms_tot / 1e3) / 1e9, "peak_GBps": host_peak,
                  "feature_frac": host_b / (ms_tot / 1e3) / 1e9 / host_peak, "peak_kind": host_kind,
                  "adj_miss_Mreads_per_s": cn[1] / (ms_tot / 1e3) / 1e6,
                  "host_rows_read": host_rows_read, "host_adj_sectors": host_adj_sectors,
                  "host_payload_GBps": B_host / (ms_tot / 1e3) / 1e9, "host_read_peak_GBps": bw_host,
                  "host_read_peak_kind": bw_host_kind,
+                 "request_view": request_view,
                  "step_roofline": {"T_roof_ms": T_roof, "T_measured_ms": ms_tot, "frac": T_roof / ms_tot,
                                    "binding": max(T_terms, key=T_terms.get), **T_terms,
                                    "B_hbm_bytes": B_hbm, "B_host_bytes": B_host,

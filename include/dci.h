@@ -350,6 +350,9 @@ typedef struct dci_ws_stats {
   uint64_t gather_kinds[3]; /* group gathers this workspace led: row mode, node sweep with register
                                copies, node sweep with bulk copies */
   uint64_t table_bytes;     /* device bytes of the workspace's position table (dense 8 N, or hashed) */
+  uint64_t host_adj_runs;   /* (dst, hop) runs with at least one adjacency miss: the random host requests
+                               of the sampler (a run's sectors are contiguous); with host_rows_read the
+                               request count of the bench's host-link request view */
 } dci_ws_stats;
 
 dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t reset);

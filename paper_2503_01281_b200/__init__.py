@@ -54,7 +54,7 @@ class dci_ws_stats(C.Structure):
                 ("counters", C.c_uint64 * 4), ("timed_batches", C.c_uint64), ("sample_ms", C.c_double),
                 ("gather_ms", C.c_double), ("gather_launches", C.c_uint64), ("rows_read", C.c_uint64),
                 ("gather_bytes", C.c_uint64), ("host_rows_read", C.c_uint64), ("host_adj_sectors", C.c_uint64),
-                ("gather_kinds", C.c_uint64 * 3), ("table_bytes", C.c_uint64)]
+                ("gather_kinds", C.c_uint64 * 3), ("table_bytes", C.c_uint64), ("host_adj_runs", C.c_uint64)]
 
 
 class dci_fill_times(C.Structure):
@@ -255,7 +255,8 @@ class Workspace:
                 "sample_ms": st.sample_ms, "gather_ms": st.gather_ms, "gather_launches": st.gather_launches,
                 "rows_read": st.rows_read, "gather_bytes": st.gather_bytes,
                 "host_rows_read": st.host_rows_read, "host_adj_sectors": st.host_adj_sectors,
-                "gather_kinds": [int(k) for k in st.gather_kinds], "table_bytes": int(st.table_bytes)}
+                "gather_kinds": [int(k) for k in st.gather_kinds], "table_bytes": int(st.table_bytes),
+                "host_adj_runs": int(st.host_adj_runs)}
 
     def stage_ms(self):
         s, g = C.c_float(), C.c_float()

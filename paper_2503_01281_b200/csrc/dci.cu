@@ -1380,12 +1380,13 @@ dci_status dci_workspace_stats(dci_workspace* ws, dci_ws_stats* out, int32_t res
   out->gather_bytes = h.acc_gather_bytes;
   out->host_rows_read = h.acc_host_rows;
   out->host_adj_sectors = h.acc_host_sectors;
+  out->host_adj_runs = h.acc_host_runs;
   for (int k = 0; k < 3; ++k) out->gather_kinds[k] = ws->kind_launches[k];
   out->table_bytes = ws->table_bytes;
   if (reset) {
     h.acc_batches = h.acc_seeds = h.acc_rows = 0;
     h.acc_rows_read = h.acc_gather_bytes = 0;
-    h.acc_host_rows = h.acc_host_sectors = 0;
+    h.acc_host_rows = h.acc_host_sectors = h.acc_host_runs = 0;
     for (auto& k : ws->kind_launches) k = 0;
     for (int c = 0; c < 4; ++c) h.acc_counters[c] = 0;
     DCI_CUDA(cudaMemcpy(ws->scal, &h, sizeof(h), cudaMemcpyHostToDevice));

@@ -117,7 +117,7 @@ struct BatchScalars {
   unsigned long long acc_rows_read, acc_gather_bytes, launch_reads;
   // host-link traffic (bench roofline): 32-byte host sectors read by adjacency misses (sampling
   // kernels), feature rows read from pinned host memory (gathers); booked on a launch's first batch
-  unsigned long long acc_host_sectors, acc_host_rows;
+  unsigned long long acc_host_sectors, acc_host_rows, acc_host_runs;
   // node-sweep gather: next 32-node group to take (dynamic schedule; reset by the launch's last block)
   unsigned long long sweep_ticket;
 };

@@ -112,6 +112,7 @@ struct HopShared {
   const int32_t* Fin[DCI_MAX_GROUP];
   unsigned cnt[DCI_MAX_GROUP][2];     // adjacency hits / misses of this block, per batch
   unsigned host_sectors;              // distinct 32-byte host sectors its adjacency misses read
+  unsigned host_runs;                 // (dst, hop) runs with at least one adjacency miss
   unsigned long long tbase[DCI_MAX_GROUP];  // epoch << 32 | ~n_h: a candidate's tag = tbase - (d f + slot)
   uint32_t nh[DCI_MAX_GROUP];         // n_h of each batch
   unsigned sweep_next;                // node sweep: the block's next node group (shared ticket)
@@ -166,6 +167,7 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
     if (b == 0) {
       S.all_ok = all_ok;
       S.host_sectors = 0u;
+      S.host_runs = 0u;
       S.sweep_next = 0u;
     }
   }
@@ -177,14 +179,26 @@ __device__ __forceinline__ void hop_shared_init(const HopLaunch& a, HopShared& S
 // that misses is a 4-byte zero-copy read of pinned host memory, and the GPU fetches system memory
 // in 32-byte sectors, so misses of one (dst, hop) that fall in the same sector are served together.
 // Ranks are sorted within a G-lane group, so the misses are its last lanes in address order: a miss
-// lane opens a new sector unless the lane before it missed in the same sector.  Returns the
-// sectors the warp's groups open (warp-uniform).
+// lane opens a new sector unless the lane before it missed in the same sector, and the group's
+// first miss lane opens its run (one contiguous stretch of the node's host run: the request view
+// counts runs).  Adds the warp's counts to the caller's (warp-uniform) register totals, which are
+// flushed once per thread block-wide at the end (no shared atomics in the sampling loops).
 template <int G>
-__device__ __forceinline__ unsigned host_sectors_opened(bool miss, int64_t elem, int gl) {
+__device__ __forceinline__ void host_miss_counts(bool miss, int64_t elem, int gl, unsigned& sectors,
+                                                 unsigned& runs) {
   const long long line = elem >> 3;  // 8 int32 per 32-byte sector
   const long long pl = __shfl_up_sync(0xffffffffu, line, 1, G);
   const bool pmiss = __shfl_up_sync(0xffffffffu, (int)miss, 1, G) != 0;
-  return __popc(__ballot_sync(0xffffffffu, miss && (gl == 0 || !pmiss || pl != line)));
+  const bool first = miss && (gl == 0 || !pmiss);
+  sectors += __popc(__ballot_sync(0xffffffffu, miss && (first || pl != line)));
+  runs += __popc(__ballot_sync(0xffffffffu, first));
+}
+
+__device__ __forceinline__ void host_miss_flush(HopShared& S, unsigned sectors, unsigned runs) {
+  if ((threadIdx.x & 31) == 0) {
+    if (sectors) atomicAdd(&S.host_sectors, sectors);
+    if (runs) atomicAdd(&S.host_runs, runs);
+  }
 }
 
 // batch of item q in a prefix table (n <= DCI_MAX_GROUP = 32: a linear scan over shared memory;
@@ -203,6 +217,7 @@ __device__ __forceinline__ void hop_shared_flush(const HopLaunch& a, HopShared& 
     if (S.cnt[threadIdx.x][1]) atomicAdd(&sc->counters[1], (unsigned long long)S.cnt[threadIdx.x][1]);
   }
   if (threadIdx.x == 0 && S.host_sectors) atomicAdd(&a.b[0].sc->acc_host_sectors, (unsigned long long)S.host_sectors);
+  if (threadIdx.x == 0 && S.host_runs) atomicAdd(&a.b[0].sc->acc_host_runs, (unsigned long long)S.host_runs);
 }
 
 // Fused extra work of every hop kernel: hop 0 writes the seeds into F and the position table
@@ -383,6 +398,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
   };
   unsigned long long tc[CH], tn[CH];
   unsigned acc_h[CH], acc_m[CH];
+  unsigned hsec = 0, hrun = 0;  // host sectors / runs of the adjacency misses (warp-uniform)
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc_h[c] = acc_m[c] = 0u;
   int4 e0, e1, e0n, e1n;
@@ -429,8 +445,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       x = hit ? ld_keep_i32(a.acache + cache_off + rank, epol) : ld_host_i32(a.uidx + host_off + rank);
     }
     {  // read once for every batch holding v: its host sectors count once
-      const unsigned nl = host_sectors_opened<G>(valid && !hit, host_off + rank, gl);
-      if (lane == 0 && nl) atomicAdd(&S.host_sectors, nl);
+      host_miss_counts<G>(valid && !hit, host_off + rank, gl, hsec, hrun);
     }
     // v's hits / misses, counted once per node and added to every batch holding v: lane gl keeps
     // the running counts of batches gl, gl + G, ... in registers (no per-sample shared atomics)
@@ -478,6 +493,7 @@ __device__ __forceinline__ void sample_sweep(const HopLaunch& a, HopShared& S, i
       if (acc_m[c]) atomicAdd(&S.cnt[bb][1], acc_m[c]);
     }
   }
+  host_miss_flush(S, hsec, hrun);
 }
 
 // ------------------------------------------------------------------------------------
@@ -552,6 +568,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   };
   int64_t dbase = warp_id * GPW;
   int b = 0;
+  unsigned hsec = 0, hrun = 0;  // host sectors / runs of the adjacency misses (warp-uniform)
   int32_t v = fetch_v(dbase, 0);
   int4 e0, e1;
   fetch_dir(v, e0, e1);
@@ -577,10 +594,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     const int32_t rank = select_rank<G>(gl, lane, gmask, f, deg, floyd, S.seed[b], a.pass, (uint32_t)h, (uint32_t)v);
     const int pos = gl;
     const bool valid = active && gl < k;
-    {
-      const unsigned nl = host_sectors_opened<G>(valid && rank >= cached_len, host_off + rank, gl);
-      if (lane == 0 && nl) atomicAdd(&S.host_sectors, nl);
-    }
+    host_miss_counts<G>(valid && rank >= cached_len, host_off + rank, gl, hsec, hrun);
     int32_t x = -1;
     const bool hit = valid && rank < cached_len;
     if (valid) {
@@ -610,6 +624,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
     e1 = e1_next;
     v_next = v_next2;
   }
+  host_miss_flush(S, hsec, hrun);
   hop_shared_flush(a, S);
 }
 
@@ -639,6 +654,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
   const long long total = S.pre[a.n];
   const uint64_t keep = policy_evict_last();
   const uint64_t epol = policy_by(a.elem_policy);
+  unsigned hsec = 0, hrun = 0;  // host sectors / runs of the adjacency misses (warp-uniform)
   for (int64_t q = tid >> 5; q < total; q += nthreads >> 5) {
     const int b = batch_of(S.pre, a.n, q);
     const HopBatch& hb = a.b[b];
@@ -700,6 +716,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
     // element reads in sorted-rank order: pos -> rank (all lanes run every pass: the host-sector
     // count shuffles across the warp, carrying the previous pass's last miss sector)
     long long carry_line = -1;
+    bool any_miss = false;  // this dst's run had a miss (one run per dst, warp-uniform)
     for (int base = 0; base < f; base += 32) {
       const int pos = base + lane;
       {
@@ -716,7 +733,8 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
         const unsigned missm = __ballot_sync(0xffffffffu, miss);
         const long long last = __shfl_sync(0xffffffffu, line, 31);
         carry_line = (missm >> 31) & 1u ? last : -1;
-        if (lane == 0 && opened) atomicAdd(&S.host_sectors, (unsigned)__popc(opened));
+        hsec += __popc(opened);
+        any_miss |= missm != 0u;
       }
       if (pos >= f) continue;
       int32_t x = -1;
@@ -736,8 +754,10 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
       hb.cand[d * f + pos] = x;
     }
     if (lane == 0) hb.kcnt[d] = k;
+    hrun += any_miss ? 1u : 0u;
     __syncwarp();
   }
+  host_miss_flush(S, hsec, hrun);
   hop_shared_flush(a, S);
 }
 

@@ -40,7 +40,7 @@ __device__ __forceinline__ uint64_t perm(uint64_t x, int bits) {
 
 // load kinds: 0 = ld.global.nc.L1::no_allocate (round 1's miss-path load), 1 = plain ld.global
 // (L1-allocating; the library's miss-path load since round 2), 2 = ld.global.L1::no_allocate
-// (coherent), 3 = ld.global.nc (read-only path, L1-allocating)
+// (coherent), 3 = ld.global.nc (read-only path, L1-allocating); plus TMA bulk copies ("bulk")
 __device__ int g_kind_dummy;
 template <int KIND>
 __device__ __forceinline__ int ld32(const int* p) {
@@ -130,6 +130,52 @@ __global__ void rand_wide(const char* __restrict__ src, int bits, int iters, int
   if (acc == 0x12345678) sink[0] = acc;
 }
 
+
+// S-byte random reads by TMA bulk copies (cp.async.bulk global -> shared, mbarrier completion):
+// lane 0 of each warp keeps U requests in flight in a U-slot ring (the row-mode group gather's
+// miss path reads host rows this way)
+template <int S, int U>
+__global__ void rand_bulk(const char* __restrict__ src, int bits, int iters, int* sink) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) unsigned long long bar[8][U];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned char* mine = ring + (size_t)wib * U * S;
+  if (lane == 0) {
+    for (int u = 0; u < U; ++u)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar[wib][u])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  int acc = 0;
+  if (lane == 0) {
+    const int total = iters * U;
+    auto issue = [&](int k) {
+      const int u = k % U;
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[wib][u]);
+      const uint64_t slot = perm((uint64_t)k * nw + gw, bits);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(S) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(mine + (size_t)u * S)),
+                   "l"(src + slot * S), "r"(S), "r"(b)
+                   : "memory");
+    };
+    for (int k = 0; k < U && k < total; ++k) issue(k);
+    for (int k = 0; k < total; ++k) {
+      const int u = k % U;
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[wib][u]);
+      const uint32_t par = (uint32_t)((k / U) & 1);
+      asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(b),
+                   "r"(par)
+                   : "memory");
+      acc ^= mine[(size_t)u * S];
+      if (k + U < total) issue(k + U);
+    }
+  }
+  if (acc == 0x12345678) sink[0] = acc;
+}
+
 template <int S, int KIND>
 static double run(const char* src, size_t region, int* sink, int sms, double* mreq) {
   int bits = 0;
@@ -168,6 +214,38 @@ static double run(const char* src, size_t region, int* sink, int sms, double* mr
   return nreq * S / best / 1e6;  // payload GB/s
 }
 
+
+template <int S>
+static double run_bulk_probe(const char* src, size_t region, int* sink, int sms, double* mreq) {
+  int bits = 0;
+  while ((2ull << bits) <= region / S) ++bits;
+  constexpr int U = 8;
+  const int warps = 8, grid = sms * 2;
+  const size_t smem = (size_t)warps * U * S;
+  CK(cudaFuncSetAttribute(rand_bulk<S, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const double per_iter = (double)grid * warps * U;
+  const int iters = (int)std::min(64.0, std::max(1.0, std::min((double)(1ull << bits) / 2, 8.0e6) / per_iter));
+  const double nreq = per_iter * iters;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  rand_bulk<S, U><<<grid, 32 * warps, smem>>>(src, bits, iters, sink);
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    CK(cudaEventRecord(a));
+    rand_bulk<S, U><<<grid, 32 * warps, smem>>>(src, bits, iters, sink);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (ms < best) best = ms;
+  }
+  CK(cudaGetLastError());
+  *mreq = nreq / best / 1e3;
+  return nreq * S / best / 1e6;
+}
+
 int main(int argc, char** argv) {
   const double max_gb = argc > 1 ? atof(argv[1]) : 64.0;
   int sms;
@@ -194,6 +272,13 @@ int main(int argc, char** argv) {
   fflush(stdout);
 #define ONE(S) ONEK(S, 0) ONEK(S, 1) ONEK(S, 2) ONEK(S, 3)
     ONE(4) ONE(32) ONE(64) ONE(128) ONE(256) ONE(512) ONE(2048)
+#define BULK(S)                                                                                                \
+  g = run_bulk_probe<S>(src, region, sink, sms, &m);                                                           \
+  printf("{\"probe\":\"host_random_read\",\"region_GB\":%.1f,\"bytes\":%d,\"load\":\"bulk\",\"Mreq_per_s\":%.1f," \
+         "\"GBps\":%.2f}\n",                                                                                    \
+         gb, S, m, g);                                                                                         \
+  fflush(stdout);
+    BULK(512) BULK(2048)
   }
   CK(cudaFreeHost(h));
   return 0;
