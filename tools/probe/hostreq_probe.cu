@@ -176,6 +176,33 @@ __global__ void rand_bulk(const char* __restrict__ src, int bits, int iters, int
   if (acc == 0x12345678) sink[0] = acc;
 }
 
+
+// Mixed pattern (512-B rows, plain loads): a fraction hot_pct/100 of the requests go to the first
+// 2^hot_bits slots (a compact "warm" sub-region), the rest to the whole region -- does a warm
+// sub-region keep its translations while the rest of the requests thrash the TLB?
+__global__ void rand_mixed512(const char* __restrict__ src, int bits, int hot_bits, int hot_pct, int iters, int* sink) {
+  constexpr int S = 512, L = 32, U = 8;
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t ngrp = (uint64_t)gridDim.x * blockDim.x / L;
+  const uint64_t grp = t / L;
+  const int gl = (int)(t % L);
+  int acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    int v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = ((uint64_t)(it * U + u)) * ngrp + grp;
+      const bool hot = (perm(idx ^ 0x5bd1e995ull, 20) % 100) < (uint64_t)hot_pct;
+      const uint64_t slot = hot ? perm(idx, hot_bits) : perm(idx, bits);
+      const int4 x = ld128<1>(reinterpret_cast<const int4*>(src + slot * S) + gl);
+      v[u] = x.x ^ x.w;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u];
+  }
+  if (acc == 0x12345678) sink[0] = acc;
+}
+
 template <int S, int KIND>
 static double run(const char* src, size_t region, int* sink, int sms, double* mreq) {
   int bits = 0;
@@ -259,8 +286,9 @@ int main(int argc, char** argv) {
   int* sink;
   CK(cudaMalloc(&sink, 64));
   const double regions[] = {0.5, 1, 2, 8, 32, 64};
+  const bool mixed_only = argc > 2 && argv[2][0] == 'm';
   for (double gb : regions) {
-    if (gb > max_gb) break;
+    if (gb > max_gb || mixed_only) break;
     const size_t region = (size_t)(gb * (1ull << 30));
     const char* src = static_cast<const char*>(hd);
     double m, g;
@@ -279,6 +307,38 @@ int main(int argc, char** argv) {
          gb, S, m, g);                                                                                         \
   fflush(stdout);
     BULK(512) BULK(2048)
+  }
+  // mixed warm / cold pattern over the largest region
+  {
+    const size_t region = (size_t)(max_gb * (1ull << 30));
+    int bits = 0;
+    while ((2ull << bits) <= region / 512) ++bits;
+    for (double hot_gb : {1.0, 2.0}) {
+      int hb = 0;
+      while ((2ull << hb) <= (size_t)(hot_gb * (1ull << 30)) / 512) ++hb;
+      for (int pct : {0, 30, 50, 100}) {
+        const int grid = sms * 8, threads = 256, iters = 4;
+        const double nreq = (double)grid * threads / 32 * 8 * iters;
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        rand_mixed512<<<grid, threads>>>(static_cast<const char*>(hd), bits, hb, pct, iters, sink);
+        CK(cudaDeviceSynchronize());
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+          CK(cudaEventRecord(a));
+          rand_mixed512<<<grid, threads>>>(static_cast<const char*>(hd), bits, hb, pct, iters, sink);
+          CK(cudaEventRecord(b));
+          CK(cudaEventSynchronize(b));
+          float ms;
+          CK(cudaEventElapsedTime(&ms, a, b));
+          if (ms < best) best = ms;
+        }
+        printf("{\"probe\":\"host_mixed_512\",\"region_GB\":%.1f,\"hot_GB\":%.1f,\"hot_pct\":%d,\"Mreq_per_s\":%.1f,"
+               "\"GBps\":%.2f}\n", max_gb, hot_gb, pct, nreq / best / 1e3, nreq * 512 / best / 1e6);
+        fflush(stdout);
+      }
+    }
   }
   CK(cudaFreeHost(h));
   return 0;
