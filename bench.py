@@ -290,6 +290,16 @@ def light_check(cfg, ip, ix, c_adj, c_feat, gpu_results, npre=8, rows=4096):
                     "vs the closed-form features"}
 
 
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_results=None, npre=8):
     """Time the oracle as it stands on host cores: its own presample + fill (reported), then
     inference batches spread over `threads` threads (ctypes releases the GIL), until about
@@ -328,7 +338,7 @@ def oracle_leg(cfg, ip, ix, ft, c_adj, c_feat, batches, seconds, threads, gpu_re
         list(ex.map(one_batch, work))
     wall = time.time() - t2
     seeds = sum(len(s) for s in work)
-    return {"value": seeds / wall, "unit": UNIT, "cores": threads, "kind": "oracle",
+    return {"value": seeds / wall, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": _cpu_model(),
             "sample": f"{nb} batches of {B} seeds ({cfg.name}, {','.join(map(str, fan))}) after the oracle's own "
                       f"presample+fill ({prep_s:.1f} s, not timed); {wall:.1f} s wall on {threads} threads"}, check
 
