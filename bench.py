@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle wall time for cpu_baseline")
     ap.add_argument("--no-check", action="store_true", help="skip the bit-exact spot check vs the oracle")
+    ap.add_argument("--no-aggregate", action="store_true",
+                    help="skip timing the NEXT F2 mean-aggregate consumer after the timed region")
     ap.add_argument("--check-light", action="store_true",
                     help="full-size parity without a host feature copy: oracle presample/fill/sampling on the "
                          "same graph, X rows checked against the closed-form features (papers100M-shaped)")
@@ -666,6 +668,44 @@ def run_ours(args):
             alone = {"achieved": st0["gather_bytes"] / (st0["gather_ms"] / 1e3) / 1e9,
                      "avg_gather_ms": st0["gather_ms"] / max(1, st0["gather_launches"]),
                      "launches": st0["gather_launches"]}
+    # ---- NEXT F2: the GraphSAGE mean-aggregate consumer over the input-layer block of the last
+    # timed outputs (one dci_mean_aggregate launch per batch), timed alone with CUDA events ----
+    consumer = None
+    if not args.no_aggregate:
+        agg_outs = outs[0][:per]
+        torch.cuda.synchronize()
+        n_dst = [int(o.sizes[L - 1].item()) for o in agg_outs]
+        n_src = [int(o.sizes[L].item()) for o in agg_outs]
+        n_edge = [int(o.bptr[L - 1][n_dst[i]].item()) for i, o in enumerate(agg_outs)]
+        Hs = [torch.empty((max(o.bptr[L - 1].numel() - 1, 1), o.ldx), dtype=torch.float32, device=dev)
+              for o in agg_outs]
+        for o, Hb in zip(agg_outs, Hs):  # warm-up
+            dci.mean_aggregate(ctx, o, H=Hb, stream=main)
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a0.record(main)
+        for _ in range(reps):
+            for o, Hb in zip(agg_outs, Hs):
+                dci.mean_aggregate(ctx, o, H=Hb, stream=main)
+        a1.record(main)
+        torch.cuda.synchronize()
+        a_ms = a0.elapsed_time(a1) / reps
+        # compulsory bytes: every source row (F_L) read once + every output row written once (+ 4 B
+        # bsrc per edge, 4 B bptr per dst); edge bytes: a source row per edge (what the gather-reduce
+        # requests; re-reads of a row shared by several dsts may hit L2)
+        min_bytes = sum(4.0 * D * (sr + d) + 4.0 * (e + d) for sr, e, d in zip(n_src, n_edge, n_dst))
+        edge_bytes = sum(4.0 * D * (e + d) + 4.0 * (e + d) for e, d in zip(n_edge, n_dst))
+        hbm_pk = measured_peaks()[0]
+        consumer = {"kernel": "k_mean_aggregate_v4 (dci_mean_aggregate, input-layer block, one launch per batch)",
+                    "batches": len(agg_outs), "edges": sum(n_edge), "src_rows": sum(n_src), "dst_rows": sum(n_dst),
+                    "ms": a_ms, "GBps": min_bytes / (a_ms / 1e3) / 1e9, "peak_GBps": hbm_pk,
+                    "frac": min_bytes / (a_ms / 1e3) / 1e9 / hbm_pk,
+                    "edge_GBps": edge_bytes / (a_ms / 1e3) / 1e9,
+                    "note": "after the timed region (not part of the seeds/s metric); GBps = compulsory bytes "
+                            "(each source row read once, each output row written once) / time; edge_GBps = a "
+                            "source row per edge / time (L2 serves the re-reads)"}
     clocks = parallel.gather_clocks(clk.stop())
     clocks["window"] = "sampled every 100 ms on every rank's GPU from input generation through the e2e region"
 
@@ -803,6 +843,7 @@ def run_ours(args):
                              "aggregate_achieved = the same bytes / timed wall time; alone = the same launch "
                              "with nothing else on the GPU (3 groups after the timed region)"},
         "host_link": host_link,
+        "consumer": consumer,
         "clocks": clocks,
         "stats": {"avg_F_L": avg_fl, "F_L_per_seed": avg_fl / B, **hit_rates,
                   "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre,
