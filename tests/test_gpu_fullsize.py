@@ -178,3 +178,37 @@ def test_no_graph_path_subprocess():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "smoke ok" in r.stdout
+
+
+def test_m2_fullsize_bench_launch_configuration():
+    """configs[1] in exactly the launch configuration bench.py times: groups of 20 batches, two
+    groups in flight on two streams, X rows padded to whole 128-byte lines (ldx 608), auto budget;
+    EVERY batch of both groups bit-exact against the oracle (the bench's parity_check samples 3)."""
+    from concurrent.futures import ThreadPoolExecutor
+    cfg = synth.CONFIGS["M2"]
+    ip, ix, ft, ctx, nv, ec, nv_o, ec_o, ts, tf = _setup(cfg)
+    c_adj, c_feat = dci.allocate(ctx, 0, ts, tf)
+    fan, B, G = cfg.fanouts, cfg.batch, 20
+    ldx = -(-cfg.D // 32) * 32
+    gw = [[dci.workspace_create(ctx, B, fan) for _ in range(G)] for _ in range(2)]
+    go = [[dci.BatchOut(ctx, B, fan, ldx=ldx) for _ in range(G)] for _ in range(2)]
+    dci.fill(ctx, nv, ec, c_adj, c_feat)
+    R, cl, _, _ = oracle.adj_fill(ip, ix, ec_o, c_adj)
+    slot_o, _ = oracle.feat_fill(nv_o, c_feat // (4 * cfg.pitch_floats()))
+    batches = synth.inference_batches(ip, B)[: 2 * G]
+    sd = [torch.from_numpy(b).to(DEV) for b in batches]
+    gs = [torch.cuda.Stream() for _ in range(2)]
+    for rep in range(2):  # the second round reuses the workspaces (epochs, cached graphs)
+        for k in range(2):
+            dci.sample_gather_many(ctx, gw[k], sd[k * G:(k + 1) * G], fan, synth.SAMPLE_SEED, go[k], stream=gs[k])
+    torch.cuda.synchronize()
+    assert go[0][0].ldx == ldx
+    got = [go[i // G][i % G].result() for i in range(2 * G)]
+
+    def check(i):
+        o = oracle.sample_gather(ip, R, ft, batches[i], fan, synth.SAMPLE_SEED, cl, slot_o)
+        return _same(got[i], o, len(fan))
+
+    with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
+        ok = list(ex.map(check, range(2 * G)))
+    assert all(ok), [i for i, v in enumerate(ok) if not v]
