@@ -985,6 +985,16 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     DCI_CUDA(cudaEventRecord(ctx->gather_q_ev, gs));
     ctx->gather_q_valid = true;
   }
+  // the last hop's relabel beside the gather (default), or after it (DCI_EPI_AFTER=1, a measurement
+  // knob: the relabel's random tag reads compete with the gather's writes)
+  static const bool epi_after = [] {
+    const char* e = getenv("DCI_EPI_AFTER");
+    return e && e[0] == '1';
+  }();
+  if (epi_after && gs != s) {
+    DCI_CUDA(cudaEventRecord(w0->ev_done, gs));
+    DCI_CUDA(cudaStreamWaitEvent(s, w0->ev_done, 0));
+  }
   enqueue_epilogue(s);
   if (phased) {
     DCI_CUDA(cudaEventRecord(ctx->gather_ev, gs));

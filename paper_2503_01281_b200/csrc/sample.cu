@@ -1193,7 +1193,13 @@ void launch_hop_epilogue(dci_ctx* ctx, dci_workspace* const* ws, const HopParams
   int64_t items = 0;
   for (int i = 0; i < n; ++i) items += ws[i]->hop_cap[p[0].hop - 1] * p[0].prev_f;
   const int64_t need = std::max<int64_t>(1, (items + 255) / 256);
-  const int grid = (int)std::min<int64_t>(persistent_grid(ctx, k_hop_epilogue, 256, 8), need);
+  // DCI_EPI_BLOCKS caps the grid (a measurement knob: the relabel runs beside the group gather)
+  static const int cap = [] {
+    const char* e = getenv("DCI_EPI_BLOCKS");
+    return e ? atoi(e) : 0;
+  }();
+  int grid = (int)std::min<int64_t>(persistent_grid(ctx, k_hop_epilogue, 256, 8), need);
+  if (cap > 0 && grid > cap) grid = cap;
   k_hop_epilogue<<<grid, 256, 0, s>>>(a);
   ++ctx->launches;
 }
