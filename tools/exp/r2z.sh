@@ -1,5 +1,5 @@
 # round-2 closing evidence with the final code (one B200)
-mkdir -p gpurun_out/fin gpurun_out/san
+mkdir -p gpurun_out/fin gpurun_out/san; rm -rf gpurun_out/fin/* gpurun_out/prof_fin
 timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -4 > gpurun_out/fin/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin/smoke.txt 2>&1
 bash tools/sanitize.sh > gpurun_out/fin/sanitize_summary.txt 2>&1
