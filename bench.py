@@ -728,7 +728,12 @@ def run_ours(args):
     bind_b = host_b if host_bound else hbm_b
     bind_peak = host_peak if host_bound else hbm_peak
     n_launch = max(1.0, tot[7])
-    achieved_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per launch (live events)
+    per_launch_gbs = bind_b / (tot[4] / 1e3) / 1e9 if tot[4] > 0 else None  # per launch (live events)
+    # single-batch calls with several in flight run their gather launches concurrently, so one
+    # launch's own rate says little (round-1 VERDICT): there `achieved` is the aggregate over the
+    # timed wall time; group gathers run one at a time on the gather stream: per launch
+    overlapped = (G == 0 and nws > 1)
+    achieved_gbs = (bind_b / (ms_tot / 1e3) / 1e9) if overlapped else per_launch_gbs
     # the group gather kernels the timed regions launched (the library picks the node sweep's kernel
     # per launch: bulk copies when nothing is queued ahead of the gather, register copies otherwise)
     knames = ["k_gather_tma (rows)", "k_gather_sweep (register copies)", "k_gather_sweep_tma (bulk copies)"]
@@ -829,6 +834,9 @@ def run_ours(args):
         "roofline": {"bound": "host-link" if host_bound else "hbm",
                      "kernel": kernel,
                      "achieved": achieved_gbs, "peak": bind_peak,
+                     "achieved_kind": ("aggregate over the timed regions (overlapping single-batch gather launches)"
+                                       if overlapped else "per gather launch (group gathers run one at a time)"),
+                     "per_launch_achieved": per_launch_gbs,
                      "peak_kind": host_kind if host_bound else peak_kind, "unit": "GB/s",
                      "frac": (achieved_gbs / bind_peak) if achieved_gbs else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": bind_b / n_launch, "launches": int(tot[7]),
@@ -839,8 +847,9 @@ def run_ours(args):
                      "alone": None if alone is None or host_bound else dict(alone, frac=alone["achieved"] / bind_peak),
                      "pattern": pattern,
                      "note": "achieved = algorithmic bytes per gather launch / mean live launch time (CUDA events "
-                             "on the launch stream); group gathers run one at a time on the gather stream. "
-                             "aggregate_achieved = the same bytes / timed wall time; alone = the same launch "
+                             "on the launch stream) for group gathers, which run one at a time on the gather "
+                             "stream; for overlapping single-batch launches the same bytes / timed wall time. "
+                             "aggregate_achieved = the bytes / timed wall time; alone = the same launch "
                              "with nothing else on the GPU (3 groups after the timed region)"},
         "host_link": host_link,
         "consumer": consumer,
