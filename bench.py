@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle wall time for cpu_baseline")
     ap.add_argument("--no-check", action="store_true", help="skip the bit-exact spot check vs the oracle")
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-batch latency measurement")
     ap.add_argument("--no-aggregate", action="store_true",
                     help="skip timing the NEXT F2 mean-aggregate consumer after the timed region")
     ap.add_argument("--check-light", action="store_true",
@@ -290,6 +291,22 @@ def light_check(cfg, ip, ix, c_adj, c_feat, gpu_results, npre=8, rows=4096):
     return {"batches": len(gpu_results), "bit_exact": ok,
             "mode": f"light: oracle presample+fill+sampling on the full graph, X on {rows} random rows per batch "
                     "vs the closed-form features"}
+
+
+def host_mem() -> dict:
+    """This process's host memory from /proc/self/status (GB): private anonymous pages, shared-memory
+    pages it maps (the node-shared adopted graph counts here, once per node), and the peak RSS."""
+    out = {}
+    try:
+        with open("/proc/self/status") as f:
+            for ln in f:
+                k, _, v = ln.partition(":")
+                if k in ("RssAnon", "RssShmem", "RssFile", "VmHWM"):
+                    out[k] = int(v.split()[0]) / 2 ** 20  # kB -> GB
+    except OSError:
+        pass
+    return {"rss_anon_GB": out.get("RssAnon"), "rss_shmem_GB": out.get("RssShmem"),
+            "rss_file_GB": out.get("RssFile"), "peak_rss_GB": out.get("VmHWM")}
 
 
 def _cpu_model() -> str:
@@ -668,6 +685,28 @@ def run_ours(args):
             alone = {"achieved": st0["gather_bytes"] / (st0["gather_ms"] / 1e3) / 1e9,
                      "avg_gather_ms": st0["gather_ms"] / max(1, st0["gather_launches"]),
                      "launches": st0["gather_launches"]}
+    # ---- batch latency (latency-bound configs report it next to seeds/s): one
+    # single-batch dci_sample_gather call at a time on device-resident seeds, synchronised, CUDA
+    # events on its stream; launches per batch from the library's launch counter ----
+    latency = None
+    if not args.no_latency:
+        w0, o0 = wss[0][0], outs[0][0]
+        for r in range(3):  # the single-batch shape's graph is captured here, outside the timing
+            dci.sample_gather(ctx, w0, seeds_dev[r % len(seeds_dev)], fan, synth.SAMPLE_SEED, o0, stream=streams[0])
+        torch.cuda.synchronize()
+        lts, l0, ncall = [], ctx.launches, 20
+        for r in range(ncall):
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(streams[0])
+            dci.sample_gather(ctx, w0, seeds_dev[r % len(seeds_dev)], fan, synth.SAMPLE_SEED, o0, stream=streams[0])
+            a1.record(streams[0])
+            a1.synchronize()
+            lts.append(a0.elapsed_time(a1) * 1e3)
+        latency = {"us_median": float(np.median(lts)), "us_min": float(np.min(lts)), "us_max": float(np.max(lts)),
+                   "launches_per_batch": (ctx.launches - l0) / ncall, "calls": ncall,
+                   "note": "one single-batch dci_sample_gather at a time (B seeds on the device, nothing else "
+                           "queued), after the timed regions; not part of the seeds/s value"}
     # ---- NEXT F2: the GraphSAGE mean-aggregate consumer over the input-layer block of the last
     # timed outputs (one dci_mean_aggregate launch per batch), timed alone with CUDA events ----
     consumer = None
@@ -708,6 +747,11 @@ def run_ours(args):
                             "source row per edge / time (L2 serves the re-reads)"}
     clocks = parallel.gather_clocks(clk.stop())
     clocks["window"] = "sampled every 100 ms on every rank's GPU from input generation through the e2e region"
+    hm = host_mem()
+    host_memory = dict(hm, max_rss_anon_GB_over_ranks=parallel.max_over_ranks(hm["rss_anon_GB"] or 0.0, device=dev),
+                       note="rank 0's /proc/self/status at the end of the run; anon = private to the rank, "
+                            "shmem = shared mappings: the node-shared adopted graph and the library's pinned "
+                            "(cudaHostAlloc) host copies")
 
     e_value = seeds_all / (ems / 1e3)
 
@@ -853,6 +897,8 @@ def run_ours(args):
                              "with nothing else on the GPU (3 groups after the timed region)"},
         "host_link": host_link,
         "consumer": consumer,
+        "latency": latency,
+        "host_memory": host_memory,
         "clocks": clocks,
         "stats": {"avg_F_L": avg_fl, "F_L_per_seed": avg_fl / B, **hit_rates,
                   "preprocess_s": {"generate": t_gen, "load": t_load, "presample": t_pre,
