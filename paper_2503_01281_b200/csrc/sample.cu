@@ -36,12 +36,6 @@ __device__ __forceinline__ int32_t ld_host_i32(const int32_t* p) {
   return v;
 }
 
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
 __device__ __forceinline__ int32_t ld_keep_i32(const int32_t* p, uint64_t pol) {
   int32_t v;
   asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -83,7 +77,9 @@ struct HopLaunch {
   int64_t N;
   int32_t hop, f, prev_f, n;
   uint32_t pass;
-  int32_t elem_policy;  // L2 policy of adjacency-cache element loads: 0 evict-last, 1 normal, 2 evict-first
+  int32_t elem_policy;  // L2 policy of adjacency-cache element loads: 0 evict-last, 1 normal (default), 2 evict-first
+  int32_t dir_policy;   // L2 policy of directory-entry loads (same codes; default normal: evict-last measured
+                        // 1 % slower on M2 and 3.6 % on M4s -- lines pinned in L2 crowd out the gather's)
   int32_t* edge_counts; // presample only (nullable, n = 1)
   int32_t precheck;     // read the tag before the atomicMax (DCI_PRECHECK=1; measured slower on M2)
   int32_t sweep;        // node-sweep sampling allowed (multi-batch hops covering >= N nodes)
@@ -531,7 +527,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const __grid_constant__ HopL
   const int GPW = 32 / G;
   const int64_t warp_id = tid >> 5;
   const int64_t nwarps = nthreads >> 5;
-  const uint64_t keep = policy_evict_last();
+  const uint64_t keep = policy_by(a.dir_policy);
   const uint64_t epol = policy_by(a.elem_policy);
   // (not at hop 0: the seeds' table tags are written by this kernel's own prologue, so they are
   // not final until the kernel ends; from hop 1 on, F_h's tags were finalised by the last scan)
@@ -652,7 +648,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_sample_hop_wide(const __gri
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   hop_prologue(a, S, tid, nthreads);
   const long long total = S.pre[a.n];
-  const uint64_t keep = policy_evict_last();
+  const uint64_t keep = policy_by(a.dir_policy);
   const uint64_t epol = policy_by(a.elem_policy);
   unsigned hsec = 0, hrun = 0;  // host sectors / runs of the adjacency misses (warp-uniform)
   for (int64_t q = tid >> 5; q < total; q += nthreads >> 5) {
@@ -1053,7 +1049,7 @@ __global__ void __launch_bounds__(kScanTile) k_scan_hop(const __grid_constant__ 
 static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopParams* p, int32_t n) {
   static const int elem_policy = [] {
     const char* e = getenv("DCI_ELEM_POLICY");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   HopLaunch a;
   memset(&a, 0, sizeof(a));
@@ -1067,6 +1063,11 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
   a.n = n;
   a.pass = p[0].pass;
   a.elem_policy = elem_policy;
+  static const int dir_policy = [] {
+    const char* e = getenv("DCI_DIR_POLICY");
+    return e ? atoi(e) : 1;
+  }();
+  a.dir_policy = dir_policy;
   a.edge_counts = p[0].edge_counts;
   static const int precheck = [] {
     const char* e = getenv("DCI_PRECHECK");
