@@ -56,6 +56,12 @@ def test_bench_line_m1(group):
     assert d["parity_check"]["bit_exact"] is True
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["cores"] >= 1 and cb["unit"] == d["unit"]
+    # single-batch latency (latency-bound configs) and per-rank host memory
+    lat = d["latency"]
+    assert lat["calls"] > 0 and 0 < lat["us_min"] <= lat["us_median"] <= lat["us_max"]
+    assert lat["launches_per_batch"] >= 1
+    hm = d["host_memory"]
+    assert hm["rss_anon_GB"] is not None and hm["rss_anon_GB"] > 0 and hm["peak_rss_GB"] >= hm["rss_anon_GB"]
 
 
 def test_bench_reference_arm_m1():
