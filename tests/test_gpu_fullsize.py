@@ -156,7 +156,9 @@ def test_workspace_stats_and_graph_recapture():
                                  {"DCI_SWEEP_KIND": "tma"}, {"DCI_SWEEP_KIND": "tma", "DCI_SWEEP_WARPS": "2"},
                                  {"DCI_SWEEP_BPS": "1", "DCI_SWEEP_SMS": "20"}, {"DCI_SPLIT_GATHER": "0"},
                                  {"DCI_SPLIT_GATHER": "1", "DCI_GRAPH": "0"}, {"DCI_SPLIT_GATHER": "1", "DCI_PHASED": "2"},
-                                 {"DCI_SPLIT_GATHER": "1", "DCI_SWEEP_KIND": "ldg"}, {"DCI_NMASK_SWEEP": "0"}])
+                                 {"DCI_SPLIT_GATHER": "1", "DCI_SWEEP_KIND": "ldg"}, {"DCI_NMASK_SWEEP": "0"},
+                                 {"DCI_ELEM_POLICY": "0", "DCI_DIR_POLICY": "0"},
+                                 {"DCI_ELEM_POLICY": "2", "DCI_DIR_POLICY": "2"}])
 def test_gather_variants_subprocess(env):
     """Process-wide switches (read once per process): the TMA gather for single-batch
     calls, row mode for groups, group gathers on the caller's stream, a small TMA ring, phased
