@@ -1173,6 +1173,11 @@ void launch_newmask_sweep(dci_ctx* ctx, dci_workspace* const* ws, const HopParam
   const HopLaunch a = hop_launch(ctx, ws, p, n);
   if (!(a.nmask_on && n >= 2 && a.f >= 3 && a.f <= 32 && a.hop >= 1 && a.sweep && a.edge_counts == nullptr))
     return;
+  // the frontiers' capacities bound their sizes: below N together, the hop cannot sweep (the
+  // kernel would exit at once), so nothing is launched
+  int64_t cap = 0;
+  for (int i = 0; i < n; ++i) cap += ws[i]->hop_cap[p[i].hop];
+  if (cap < ctx->N) return;
   const int64_t grid = std::min<int64_t>(persistent_grid(ctx, k_newmask_sweep, 256, 8), (ctx->N + 255) / 256);
   k_newmask_sweep<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, s>>>(a);
   ++ctx->launches;
