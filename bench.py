@@ -403,7 +403,15 @@ def run_ours(args):
     import paper_2503_01281_b200 as dci
     from paper_2503_01281_b200 import parallel
 
-    rank, world, local = parallel.init(args.backend)
+    backend = args.backend
+    ndev = torch.cuda.device_count()
+    if backend == "nccl" and parallel.dist_env()[1] > ndev:
+        # NCCL refuses two ranks on one device: more ranks than visible GPUs run over gloo
+        print(f"[bench] note: {parallel.dist_env()[1]} ranks on {ndev} visible GPU(s): gloo instead of nccl",
+              file=sys.stderr)
+        backend = "gloo"
+    args.backend = backend
+    rank, world, local = parallel.init(backend)
     if world != args.gpus:
         print(f"[bench] note: {world} ranks launched with --gpus {args.gpus}; n_gpus reports the ranks",
               file=sys.stderr)
