@@ -429,9 +429,11 @@ def run_ours(args):
     # ---- inputs + S0 load.  Several ranks on one node share ONE host copy of the graph
     # (parallel.SharedGraph: local rank 0 generates it into /dev/shm, every rank's context adopts it
     # in place with DCI_ADOPT_HOST) instead of a copy per rank ----
-    use_shm = world > 1 and args.shm_graph != "off" and parallel.SharedGraph.fits(cfg.N, cfg.E, cfg.D)
+    # (auto: with several ranks; on: also a single rank, e.g. to pin papers100M-shaped data once)
+    use_shm = ((world > 1 and args.shm_graph == "auto") or args.shm_graph == "on") and \
+        parallel.SharedGraph.fits(cfg.N, cfg.E, cfg.D)
     if args.shm_graph == "on" and not use_shm:
-        raise SystemExit("--shm-graph on: /dev/shm cannot hold the graph (or a single rank)")
+        raise SystemExit("--shm-graph on: /dev/shm cannot hold the graph")
     t0 = time.time()
     sg = None
     if use_shm:
@@ -941,6 +943,8 @@ def run_ours(args):
         gpu_results = check_batches()
         line["parity_check"] = light_check(cfg, ip, ix, c_adj, c_feat, gpu_results, npre=args.presample_batches)
     if not args.profile_only and world == 1 and not args.no_cpu_baseline:
+        if ft is None and sg is not None:  # single rank over the adopted shared graph
+            ft = np.ascontiguousarray(sg.feats[:, :cfg.D])
         gpu_results = None
         if not args.no_check:
             gpu_results = check_batches()
