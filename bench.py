@@ -563,11 +563,15 @@ def run_ours(args):
         nxt[0] += nb
         return sel
 
+    calls = {}  # (stream slot, group size) -> dci.GroupCall (workspaces, outputs, fan-outs marshalled once)
+
     def step(i, nb):
         w = i % nws
         if G:
-            dci.sample_gather_many(ctx, wss[w][:nb], take(seeds_dev, nb), fan, synth.SAMPLE_SEED, outs[w][:nb],
-                                   stream=streams[w])
+            gc = calls.get((w, nb))
+            if gc is None:
+                gc = calls[(w, nb)] = dci.GroupCall(ctx, wss[w][:nb], fan, outs[w][:nb])
+            gc(take(seeds_dev, nb), synth.SAMPLE_SEED, stream=streams[w])
         else:
             dci.sample_gather(ctx, wss[w][0], take(seeds_dev, 1)[0], fan, synth.SAMPLE_SEED, outs[w][0],
                               stream=streams[w])

@@ -77,6 +77,30 @@ def test_many_parity(filled, n):
         assert 0 < hits  # both feature paths (HBM hit rows, host miss rows) are exercised
 
 
+def test_group_call_repeated_bit_exact(filled):
+    """dci.GroupCall (workspaces, outputs and fan-outs marshalled once) gives every batch the
+    oracle's outputs, call after call with new seeds on a side stream, and checks its seeds."""
+    ip, R, ft, ctx, cl, slot, fan, B = filled
+    batches = synth.inference_batches(ip, B)
+    n = 6
+    wss = [dci.workspace_create(ctx, B, fan) for _ in range(n)]
+    outs = [dci.BatchOut(ctx, B, fan) for _ in range(n)]
+    gc = dci.GroupCall(ctx, wss, fan, outs)
+    st = torch.cuda.Stream()
+    for rep in range(3):
+        group = [batches[(rep * n + i) % len(batches)] for i in range(n)]
+        seeds = [torch.from_numpy(np.ascontiguousarray(s, np.int32)).to(DEV) for s in group]
+        gc(seeds, synth.SAMPLE_SEED, stream=st)
+        st.synchronize()
+        for s, o_gpu in zip(group, outs):
+            _assert_batch_equal(o_gpu.result(), oracle.sample_gather(ip, R, ft, s, fan, synth.SAMPLE_SEED, cl, slot),
+                                len(fan))
+    with pytest.raises(TypeError):
+        gc([torch.zeros(4, dtype=torch.int64, device=DEV)] * n, synth.SAMPLE_SEED)
+    with pytest.raises(ValueError):
+        gc(seeds[:2], synth.SAMPLE_SEED)
+
+
 @pytest.fixture(scope="module", params=[(32, 0.3), (602, 0.3), (100, 2.0)])
 def dense(request):
     """A small graph where one batch touches most nodes, so groups take the node-sweep path

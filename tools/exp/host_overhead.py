@@ -32,6 +32,8 @@ def t_host(f, reps=50):
     return 1e6 * float(np.median(ts))
 
 print("call_us", t_host(lambda: dci.sample_gather_many(ctx, wss, seeds, fan, 4, outs, stream=st)))
+gc = dci.GroupCall(ctx, wss, fan, outs)
+print("groupcall_us", t_host(lambda: gc(seeds, 4, stream=st)))
 print("check_us", t_host(lambda: [dci._device_i32(s, "seeds", 0) for s in seeds]))
 print("record_us", t_host(lambda: [dci._record(s, st) for s in seeds]))
 print("outs_record_us", t_host(lambda: [o.record_stream(st) for o in outs]))
@@ -56,12 +58,12 @@ def region_preq():
     x = torch.cuda.Event(); x.record(st); m.wait_event(x); e1.record(m)
     torch.cuda.synchronize(); return e0.elapsed_time(e1) * 1e3
 print("region_us", float(np.median([region() for _ in range(30)])))
+def region_gc():
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    m = torch.cuda.current_stream()
+    e0.record(m); st.wait_event(e0)
+    gc(seeds, 4, stream=st)
+    x = torch.cuda.Event(); x.record(st); m.wait_event(x); e1.record(m)
+    torch.cuda.synchronize(); return e0.elapsed_time(e1) * 1e3
+print("region_groupcall_us", float(np.median([region_gc() for _ in range(30)])))
 print("region_prequeued_us", float(np.median([region_preq() for _ in range(30)])))
-import cProfile, pstats
-pr = cProfile.Profile()
-pr.enable()
-for _ in range(200):
-    dci.sample_gather_many(ctx, wss, seeds, fan, 4, outs, stream=st)
-    torch.cuda.synchronize()
-pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
