@@ -657,8 +657,10 @@ def run_ours(args):
     def estep(i, nb):
         w = i % nws
         if G:
-            dci.sample_gather_many_host(ctx, wss[w][:nb], take(pinned_seeds, nb), fan, synth.SAMPLE_SEED,
-                                        outs[w][:nb], e_res[w], stream=streams[w])
+            gc = calls.get((w, nb))
+            if gc is None:
+                gc = calls[(w, nb)] = dci.GroupCall(ctx, wss[w][:nb], fan, outs[w][:nb])
+            gc.host(take(pinned_seeds, nb), synth.SAMPLE_SEED, e_res[w], stream=streams[w])
         else:
             dci.sample_gather_host(ctx, wss[w][0], take(pinned_seeds, 1)[0], fan, synth.SAMPLE_SEED,
                                    outs[w][0], e_sizes[w, 0], e_cnt[w, 0], e_st[w, 0], stream=streams[w])

@@ -453,6 +453,25 @@ class GroupCall:
                                             self.fan.ctypes.data, len(self.fan), seed, self.out_arr,
                                             st.cuda_stream), "dci_sample_gather_many")
 
+    def host(self, seeds_host_list, seed: int, results_host=None, stream=None):
+        """The dci_sample_gather_many_host form: pinned host seed tensors in, every batch's
+        sizes / counters / status back in one copy into results_host (see result_buffer)."""
+        import torch
+        if len(seeds_host_list) != self.n:
+            raise ValueError(f"expected {self.n} seed tensors")
+        st = torch.cuda.current_stream() if stream is None else stream
+        for i, sd in enumerate(seeds_host_list):
+            _host_i32(sd, "seeds_host")
+            self.sd_arr[i] = sd.data_ptr()
+            self.b_arr[i] = sd.numel()
+        for o in self.outs:
+            o.record_stream(st)
+        assert results_host is None or (results_host.shape[0] >= self.n and results_host.shape[-1] == RESULT_WORDS)
+        _check(lib().dci_sample_gather_many_host(self.ctx.handle, self.n, self.ws_arr, self.sd_arr, self.b_arr,
+                                                 self.fan.ctypes.data, len(self.fan), seed, self.out_arr,
+                                                 results_host.data_ptr() if results_host is not None else None,
+                                                 st.cuda_stream), "dci_sample_gather_many_host")
+
 
 MAX_LAYERS = 8
 RESULT_WORDS =MAX_LAYERS + 1 + 4 + 1  # dci_batch_result as int64 words: sizes[9], counters[4], status|pad

@@ -95,6 +95,17 @@ def test_group_call_repeated_bit_exact(filled):
         for s, o_gpu in zip(group, outs):
             _assert_batch_equal(o_gpu.result(), oracle.sample_gather(ip, R, ft, s, fan, synth.SAMPLE_SEED, cl, slot),
                                 len(fan))
+    # the host-seed form: pinned seeds in, results in one copy
+    group = [batches[(7 + i) % len(batches)] for i in range(n)]
+    hs = [torch.from_numpy(np.ascontiguousarray(s, np.int32)).pin_memory() for s in group]
+    res = dci.result_buffer(n)
+    gc.host(hs, synth.SAMPLE_SEED, res, stream=st)
+    st.synchronize()
+    parsed = dci.parse_results(res, len(fan))
+    for s, o_gpu, r in zip(group, outs, parsed):
+        o = oracle.sample_gather(ip, R, ft, s, fan, synth.SAMPLE_SEED, cl, slot)
+        _assert_batch_equal(o_gpu.result(), o, len(fan))
+        assert r["status"] == 0 and np.array_equal(r["sizes"], o.sizes)
     with pytest.raises(TypeError):
         gc([torch.zeros(4, dtype=torch.int64, device=DEV)] * n, synth.SAMPLE_SEED)
     with pytest.raises(ValueError):
