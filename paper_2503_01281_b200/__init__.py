@@ -422,7 +422,9 @@ class GroupCall:
     """dci_sample_gather_many with its fixed arguments (workspaces, outputs, fan-outs) marshalled
     once: each call passes only the n seed tensors, so a group's host enqueue -- which every timed
     region waits on before the group's first kernel -- costs a few microseconds of Python instead
-    of rebuilding four ctypes arrays.  Holds references to the workspaces and outputs."""
+    of rebuilding four ctypes arrays.  Holds references to the workspaces and outputs.  One
+    GroupCall is not for concurrent use from several host threads (its argument arrays are
+    reused); the library has copied them when a call returns."""
 
     def __init__(self, ctx: Context, wss, fanouts, outs):
         if len(wss) != len(outs):
@@ -455,7 +457,9 @@ class GroupCall:
 
     def host(self, seeds_host_list, seed: int, results_host=None, stream=None):
         """The dci_sample_gather_many_host form: pinned host seed tensors in, every batch's
-        sizes / counters / status back in one copy into results_host (see result_buffer)."""
+        sizes / counters / status back in one copy into results_host (see result_buffer).  The
+        copies are asynchronous: keep the seed tensors and results_host alive, and read the
+        results, after synchronising `stream`."""
         import torch
         if len(seeds_host_list) != self.n:
             raise ValueError(f"expected {self.n} seed tensors")
