@@ -8,7 +8,8 @@ or no CUDA device is present, the compute calls raise.
 
 Names follow the C ABI: ``load_graph``, ``presample``, ``allocate``, ``fill``,
 ``sample_gather`` (+ ``sample_gather_host``), ``output_bounds``, ``workspace_create``,
-``cache_state``, ``cache_info``.
+``cache_state``, ``cache_info``; ``GroupCall`` is ``dci_sample_gather_many`` with its fixed
+arguments marshalled once.
 """
 from __future__ import annotations
 
