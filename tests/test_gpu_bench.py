@@ -87,6 +87,18 @@ def test_bench_spawns_ranks_for_gpus_n(scaling):
     assert len(d["clocks"]["per_rank"]) == 2
 
 
+def test_bench_single_rank_adopted_shm_graph():
+    """`--shm-graph on` with one rank: the graph is generated into /dev/shm and adopted in place
+    (DCI_ADOPT_HOST); the timed call is bit-exact against the oracle, whose leg reads its features
+    from the shared graph, and the line reports the adopted host graph and the rank's memory."""
+    d = run_bench("--config", "M1", "--steps", "20", "--warmup", "4", "--repeats", "1", "--cpu-seconds", "2",
+                  "--shm-graph", "on")
+    check_common(d, 20, 4)
+    assert d["config"]["host_graph"] == "node-shared (adopted)"
+    assert d["parity_check"]["bit_exact"] is True
+    assert d["cpu_baseline"]["value"] > 0 and d["host_memory"]["rss_anon_GB"] > 0
+
+
 def test_bench_m4s_hashed_tables_light_parity():
     """Hashed position tables at scale (S6): the papers100M-shaped graph at 1/10
     scale (11.1 M nodes, 161.6 M edges, 25 % budget, host-resident misses, groups of 8) with the
