@@ -423,6 +423,13 @@ def run_ours(args):
     cfg = _cfg(args)
     B, fan, L = cfg.batch, cfg.fanouts, len(cfg.fanouts)
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
+    # measured defaults: groups of 20 everywhere -- node sweeps read each feature row
+    # (HBM hit or host miss) once per group: M2 11 M seeds/s, M3 2.6 -> 4.0 M, M4s 0.40 -> 0.91 M.
+    # A sweep probes every node id in dense position tables, so papers100M-shaped M4 (whose tables
+    # would be hashed) asks for dense ones: 8 N = 0.9 GB per workspace, before any is created
+    default_group = {"M1": 20, "M2": 20, "M3": 20, "M4": 20, "M4s": 20, "M5": 20}.get(cfg.name.split("-")[0], 0)
+    if cfg.name.startswith("M4-") and (args.group is None or args.group >= 2):
+        os.environ.setdefault("DCI_TABLE", "dense")
 
     clk = ClockSampler(local)
     clk.start()
@@ -482,9 +489,6 @@ def run_ours(args):
     t_allreduce = time.time() - t2
 
     # ---- inference workspaces and outputs, created BEFORE the (auto) budget is cut (dci.h) ----
-    # measured defaults: groups of 20 on HBM-resident data (node sweeps), groups of 8
-    # on papers100M-shaped host-resident data, one batch per call on products-shaped (400 B rows)
-    default_group = {"M1": 20, "M2": 20, "M4": 8, "M4s": 8}.get(cfg.name.split("-")[0], 0)
     G = max(0, args.group) if args.group is not None else default_group
     nws = max(1, args.inflight) if args.inflight is not None else (2 if G else 6)
     per = max(1, G)  # batches per call

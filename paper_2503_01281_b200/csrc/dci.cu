@@ -852,8 +852,19 @@ dci_status dci_sample_gather_many(dci_ctx* ctx, int32_t n, dci_workspace* const*
     int64_t grow = 1;
     for (int h = 0; h < L; ++h) grow = std::min<int64_t>(ctx->N, grow * (1 + (int64_t)fanouts[h]));
     int64_t cover = 0;
-    for (int i = 0; i < n && cover < ctx->N; ++i) cover += std::min<int64_t>(ctx->N, (int64_t)B[i] * grow);
+    for (int i = 0; i < n; ++i) cover += std::min<int64_t>(ctx->N, (int64_t)B[i] * grow);
     sweep = cover >= ctx->N;
+    // host-resident feature rows: the sweep reads each MISS row once per group instead of once per
+    // batch (and each hit row once), at the price of probing n tables for every node id.  Taken
+    // when the host bytes a row-mode gather would move -- the frontier bound x the uncached share
+    // of the rows x the row size, at ~50 GB/s -- exceed twice the probe bytes at ~6 TB/s
+    // (M3 groups of 20 sweep anyway: 2.6 -> 4.0 M seeds/s; papers100M-shaped M4 needs this rule)
+    if (!sweep && ctx->fcache_total_rows < ctx->N) {
+      const double miss = 1.0 - (double)ctx->fcache_total_rows / (double)ctx->N;
+      const double host_s = (double)cover * miss * 4.0 * (double)ctx->pitch / 50e9;
+      const double probe_s = (double)ctx->N * (double)n * 8.0 / 6e12;
+      sweep = host_s > 2.0 * probe_s;
+    }
   }
   // alone: the previous group's gather had already finished when this group was enqueued, so
   // nothing is queued ahead of this group's gather
