@@ -785,6 +785,12 @@ def run_ours(args):
     # Binding resource of the gather kernel: HBM (hit rows read + every row written + 4 B
     # slot lookup) vs the host link (miss rows read through UVA).
     host_peak, _, host_kind = host_link_peaks(cfg.N * 4.0 * cfg.pitch_floats(), 4 * cfg.pitch_floats())
+    if kinds[0] == 0 and kinds[1] + kinds[2] > 0 and os.path.exists(os.path.join(ROOT, "profiles", "hostlink_peaks.json")):
+        # every gather was a node sweep: miss rows are read in ascending node order, not at random,
+        # so the link's streaming read rate bounds them (a random-request rate would be exceeded)
+        host_peak = float(json.load(open(os.path.join(ROOT, "profiles", "hostlink_peaks.json")))["uva_stream_read_GBps"])
+        host_kind = ("measured streaming UVA read rate (tools/probe/hostlink_probe.cu): node-sweep gathers read "
+                     "the miss rows in ascending node order")
     hits_rows, miss_rows = cn[2], cn[3]
     # rows actually read: a node-sweep group reads each row once for all its batches; misses
     # among them are apportioned by the batches' miss fraction
@@ -822,6 +828,8 @@ def run_ours(args):
     B_host = host_rows_read * 4.0 * cfg.pitch_floats() + 32.0 * host_adj_sectors
     region = cfg.N * 4.0 * cfg.pitch_floats() + 4.0 * cfg.E
     bw_host, bw_host_kind = host_read_peak(region)
+    if kinds[0] == 0 and kinds[1] + kinds[2] > 0 and bw_host < host_peak:
+        bw_host, bw_host_kind = host_peak, host_kind  # node sweeps: the streaming read rate (above)
     T_terms = {"hbm_ms": B_hbm / (hbm_peak * 1e9) * 1e3, "host_ms": B_host / (bw_host * 1e9) * 1e3}
     T_roof = max(T_terms.values())
     # Request view (SURVEY §8(d)'s N_req/R_req term, reported beside the byte roofline, not in it):
