@@ -423,11 +423,13 @@ def run_ours(args):
     cfg = _cfg(args)
     B, fan, L = cfg.batch, cfg.fanouts, len(cfg.fanouts)
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
-    # measured defaults: groups of 20 everywhere -- node sweeps read each feature row
-    # (HBM hit or host miss) once per group: M2 11 M seeds/s, M3 2.6 -> 4.0 M, M4s 0.40 -> 0.91 M.
-    # A sweep probes every node id in dense position tables, so papers100M-shaped M4 (whose tables
-    # would be hashed) asks for dense ones: 8 N = 0.9 GB per workspace, before any is created
-    default_group = {"M1": 20, "M2": 20, "M3": 20, "M4": 20, "M4s": 20, "M5": 20}.get(cfg.name.split("-")[0], 0)
+    # measured defaults: node sweeps read each feature row (HBM hit or host miss) once
+    # per group -- groups of 20 on HBM-resident data (M1, M2: the driver's K = 20 is one group), of
+    # 32 (DCI_MAX_GROUP) on host-resident data, where a larger group shares more miss rows (M3
+    # 2.6 -> 4.7 M seeds/s, M4s 0.40 -> 1.08 M, M4 0.15 -> 0.36 M at K = 64).  A sweep probes every
+    # node id in dense position tables, so papers100M-shaped M4 (whose tables would be hashed) asks
+    # for dense ones: 8 N = 0.9 GB per workspace, before any is created
+    default_group = {"M1": 20, "M2": 20, "M3": 32, "M4": 32, "M4s": 32, "M5": 32}.get(cfg.name.split("-")[0], 0)
     if cfg.name.startswith("M4-") and (args.group is None or args.group >= 2):
         os.environ.setdefault("DCI_TABLE", "dense")
 
