@@ -54,6 +54,9 @@ def parse():
                          "slower, tools/probe/scatter_probe.cu); auto = line when it adds <= 32 B per row")
     ap.add_argument("--repeats", type=int, default=5, help="timed regions of K steps (value = median)")
     ap.add_argument("--ratio", type=float, default=None, help="explicit C_adj/C split (sweeps)")
+    ap.add_argument("--eq1-times", default="group", choices=["presample", "group"],
+                    help="Eq. 1's T_sample / T_feature: dci_presample's per-batch stage times, or the "
+                         "presample batches run as inference groups")
     ap.add_argument("--budget", default=None, help="override the config's budget (bytes:<n>|frac:<x>|auto)")
     ap.add_argument("--fanouts", default=None, help="override the config's fan-outs, e.g. 15,10,5 (DGL order)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch size")
@@ -500,6 +503,25 @@ def run_ours(args):
     ldx = ldx_line if line else None
     outs = [[dci.BatchOut(ctx, B, fan, ldx=ldx) for _ in range(per)] for _ in range(nws)]
 
+    # ---- Eq. 1 inputs measured the way inference runs (--eq1-times group): the presample batches
+    # once more through dci_sample_gather_many in groups (no caches yet, as in the presample), their
+    # sampling / gather stage times (CUDA events) replacing the per-batch ones of dci_presample ----
+    eq1_src = "presample (per batch)"
+    if args.eq1_times == "group" and G >= 2 and world == 1:
+        for w in wss[0]:
+            w.set_profiling(True)
+            w.stats(reset=True)
+        torch.cuda.synchronize()
+        for start in range(0, npre, per):
+            chunk = pre_batches[start:start + per]
+            dci.sample_gather_many(ctx, wss[0][:len(chunk)], chunk, fan, synth.PRESAMPLE_SEED, outs[0][:len(chunk)])
+        torch.cuda.synchronize()
+        gst = [w.stats(reset=True) for w in wss[0]]
+        S = int(sum(g["sample_ms"] for g in gst) * 1e6)
+        F = int(sum(g["gather_ms"] for g in gst) * 1e6)
+        eq1_src = f"the presample batches as groups of {min(per, npre)} (dci_sample_gather_many stage times)"
+        log(f"[bench] Eq. 1 inputs from group stage times: T_sample {S / 1e6:.2f} ms, T_feature {F / 1e6:.2f} ms")
+
     # ---- S2 allocate (Eq. 1) + S3/S4 fill ----
     t3 = time.time()
     C = synth.parse_budget(args.budget or cfg.budget, synth.data_bytes(cfg.N, cfg.E, cfg.D))
@@ -941,7 +963,7 @@ def run_ours(args):
                                    "note": "presample = the dci_presample calls only (seed lists and count "
                                            "arrays are made before); presample_device_s = sum of the "
                                            "per-batch CUDA-event stage times it reports (Eq. 1 inputs)"},
-                  "c_adj": c_adj, "c_feat": c_feat, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
+                  "c_adj": c_adj, "c_feat": c_feat, "eq1_times": eq1_src, "adj_elems": info["adj_elems"], "feat_rows": info["feat_rows"],
                   "e2e_ms_per_step": ems / steps_eff, "host_enqueue_ms_per_step": host_s * 1e3 / steps_eff},
     }
     def check_batches(nchk=3):
