@@ -82,7 +82,8 @@ struct HopLaunch {
                         // 1 % slower on M2 and 3.6 % on M4s -- lines pinned in L2 crowd out the gather's)
   int32_t* edge_counts; // presample only (nullable, n = 1)
   int32_t precheck;     // read the tag before the atomicMax (DCI_PRECHECK=1; measured slower on M2)
-  int32_t sweep;        // node-sweep sampling allowed (multi-batch hops covering >= N nodes)
+  int32_t sweep;        // node-sweep sampling allowed (multi-batch hops covering >= sweep_min nodes)
+  int64_t sweep_min;    // frontier total from which a hop sweeps (N, or N / 20 with host adjacency)
   int32_t nmask_on;     // a sweeping hop's new-candidate masks come from k_newmask_sweep (DCI_NMASK_SWEEP)
   HopBatch b[DCI_MAX_GROUP];
 };
@@ -335,7 +336,7 @@ __device__ __forceinline__ int32_t select_rank(int gl, int lane, unsigned gmask,
 // k_sample_hop, k_newmask_sweep and k_scan_hop take the same decision from the same inputs (for
 // h >= 1 the batches' status words and frontier sizes no longer change within the hop).
 __device__ __forceinline__ bool hop_sweeps(const HopLaunch& a, long long total, int all_ok) {
-  return a.f >= 3 && a.f <= 32 && a.hop >= 1 && all_ok && a.sweep && a.n >= 2 && total >= a.N &&
+  return a.f >= 3 && a.f <= 32 && a.hop >= 1 && all_ok && a.sweep && a.n >= 2 && total >= a.sweep_min &&
          a.edge_counts == nullptr;
 }
 
@@ -1079,6 +1080,16 @@ static HopLaunch hop_launch(dci_ctx* ctx, dci_workspace* const* ws, const HopPar
     return e ? atoi(e) : 1;
   }();
   a.sweep = sweep;
+  // a hop samples by node sweep once its frontiers together reach N nodes -- or N / 20 when part of
+  // the adjacency lives in host memory: the sweep then also reads each node's host run once per
+  // group, which outweighs probing every node id (M3 4.70 -> 5.13-5.19 M seeds/s, M4s 1.105 ->
+  // 1.165 M; tools/exp/r3ll.sh).  DCI_SWEEP_FACTOR overrides the factor.
+  static const double sweep_factor = [] {
+    const char* e = getenv("DCI_SWEEP_FACTOR");
+    return e ? atof(e) : -1.0;
+  }();
+  const double factor = sweep_factor >= 0 ? sweep_factor : (ctx->whole_fit ? 1.0 : 0.05);
+  a.sweep_min = std::max<int64_t>(1, (int64_t)((double)ctx->N * factor));
   for (int i = 0; i < n; ++i)
     if (ws[i]->hmask) a.sweep = 0;  // the node sweep probes every node id: dense tables only
   static const int nmask_on = [] {
@@ -1177,7 +1188,7 @@ void launch_newmask_sweep(dci_ctx* ctx, dci_workspace* const* ws, const HopParam
   // kernel would exit at once), so nothing is launched
   int64_t cap = 0;
   for (int i = 0; i < n; ++i) cap += ws[i]->hop_cap[p[i].hop];
-  if (cap < ctx->N) return;
+  if (cap < a.sweep_min) return;
   const int64_t grid = std::min<int64_t>(persistent_grid(ctx, k_newmask_sweep, 256, 8), (ctx->N + 255) / 256);
   k_newmask_sweep<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, s>>>(a);
   ++ctx->launches;
