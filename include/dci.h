@@ -153,9 +153,13 @@ dci_status dci_sample_gather(dci_ctx* ctx, dci_workspace* ws, const int32_t* see
  * (one hop / scan launch per hop for the whole group, captured once as a CUDA graph on ws[0]);
  * then ONE feature-gather launch (Blackwell bulk copies, cp.async.bulk, through a shared-memory
  * ring) moves the rows of every batch on the context's gather stream, so group gathers run one at
- * a time while the next group samples.  When 2..32 batches together hold at least N rows, the
- * gather sweeps node ids and reads each feature row ONCE for all batches holding it (P:170's
- * hit/miss sources unchanged).  Results are identical to n dci_sample_gather calls (O-6, O-7;
+ * a time while the next group samples.  When 2..32 batches together hold at least N rows -- or
+ * part of the features live in host memory and the host bytes a row-by-row gather would move
+ * outweigh probing every node id -- the gather sweeps node ids and reads each feature row ONCE
+ * for all batches holding it, in node order (P:170's hit/miss sources unchanged).  Likewise a hop
+ * samples by node sweep once its frontiers reach N nodes (N / 20 when part of the adjacency is
+ * host-resident).  Sweeps need dense position tables (8 N bytes per workspace; DCI_TABLE=dense
+ * forces them for large graphs).  Results are identical to n dci_sample_gather calls (O-6, O-7;
  * the draws do not depend on the batch, C4).  Asynchronous on `stream`: work enqueued on `stream`
  * before the call happens before the group, and work enqueued after it sees every output; issue
  * a workspace's groups in order on one stream, and a context's groups from one host thread (they
